@@ -1,0 +1,215 @@
+/*
+ * dreg_cuda.h -- C ABI of the B200-native accelerated-ADMM registration path.
+ *
+ * This is the drop-in boundary for the reference `dreg` hot path
+ * (arXiv 2109.12688; reference C++ library at proj/core).  The reference exposes a
+ * C++ value-semantics API (`dreg::solve_velocity`, `dreg::register_pair`, ...);
+ * this header is the thin `extern "C"` layer underneath the C++ mirror in
+ * include/dreg_b200.hpp, so any FFI (ctypes, cgo, JNI, N-API) can bind it.
+ *
+ * Conventions (identical to the reference):
+ *   - grids are x-fastest, index = x + M*(y + N*z)   (volume.hpp:10-21)
+ *   - vector fields on HOST buffers are interleaved AoS (vx,vy,vz) per voxel
+ *     (volume.hpp:70-94); device-resident buffers are SoA planes [3][voxels]
+ *   - displacements are in voxel units; phi(x) = x + disp(x)   (volume.hpp:96-101)
+ *
+ * Status codes (no exceptions cross the ABI; the C++ mirror rethrows):
+ *   DREG_OK 0, DREG_INVALID_ARGUMENT 2  -> std::invalid_argument
+ *             DREG_NUMERIC 4            -> dreg::numeric_error   (errors.hpp:15-17)
+ *             DREG_RUNTIME 5            -> std::runtime_error (CUDA / allocation)
+ *
+ * A context is bound to one CUDA device, owns all device buffers (reused across
+ * calls) and is not thread-safe: use one context per host thread / GPU.  There is
+ * no CPU fallback: every compute entry point runs sm_100a kernels and returns
+ * DREG_RUNTIME when no usable device exists.
+ */
+#ifndef DREG_CUDA_H
+#define DREG_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DREG_OK 0
+#define DREG_INVALID_ARGUMENT 2
+#define DREG_NUMERIC 4
+#define DREG_RUNTIME 5
+
+#define DREG_MAX_LEVELS 8
+#define DREG_MAX_WARPS 64
+
+#define DREG_PROFILE_CAPPED 0
+#define DREG_PROFILE_CONVERGED 1
+
+/* dreg::Dims3 (volume.hpp:11-21) */
+typedef struct { int x, y, z; } dreg_dims3;
+/* dreg::Spacing3 (volume.hpp:25-30) */
+typedef struct { double x, y, z; } dreg_spacing3;
+
+/* dreg::SolverConfig (admm.hpp:13-23), same fields and meaning.
+ * Defaults (dreg_solver_cfg_default): data_term 1, order 2, lambda 0, theta 0.1,
+ * epsilon 1e-6, max_iters 100, tol 0, accelerate 1, log_objective 1. */
+typedef struct {
+    int data_term;      /* s: 1 = sum of absolute differences, 2 = sum of squares */
+    int order;          /* n: regulariser order, 1..6 */
+    double lambda;      /* >= 0 */
+    double theta;       /* ADMM penalty (north-star "rho"), > 0 */
+    double epsilon;     /* guards |grad|^2 in the s=1 update, > 0 */
+    int max_iters;      /* >= 1 */
+    double tol;         /* stop when mean |v_k - v_{k-1}| <= tol */
+    int accelerate;     /* Nesterov extrapolation of w and b */
+    int log_objective;  /* record the objective per iteration */
+} dreg_solver_cfg;
+
+/* dreg::RegistrationConfig (registration.hpp:16-24). Per-level arrays are indexed
+ * coarsest first; only the first `levels` entries are read. */
+typedef struct {
+    dreg_solver_cfg solver;
+    int levels;
+    int max_warps_per_level[DREG_MAX_LEVELS];
+    int max_admm_iters_per_level[DREG_MAX_LEVELS];
+    double warp_improvement_threshold;
+    int profile;        /* DREG_PROFILE_* */
+    int smooth_levels;
+} dreg_reg_cfg;
+
+/* dreg::SolverDiagnostics (admm.hpp:28-34).  objective / constraint_residual are
+ * caller-owned arrays of at least max_iters entries (nullable). */
+typedef struct {
+    int iterations;
+    double final_change;
+    int converged;
+    double* objective;
+    double* constraint_residual;
+} dreg_solver_diag;
+
+/* dreg::LevelLog (registration.hpp:32-37) with fixed capacity. */
+typedef struct {
+    dreg_dims3 dims;
+    int warps;
+    double mean_sad[DREG_MAX_WARPS + 1];
+    int solver_iterations[DREG_MAX_WARPS];
+} dreg_level_log;
+
+/* dreg::RegistrationResult (registration.hpp:39-45) minus the fields, which are
+ * returned through caller buffers. */
+typedef struct {
+    int status;          /* per-pair DREG_* status */
+    int velocity_count;
+    int levels;
+    dreg_level_log per_level[DREG_MAX_LEVELS];
+    double elapsed_seconds;
+} dreg_pair_result;
+
+/* dreg::JacobianStats (metrics.hpp:44-48) plus the raw counts. */
+typedef struct {
+    double pct_nonpositive;
+    double min_det;
+    int64_t nonpositive;
+    int64_t interior;
+} dreg_jacobian_stats;
+
+typedef struct dreg_cuda_ctx dreg_cuda_ctx;
+
+/* ---- configuration helpers (host only, pure) ---------------------------------- */
+void dreg_solver_cfg_default(dreg_solver_cfg* cfg);
+/* dreg::validate (admm.cpp:174-196): DREG_OK or DREG_INVALID_ARGUMENT */
+int dreg_validate_solver_cfg(const dreg_solver_cfg* cfg);
+/* dreg::make_registration_config (registration.cpp:62-83) */
+int dreg_make_registration_config(int profile, const dreg_solver_cfg* solver, int levels,
+                                  dreg_reg_cfg* out);
+/* dreg::nesterov_next_alpha (admm.cpp:198-200) */
+double dreg_nesterov_next_alpha(double alpha);
+/* dreg::laplacian_symbol (regularizer.cpp:51-79); out has x*y*z doubles */
+int dreg_laplacian_symbol(int order, dreg_dims3 dims, double* out);
+
+/* ---- context ------------------------------------------------------------------ */
+int dreg_cuda_ctx_create(int device, dreg_cuda_ctx** out);
+void dreg_cuda_ctx_destroy(dreg_cuda_ctx* ctx);
+/* Message of the last failing call on this context (never NULL). */
+const char* dreg_cuda_last_error(const dreg_cuda_ctx* ctx);
+/* Work is issued on `stream` (a cudaStream_t; NULL = the context's own stream). */
+int dreg_cuda_set_stream(dreg_cuda_ctx* ctx, void* stream);
+/* Number of kernels this context launched since creation (evidence counter). */
+int64_t dreg_cuda_kernel_launches(const dreg_cuda_ctx* ctx);
+/* Pairs processed concurrently per batch chunk (0 = automatic). */
+int dreg_cuda_set_batch_chunk(dreg_cuda_ctx* ctx, int pairs);
+/* 1 = capture each registration chunk as a CUDA graph (default), 0 = plain launches */
+int dreg_cuda_set_use_graphs(dreg_cuda_ctx* ctx, int enable);
+
+/* ---- hot path: registration (registration.hpp:74-75) ---------------------------
+ * Host buffers.  phi_out: AoS 3*voxels floats (nullable); warped_out: voxels
+ * floats (nullable).  Returns the first failing pair's status. */
+int dreg_cuda_register_pair(dreg_cuda_ctx* ctx, const float* target, const float* source,
+                            dreg_dims3 dims, dreg_spacing3 spacing, const dreg_reg_cfg* cfg,
+                            float* phi_out, float* warped_out, dreg_pair_result* result);
+
+/* n_pairs independent registrations sharing dims and cfg; per-pair host pointers. */
+int dreg_cuda_register_batch(dreg_cuda_ctx* ctx, int n_pairs, const float* const* targets,
+                             const float* const* sources, dreg_dims3 dims,
+                             dreg_spacing3 spacing, const dreg_reg_cfg* cfg,
+                             float* const* phi_out, float* const* warped_out,
+                             dreg_pair_result* results);
+
+/* Device-resident variant: targets_dev / sources_dev are device arrays laid out
+ * [n_pairs][voxels]; phi_dev_out is [n_pairs][3][voxels] SoA (nullable),
+ * warped_dev_out [n_pairs][voxels] (nullable).  No host<->device copies of fields;
+ * results (small per-pair records) are returned on the host. */
+int dreg_cuda_register_batch_device(dreg_cuda_ctx* ctx, int n_pairs, const float* targets_dev,
+                                    const float* sources_dev, dreg_dims3 dims,
+                                    dreg_spacing3 spacing, const dreg_reg_cfg* cfg,
+                                    float* phi_dev_out, float* warped_dev_out,
+                                    dreg_pair_result* results);
+
+/* ---- hot path: one velocity solve (admm.hpp:76-77) ----------------------------- */
+int dreg_cuda_solve_velocity(dreg_cuda_ctx* ctx, const float* target,
+                             const float* warped_source, dreg_dims3 dims,
+                             const dreg_solver_cfg* cfg, float* velocity_out,
+                             dreg_solver_diag* diag);
+
+/* ---- building blocks (host AoS buffers; each a GPU launch) ---------------------- */
+/* v_update_l1 / v_update_l2 (admm.hpp:49-58); data_term selects which */
+int dreg_cuda_v_update(dreg_cuda_ctx* ctx, const float* target, const float* warped_source,
+                       const float* grad, const float* w_hat, const float* b_hat,
+                       dreg_dims3 dims, const dreg_solver_cfg* cfg, float* out);
+/* w_update (admm.hpp:64-65): spectral solve with the order-cfg->order kernel */
+int dreg_cuda_w_update(dreg_cuda_ctx* ctx, const float* v, const float* b_hat,
+                       dreg_dims3 dims, const dreg_solver_cfg* cfg, float* out);
+/* regulariser_energy (regularizer.hpp:45) */
+int dreg_cuda_regulariser_energy(dreg_cuda_ctx* ctx, const float* w, dreg_dims3 dims,
+                                 int order, double* out);
+/* warp_image (volume.hpp:113) */
+int dreg_cuda_warp_image(dreg_cuda_ctx* ctx, const float* img, const float* disp,
+                         dreg_dims3 dims, float* out);
+/* image_gradient (volume.hpp:117) */
+int dreg_cuda_image_gradient(dreg_cuda_ctx* ctx, const float* img, dreg_dims3 dims,
+                             float* out);
+/* compose_deformation (volume.hpp:121) */
+int dreg_cuda_compose_deformation(dreg_cuda_ctx* ctx, const float* disp, const float* v,
+                                  dreg_dims3 dims, float* out);
+/* jacobian_determinant (volume.hpp:125); det_out nullable; stats nullable */
+int dreg_cuda_jacobian(dreg_cuda_ctx* ctx, const float* disp, dreg_dims3 dims,
+                       float* det_out, dreg_jacobian_stats* stats);
+/* normalize_intensity_pair (registration.hpp:65-66) */
+int dreg_cuda_normalize_intensity_pair(dreg_cuda_ctx* ctx, const float* a, const float* b,
+                                       dreg_dims3 dims, float* out_a, float* out_b);
+/* binomial_smooth (registration.hpp:59) */
+int dreg_cuda_binomial_smooth(dreg_cuda_ctx* ctx, const float* img, dreg_dims3 dims,
+                              float* out);
+/* mean_sad (registration.hpp:62) */
+int dreg_cuda_mean_sad(dreg_cuda_ctx* ctx, const float* a, const float* b, dreg_dims3 dims,
+                       double* out);
+/* downsample (registration.hpp:49): out has ceil-half dims */
+int dreg_cuda_downsample(dreg_cuda_ctx* ctx, const float* img, dreg_dims3 dims, float* out);
+/* upsample_velocity (registration.hpp:54): AoS in (src dims) -> AoS out (dst dims) */
+int dreg_cuda_upsample_velocity(dreg_cuda_ctx* ctx, const float* v, dreg_dims3 src_dims,
+                                dreg_dims3 dst_dims, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DREG_CUDA_H */

@@ -1,0 +1,503 @@
+// Accelerated-ADMM inner loop kernels (reference admm.cpp:252-314).
+//
+// One ADMM iteration k is two launches:
+//   xpass(k)  -- per tile of x-lines: c2r of the filtered spectrum -> w_{k-1};
+//                dual update b_{k-1} (admm.cpp:142-153); constraint residual
+//                (:163-170); Nesterov extrapolation of w and b (:130-139, :294-297);
+//                closed-form v-update (:23-63); change norm (:155-161);
+//                u_k = v_k + b_hat_k; r2c along x -> spectrum (plane-major).
+//   plane(k)  -- per (component, x-frequency) plane: y/z DIF FFT, multiply by
+//                theta / (lambda K_n + theta) / N (:83-95, regularizer.cpp:51-79),
+//                y/z inverse.
+// so the spectrum makes exactly one HBM round trip between launches and every
+// real-space field is touched once per iteration.
+#include "fft_device.cuh"
+#include "kernels.cuh"
+#include "launch.h"
+#include "pointwise.cuh"
+
+namespace dregb {
+
+constexpr int kXThreads = 256;
+constexpr int kPThreads = 512;
+
+struct XSmem {
+    float2* twx;
+    float2* xtw;
+    int* xpos;
+    float2* buf;
+    float2* Xs;
+    double* red;
+};
+
+__device__ __forceinline__ XSmem carve_x(unsigned char* smem, int L, int hx, int TL, int PM) {
+    XSmem s;
+    size_t off = 0;
+    s.twx = reinterpret_cast<float2*>(smem + off);
+    off += sizeof(float2) * L;
+    s.xtw = reinterpret_cast<float2*>(smem + off);
+    off += sizeof(float2) * (hx + 1);
+    s.buf = reinterpret_cast<float2*>(smem + off);
+    off += sizeof(float2) * 3 * TL * PM;
+    s.Xs = reinterpret_cast<float2*>(smem + off);
+    off += sizeof(float2) * hx * TL;
+    s.red = reinterpret_cast<double*>(smem + off);
+    off += sizeof(double) * 32;
+    s.xpos = reinterpret_cast<int*>(smem + off);
+    return s;
+}
+
+size_t xpass_smem_bytes(int L, int hx, int TL, int PM) {
+    return sizeof(float2) * (L + hx + 1 + 3 * (size_t)TL * PM + (size_t)hx * TL) + sizeof(double) * 32 +
+           sizeof(int) * L;
+}
+
+template <int VEC>
+__device__ __forceinline__ void ldv(const float* p, float* out) {
+    if constexpr (VEC == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        out[0] = t.x; out[1] = t.y; out[2] = t.z; out[3] = t.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) out[j] = p[j];
+    }
+}
+template <int VEC>
+__device__ __forceinline__ void stv(float* p, const float* in) {
+    if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) p[j] = in[j];
+    }
+}
+
+template <int MODE, int DT, int VEC>
+__global__ void __launch_bounds__(kXThreads) xpass_kernel(XArgs a) {
+    const int pair = blockIdx.y;
+    PairState* st = a.F.st + pair;
+    if (!st->active || st->status) return;
+    constexpr bool UTIL = (MODE == X_FWD || MODE == X_INV);
+    if (MODE <= X_GENERAL && st->solve_done) return;
+    if (UTIL && st->solve_done && a.k > st->done_iter) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int L = a.px.n, M = a.F.M, hx = a.F.hx, TL = a.TL, PM = a.PM;
+    XSmem sm = carve_x(smem, L, hx, TL, PM);
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const long long lines = a.F.lines;
+    const long long L0 = (long long)blockIdx.x * TL;
+    const int nl = (int)min((long long)TL, lines - L0);
+    const long long N = a.F.N;
+
+    for (int i = tid; i < L; i += nthr) {
+        sm.twx[i] = a.twx[i];
+        sm.xpos[i] = a.xpos[i];
+    }
+    for (int i = tid; i <= hx; i += nthr) sm.xtw[i] = a.xtw[i];
+    __syncthreads();
+
+    float* V = a.F.V + (size_t)pair * 3 * N;
+    float* BH = a.F.BH + (size_t)pair * 3 * N;
+    float* WP = a.F.WP + (size_t)pair * 3 * N;
+    float* BP = a.F.BP + (size_t)pair * 3 * N;
+    const float* G = a.F.G + (size_t)pair * 3 * N;
+    const float* Dd = a.F.D + (size_t)pair * N;
+    float2* S = a.F.S + (size_t)pair * 3 * hx * lines;
+
+    // ---- phase 1: x c2r of the filtered spectrum -> w_{k-1} (real, in smem) ----
+    if (MODE != X_FIRST && MODE != X_FWD) {
+        for (int c = 0; c < 3; ++c) {
+            const float2* Sc = S + (size_t)c * hx * lines;
+            for (int idx = tid; idx < hx * TL; idx += nthr) {
+                const int p = idx / TL, l = idx - p * TL;
+                sm.Xs[idx] = l < nl ? Sc[(size_t)p * lines + L0 + l] : make_float2(0.f, 0.f);
+            }
+            __syncthreads();
+            float2* bc = sm.buf + (size_t)c * TL * PM;
+            if (!a.odd) {
+                // Z'[k] = E + i O with E = X[k] + conj(X[L-k]), O = (X[k] - conj(X[L-k])) W_M^{-k};
+                // imaginary parts of the self-conjugate bins ignored (1-D c2r semantics).
+                for (int idx = tid; idx < L * TL; idx += nthr) {
+                    const int k = idx / TL, l = idx - k * TL;
+                    float2 A = sm.Xs[k * TL + l];
+                    float2 B = sm.Xs[(L - k) * TL + l];
+                    if (k == 0) { A.y = 0.f; B.y = 0.f; }
+                    B.y = -B.y;
+                    const float2 e = cadd(A, B);
+                    const float2 o = cmulc(csub(A, B), sm.xtw[k]);
+                    bc[l * PM + sm.xpos[k]] = make_float2(e.x - o.y, e.y + o.x);
+                }
+            } else {
+                for (int idx = tid; idx < M * TL; idx += nthr) {
+                    const int k = idx / TL, l = idx - k * TL;
+                    float2 X;
+                    if (k < hx) {
+                        X = sm.Xs[k * TL + l];
+                        if (k == 0) X.y = 0.f;
+                    } else {
+                        X = cconj(sm.Xs[(M - k) * TL + l]);
+                    }
+                    bc[l * PM + sm.xpos[k]] = X;
+                }
+            }
+            __syncthreads();
+        }
+        fft_lines<true>(sm.buf, 3 * TL, PM, 1, a.px, sm.twx, tid, nthr);
+    }
+
+    if constexpr (UTIL) {
+        const size_t base = (size_t)L0 * M;
+        const int nvox = nl * M;
+        for (int i = tid; i < 3 * nvox; i += nthr) {
+            const int c = i / nvox, r = i - c * nvox;
+            const int l = r / M, x = r - l * M;
+            float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+            const size_t gi = (size_t)c * N + base + r;
+            if (MODE == X_FWD) {
+                const float u = a.add_bh ? V[gi] + BH[gi] : V[gi];
+                if (!a.odd) reinterpret_cast<float*>(bl)[x] = u;
+                else bl[x] = make_float2(u, 0.f);
+            } else {
+                WP[gi] = !a.odd ? reinterpret_cast<const float*>(bl)[x] : bl[x].x;
+            }
+        }
+        if (MODE == X_INV) return;
+    }
+
+    // ---- phase 2: point-wise ADMM updates on the tile ----
+    const double theta = a.sp.theta, inv_theta = 1.0 / a.sp.theta, eps = a.sp.epsilon;
+    const double coef = a.coef;
+    const bool accel = a.sp.accelerate != 0;
+    double s_change = 0.0, s_res = 0.0, s_obj = 0.0;
+    const size_t base = (size_t)L0 * M;
+    const int nvox = nl * M;
+    for (int i0 = tid * VEC; i0 < (UTIL ? 0 : nvox); i0 += nthr * VEC) {
+        const int l = i0 / M, x0 = i0 - l * M;
+        const size_t gi = base + i0;
+        float w[3][VEC], vp[3][VEC];
+        if (MODE != X_FIRST) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+                if (!a.odd) {
+                    const float* wl = reinterpret_cast<const float*>(bl);
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) w[c][j] = wl[x0 + j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) w[c][j] = bl[x0 + j].x;
+                }
+                ldv<VEC>(V + (size_t)c * N + gi, vp[c]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) vp[c][j] = 0.f;
+        }
+        if (MODE == X_TAIL) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    const double dd = (double)vp[c][j] - (double)w[c][j];
+                    s_res += dd * dd;
+                }
+            continue;
+        }
+        float wh[3][VEC], bh[3][VEC];
+        if (MODE == X_FIRST) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) { wh[c][j] = 0.f; bh[c][j] = 0.f; }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float bo[VEC];
+                if (MODE == X_GENERAL) ldv<VEC>(BH + (size_t)c * N + gi, bo);
+                else {
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) bo[j] = 0.f;
+                }
+                float b[VEC];
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    // dual_update: b = b_hat + v - w  (admm.cpp:142-153)
+                    b[j] = (float)((double)bo[j] + (double)vp[c][j] - (double)w[c][j]);
+                    const double dd = (double)vp[c][j] - (double)w[c][j];
+                    s_res += dd * dd;
+                }
+                if (accel && MODE == X_GENERAL) {
+                    float wp[VEC], bp[VEC];
+                    ldv<VEC>(WP + (size_t)c * N + gi, wp);
+                    ldv<VEC>(BP + (size_t)c * N + gi, bp);
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) {
+                        const double aw = w[c][j], ab = b[j];
+                        wh[c][j] = (float)(aw + coef * (aw - (double)wp[j]));
+                        bh[c][j] = (float)(ab + coef * (ab - (double)bp[j]));
+                    }
+                } else {
+                    // coefficient is exactly 0 (first step, or accelerate off)
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) { wh[c][j] = w[c][j]; bh[c][j] = b[j]; }
+                }
+                if (accel) {
+                    stv<VEC>(WP + (size_t)c * N + gi, w[c]);
+                    stv<VEC>(BP + (size_t)c * N + gi, b);
+                }
+            }
+        }
+        float g[3][VEC], dv[VEC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ldv<VEC>(G + (size_t)c * N + gi, g[c]);
+        ldv<VEC>(Dd + gi, dv);
+        float vn[3][VEC];
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+            const float whj[3] = {wh[0][j], wh[1][j], wh[2][j]};
+            const float bhj[3] = {bh[0][j], bh[1][j], bh[2][j]};
+            const float gj[3] = {g[0][j], g[1][j], g[2][j]};
+            float vj[3];
+            v_update_voxel<DT>(whj, bhj, gj, (double)dv[j], theta, inv_theta, eps, vj);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                vn[c][j] = vj[c];
+                s_change += fabs((double)vj[c] - (double)vp[c][j]);
+            }
+            if (a.sp.log_objective) {
+                const double rho = ((double)gj[0] * vj[0] + (double)gj[1] * vj[1] + (double)gj[2] * vj[2]) +
+                                   (double)dv[j];
+                s_obj += DT == 1 ? fabs(rho) : 0.5 * rho * rho;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            stv<VEC>(V + (size_t)c * N + gi, vn[c]);
+            if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bh[c]);
+            float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+            if (!a.odd) {
+                float* ul = reinterpret_cast<float*>(bl);
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) ul[x0 + j] = vn[c][j] + bh[c][j];
+            } else {
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) bl[x0 + j] = make_float2(vn[c][j] + bh[c][j], 0.f);
+            }
+        }
+    }
+
+    // ---- phase 3: r2c along x of u_k, scatter to the plane-major spectrum ----
+    if (MODE != X_TAIL) {
+        if (nl < TL) {  // zero the unused lines so the batched FFT stays finite
+            for (int idx = tid; idx < 3 * TL * PM; idx += nthr) {
+                const int l = (idx / PM) % TL;
+                if (l >= nl) sm.buf[idx] = make_float2(0.f, 0.f);
+            }
+        }
+        __syncthreads();
+        fft_lines<false>(sm.buf, 3 * TL, PM, 1, a.px, sm.twx, tid, nthr);
+        for (int idx = tid; idx < 3 * hx * TL; idx += nthr) {
+            const int c = idx / (hx * TL);
+            const int rem = idx - c * hx * TL;
+            const int k = rem / TL, l = rem - k * TL;
+            if (l >= nl) continue;
+            const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+            float2 X;
+            if (!a.odd) {
+                const float2 zk = bl[sm.xpos[k % L]];
+                const float2 zc = cconj(bl[sm.xpos[(L - k) % L]]);
+                const float2 e = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
+                const float2 o = make_float2(0.5f * (zk.y - zc.y), -0.5f * (zk.x - zc.x));
+                X = cadd(e, cmul(sm.xtw[k], o));
+            } else {
+                X = bl[sm.xpos[k]];
+            }
+            S[((size_t)c * hx + k) * lines + L0 + l] = X;
+        }
+    }
+
+    if constexpr (UTIL) return;
+
+    // ---- deterministic reductions + per-iteration bookkeeping ----
+    const double tc = block_sum<kXThreads>(s_change, sm.red);
+    const double tr = block_sum<kXThreads>(s_res, sm.red);
+    const double to = block_sum<kXThreads>(s_obj, sm.red);
+    if (tid == 0) {
+        double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
+        part[blockIdx.x] = tc;
+        part[kMaxPartials + blockIdx.x] = tr;
+        part[2 * kMaxPartials + blockIdx.x] = to;
+        if (last_block_ticket(&st->counter, gridDim.x)) {
+            double sc = 0.0, sr = 0.0, so = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                sc += part[b];
+                sr += part[kMaxPartials + b];
+                so += part[2 * kMaxPartials + b];
+            }
+            double* dg = a.F.diag ? a.F.diag + (size_t)pair * a.F.diag_stride * 3 : nullptr;
+            if (MODE == X_TAIL) {
+                const int it = st->iterations;
+                if (dg && it >= 1) dg[(it - 1) * 3 + 1] = sqrt(sr);
+            } else {
+                const double change = sc / (3.0 * (double)N);
+                if (dg) {
+                    dg[a.k * 3 + 0] = change;
+                    if (a.k >= 1) dg[(a.k - 1) * 3 + 1] = sqrt(sr);
+                    dg[a.k * 3 + 2] = so;
+                }
+                st->iterations = a.k + 1;
+                st->final_change = change;
+                if (change <= a.sp.tol) {
+                    st->solve_done = 1;
+                    st->done_iter = a.k;
+                }
+            }
+        }
+    }
+}
+
+// ---- yz plane kernel ----------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kPThreads) plane_kernel(PArgs a) {
+    const int pair = blockIdx.y;
+    PairState* st = a.F.st + pair;
+    if (!st->active || st->status) return;
+    if (st->solve_done && (!a.need_tail || a.k > st->done_iter)) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int Ny = a.F.Ny, Nz = a.F.Nz, PY = a.PY, hx = a.F.hx;
+    float2* plane = reinterpret_cast<float2*>(smem);
+    float2* twy = plane + (size_t)PY * Nz;
+    float2* twz = twy + Ny;
+    float* sy = reinterpret_cast<float*>(twz + Nz);
+    float* sz = sy + Ny;
+    double* red = reinterpret_cast<double*>(sy + Ny + Nz + ((Ny + Nz) & 1));
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
+    const long long lines = a.F.lines;
+    float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * lines;
+
+    for (int i = tid; i < Ny; i += nthr) {
+        twy[i] = a.twy[i];
+        sy[i] = a.sy[i];
+    }
+    for (int i = tid; i < Nz; i += nthr) {
+        twz[i] = a.twz[i];
+        sz[i] = a.sz[i];
+    }
+    if ((Ny & 1) == 0) {
+        // rows of even length: move 2 complex per 16-byte access
+        const int half = Ny / 2;
+        for (int idx = tid; idx < half * Nz; idx += nthr) {
+            const int z = idx / half, y2 = idx - z * half;
+            const float4 t = *reinterpret_cast<const float4*>(Sp + (size_t)z * Ny + 2 * y2);
+            plane[z * PY + 2 * y2] = make_float2(t.x, t.y);
+            plane[z * PY + 2 * y2 + 1] = make_float2(t.z, t.w);
+        }
+    } else {
+        for (int idx = tid; idx < Ny * Nz; idx += nthr) {
+            const int z = idx / Ny, y = idx - z * Ny;
+            plane[z * PY + y] = Sp[idx];
+        }
+    }
+    __syncthreads();
+    fft_lines<false>(plane, Nz, PY, 1, a.py, twy, tid, nthr);  // y lines (rows)
+    fft_lines<false>(plane, Ny, 1, PY, a.pz, twz, tid, nthr);  // z lines (columns)
+
+    const float sxp = a.sx[p];
+    if (MODE == 0) {
+        // w-update multiplier theta/(lambda K + theta)/N (admm.cpp:92)
+        for (int idx = tid; idx < Ny * Nz; idx += nthr) {
+            const int z = idx / Ny, y = idx - z * Ny;
+            const float base = 2.0f * (sxp + sy[y] + sz[z]);
+            float K = base;
+            for (int e = 1; e < a.order; ++e) K *= base;
+            const float m = a.scale / (a.lambda * K + a.theta);
+            float2 v = plane[z * PY + y];
+            plane[z * PY + y] = make_float2(v.x * m, v.y * m);
+        }
+        __syncthreads();
+        fft_lines<true>(plane, Ny, 1, PY, a.pz, twz, tid, nthr);
+        fft_lines<true>(plane, Nz, PY, 1, a.py, twy, tid, nthr);
+        if ((Ny & 1) == 0) {
+            const int half = Ny / 2;
+            for (int idx = tid; idx < half * Nz; idx += nthr) {
+                const int z = idx / half, y2 = idx - z * half;
+                const float2 u0 = plane[z * PY + 2 * y2], u1 = plane[z * PY + 2 * y2 + 1];
+                *reinterpret_cast<float4*>(Sp + (size_t)z * Ny + 2 * y2) = make_float4(u0.x, u0.y, u1.x, u1.y);
+            }
+        } else {
+            for (int idx = tid; idx < Ny * Nz; idx += nthr) {
+                const int z = idx / Ny, y = idx - z * Ny;
+                Sp[idx] = plane[z * PY + y];
+            }
+        }
+    } else {
+        // spectral energy (admm.cpp:103-127): sum w_p K |X|^2, w_p = 1 on self-conjugate x bins
+        double acc = 0.0;
+        for (int idx = tid; idx < Ny * Nz; idx += nthr) {
+            const int z = idx / Ny, y = idx - z * Ny;
+            const double base = 2.0 * ((double)sxp + (double)sy[y] + (double)sz[z]);
+            double K = base;
+            for (int e = 1; e < a.order; ++e) K *= base;
+            const float2 v = plane[z * PY + y];
+            acc += K * ((double)v.x * v.x + (double)v.y * v.y);
+        }
+        const bool self_conj = (p == 0) || (2 * p == a.F.M);
+        const double tot = block_sum<kPThreads>(acc, red) * (self_conj ? 1.0 : 2.0);
+        if (tid == 0) {
+            double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
+            part[blockIdx.x] = tot;
+            if (last_block_ticket(&st->counter, gridDim.x)) {
+                double s = 0.0;
+                for (unsigned b = 0; b < gridDim.x; ++b) s += part[b];
+                a.energy_out[pair] = 0.5 * s / (double)a.F.N;
+            }
+        }
+    }
+}
+
+// ---- host launchers -----------------------------------------------------------
+template <int MODE>
+static cudaError_t launch_x_mode(const XArgs& a, int npairs, cudaStream_t s, int data_term, bool vec4) {
+    const dim3 grid((unsigned)((a.F.lines + a.TL - 1) / a.TL), (unsigned)npairs);
+    const size_t smem = xpass_smem_bytes(a.px.n, a.F.hx, a.TL, a.PM);
+    void (*k)(XArgs);
+    if (data_term == 1) k = vec4 ? xpass_kernel<MODE, 1, 4> : xpass_kernel<MODE, 1, 1>;
+    else k = vec4 ? xpass_kernel<MODE, 2, 4> : xpass_kernel<MODE, 2, 1>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kXThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s) {
+    const bool vec4 = (a.F.M % 4) == 0;
+    switch (mode) {
+        case X_FIRST: return launch_x_mode<X_FIRST>(a, npairs, s, a.sp.data_term, vec4);
+        case X_SECOND: return launch_x_mode<X_SECOND>(a, npairs, s, a.sp.data_term, vec4);
+        case X_GENERAL: return launch_x_mode<X_GENERAL>(a, npairs, s, a.sp.data_term, vec4);
+        case X_TAIL: return launch_x_mode<X_TAIL>(a, npairs, s, a.sp.data_term, vec4);
+        case X_FWD: return launch_x_mode<X_FWD>(a, npairs, s, 2, false);
+        default: return launch_x_mode<X_INV>(a, npairs, s, 2, false);
+    }
+}
+
+size_t plane_smem_bytes(int Ny, int Nz, int PY) {
+    return sizeof(float2) * ((size_t)PY * Nz + Ny + Nz) + sizeof(float) * (Ny + Nz + 2) + sizeof(double) * 32 + 16;
+}
+
+cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s) {
+    const dim3 grid((unsigned)(3 * a.F.hx), (unsigned)npairs);
+    const size_t smem = plane_smem_bytes(a.F.Ny, a.F.Nz, a.PY);
+    void (*k)(PArgs) = mode == 0 ? plane_kernel<0> : plane_kernel<1>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kPThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace dregb

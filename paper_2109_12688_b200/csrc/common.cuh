@@ -1,0 +1,104 @@
+// Shared device helpers for the dreg B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dreg_cuda.h"
+
+namespace dregb {
+
+constexpr int kMaxStages = 12;      // radix stages per line FFT
+constexpr int kMaxRadix = 64;       // largest prime factor handled by the generic butterfly
+constexpr int kMaxPartials = 4096;  // per-pair partial-sum slots per reduction
+
+// Per-axis line-FFT plan (host-built, passed by value).  Stage s of the DIF
+// forward transform uses radix[s] on sub-blocks of n1[s]*radix[s] elements;
+// twiddle W_{n_s}^{j1 k} = W_n^{j1 k tws[s]} is read from the axis table.
+struct AxisPlan {
+    int n;
+    int nst;
+    int radix[kMaxStages];
+    int n1[kMaxStages];
+    int tws[kMaxStages];
+};
+
+// Per-pair device state driving the warp loop of register_pair
+// (registration.cpp:245-271) without host synchronisation.
+struct PairState {
+    int active;          // level still iterating warps
+    int cur;             // accepted phi / warped buffer index
+    int solve_done;      // current solve met tol (admm.cpp:304-307)
+    int iterations;      // iterations of the current solve
+    int status;          // DREG_OK / DREG_NUMERIC
+    int velocity_count;  // registration.hpp:42
+    int warps;           // accepted warps at the current level
+    int level;
+    unsigned int counter;  // last-block reduction ticket
+    int done_iter;         // iteration at which solve_done was raised
+    double sad_prev;
+    double final_change;
+    float lo, hi;          // shared intensity range (registration.cpp:157-166)
+    int solver_iterations[DREG_MAX_LEVELS][DREG_MAX_WARPS];
+    double mean_sad[DREG_MAX_LEVELS][DREG_MAX_WARPS + 1];
+    int level_warps[DREG_MAX_LEVELS];
+};
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+
+// Deterministic block reduction of doubles (fixed tree order).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) s += red[w];
+    }
+    return s;  // valid in thread 0
+}
+
+template <int NT>
+__device__ __forceinline__ double block_min(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_down_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double s = 1.0e300;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) s = fmin(s, red[w]);
+    }
+    return s;
+}
+
+// Last-block ticket: returns true in thread 0 of the block that finishes last
+// among `nblocks` (per pair).  Callers then reduce the partials in fixed order,
+// which keeps every reduction run-to-run bit-deterministic.
+__device__ __forceinline__ bool last_block_ticket(unsigned int* counter, unsigned int nblocks) {
+    __threadfence();
+    const unsigned int t = atomicAdd(counter, 1u);
+    const bool last = (t == nblocks - 1);
+    if (last) {
+        *counter = 0u;
+        __threadfence();
+    }
+    return last;
+}
+
+}  // namespace dregb

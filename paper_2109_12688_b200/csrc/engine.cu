@@ -1,0 +1,1174 @@
+// Host engine + C ABI (include/dreg_cuda.h) for the B200 registration path.
+//
+// Owns device workspaces (one per grid size, reused across calls), builds the
+// per-axis FFT plans and their device tables, issues the registration launch
+// sequence -- captured once into a CUDA graph per (workspace, config) and replayed
+// -- and converts between the reference's AoS host layout and the device SoA one.
+// No compute happens on the host: every numerical step is an sm_100a kernel.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "dreg_cuda.h"
+#include "launch.h"
+
+using namespace dregb;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+struct Status {
+    int code = DREG_OK;
+    std::string msg;
+};
+
+#define CK(expr)                                                                     \
+    do {                                                                             \
+        cudaError_t _e = (expr);                                                     \
+        if (_e != cudaSuccess)                                                       \
+            throw CudaFail(std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+    } while (0)
+
+struct CudaFail {
+    std::string msg;
+    explicit CudaFail(std::string m) : msg(std::move(m)) {}
+};
+struct ArgFail {
+    std::string msg;
+    explicit ArgFail(std::string m) : msg(std::move(m)) {}
+};
+struct NumFail {
+    std::string msg;
+    explicit NumFail(std::string m) : msg(std::move(m)) {}
+};
+
+template <class T>
+struct DevArray {
+    T* p = nullptr;
+    size_t n = 0;
+    DevArray() = default;
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    ~DevArray() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t count) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = count;
+        if (count) CK(cudaMalloc(&p, sizeof(T) * count));
+    }
+};
+
+// ---- line FFT plan (host) ------------------------------------------------------
+AxisPlan make_plan(int n) {
+    AxisPlan P{};
+    P.n = n;
+    int rem = n, s = 0;
+    while (rem > 1) {
+        int r;
+        if (rem % 8 == 0) r = 8;
+        else if (rem % 4 == 0) r = 4;
+        else if (rem % 2 == 0) r = 2;
+        else if (rem % 3 == 0) r = 3;
+        else if (rem % 5 == 0) r = 5;
+        else if (rem % 7 == 0) r = 7;
+        else {
+            r = 11;
+            while (rem % r) r += 2;
+        }
+        if (r > kMaxRadix) throw ArgFail("FFT length " + std::to_string(n) + " has a prime factor > 64");
+        if (s >= kMaxStages) throw ArgFail("FFT length " + std::to_string(n) + " needs too many stages");
+        P.radix[s++] = r;
+        rem /= r;
+    }
+    P.nst = s;
+    int ns = n;
+    for (int i = 0; i < s; ++i) {
+        P.n1[i] = ns / P.radix[i];
+        P.tws[i] = n / ns;
+        ns = P.n1[i];
+    }
+    return P;
+}
+
+// frequency held at position `pos` after the DIF stages (digit reversal)
+int freq_of_pos(const AxisPlan& P, int pos) {
+    int f = 0, mult = 1, p = pos;
+    for (int s = 0; s < P.nst; ++s) {
+        const int k2 = p / P.n1[s];
+        p -= k2 * P.n1[s];
+        f += mult * k2;
+        mult *= P.radix[s];
+    }
+    return f;
+}
+
+float2 w_of(long num, long den) {  // exp(-2 pi i num/den), computed in double
+    long q = num % den;
+    if (q < 0) q += den;
+    const double a = -2.0 * kPi * (double)q / (double)den;
+    return make_float2((float)std::cos(a), (float)std::sin(a));
+}
+
+float one_minus_cos(int k, int n) {  // 1 - cos(2 pi k / n) = 2 sin^2(pi k / n); exactly 0 at k = 0
+    if (k == 0) return 0.f;
+    const double s = std::sin(kPi * (double)k / (double)n);
+    return (float)(2.0 * s * s);
+}
+
+// ---- geometry + device tables for one grid -------------------------------------
+struct Geometry {
+    int M = 0, Ny = 0, Nz = 0, hx = 0;
+    long long N = 0, lines = 0;
+    int L = 0, odd = 0, TL = 0, PM = 0, PY = 0;
+    AxisPlan px{}, py{}, pz{};
+    DevArray<float2> twx, xtw, twy, twz;
+    DevArray<int> xpos;
+    DevArray<float> sx, sy, sz;
+    size_t xsmem = 0, psmem = 0;
+
+    void build(dreg_dims3 d) {
+        M = d.x;
+        Ny = d.y;
+        Nz = d.z;
+        hx = M / 2 + 1;
+        N = (long long)M * Ny * Nz;
+        lines = (long long)Ny * Nz;
+        odd = (M % 2 != 0) || M < 2;
+        L = odd ? M : M / 2;
+        px = make_plan(L);
+        py = make_plan(Ny);
+        pz = make_plan(Nz);
+        PM = (L % 2 == 0) ? L + 1 : L;
+        PY = (Ny % 2 == 0) ? Ny + 1 : Ny;
+        TL = 32;
+        while (TL > 4 && xpass_smem_bytes(L, hx, TL, PM) > 110 * 1024) TL /= 2;
+        xsmem = xpass_smem_bytes(L, hx, TL, PM);
+        psmem = plane_smem_bytes(Ny, Nz, PY);
+        if (xsmem > 227 * 1024) throw ArgFail("x extent too large for the shared-memory x-pass");
+        if (psmem > 227 * 1024)
+            throw ArgFail("y*z plane of " + std::to_string(Ny) + "x" + std::to_string(Nz) +
+                          " exceeds the single-CTA plane kernel (227 KB shared memory)");
+        if ((lines + TL - 1) / TL > kMaxPartials) throw ArgFail("grid has too many x-lines");
+
+        std::vector<float2> h(L);
+        for (int e = 0; e < L; ++e) h[e] = w_of(e, L);
+        up(twx, h);
+        std::vector<float2> hxw(hx + 1);
+        for (int k = 0; k <= hx; ++k) hxw[k] = w_of(k, M);
+        up(xtw, hxw);
+        std::vector<int> hp(L);
+        for (int pos = 0; pos < L; ++pos) hp[freq_of_pos(px, pos)] = pos;
+        up(xpos, hp);
+        h.assign(Ny, {});
+        for (int e = 0; e < Ny; ++e) h[e] = w_of(e, Ny);
+        up(twy, h);
+        h.assign(Nz, {});
+        for (int e = 0; e < Nz; ++e) h[e] = w_of(e, Nz);
+        up(twz, h);
+        std::vector<float> s(hx);
+        for (int p = 0; p < hx; ++p) s[p] = one_minus_cos(p, M);
+        up(sx, s);
+        s.assign(Ny, 0.f);
+        for (int pos = 0; pos < Ny; ++pos) s[pos] = one_minus_cos(freq_of_pos(py, pos), Ny);
+        up(sy, s);
+        s.assign(Nz, 0.f);
+        for (int pos = 0; pos < Nz; ++pos) s[pos] = one_minus_cos(freq_of_pos(pz, pos), Nz);
+        up(sz, s);
+    }
+
+    template <class T>
+    static void up(DevArray<T>& d, const std::vector<T>& h) {
+        d.alloc(h.size());
+        CK(cudaMemcpy(d.p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    }
+};
+
+// ---- workspace: all per-chunk device state --------------------------------------
+struct Workspace {
+    Geometry geo;
+    int P = 0;       // pair capacity
+    int diag_iters = 0;
+    DevArray<float> V, BH, WP, BP, G, D, I0, I1, PHI0, PHI1, W0, W1;
+    DevArray<float2> S;
+    DevArray<PairState> st;
+    DevArray<double> part, diag, energy;
+    DevArray<float> stage_t, stage_s, stage3, phi_soa, warped;
+    DevArray<const float*> tgt_tab, src_tab;
+    DevArray<float*> phi_tab, warped_tab;
+    DevArray<unsigned int> counter;
+    DevArray<double> scal;   // small scalar outputs
+    DevArray<float> fscal;
+    std::map<std::string, std::pair<cudaGraphExec_t, int>> graphs;
+
+    ~Workspace() { clear_graphs(); }
+    void clear_graphs() {
+        for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.first);
+        graphs.clear();
+    }
+
+    static size_t bytes_per_pair(const Geometry& g) {
+        return sizeof(float) * (size_t)g.N * (15 + 1 + 2 + 6 + 2 + 2 + 3 + 3 + 1) +
+               sizeof(float2) * 3 * (size_t)g.hx * g.lines + sizeof(double) * 3 * kMaxPartials;
+    }
+
+    void alloc(dreg_dims3 d, int pairs) {
+        geo.build(d);
+        P = pairs;
+        const size_t N = (size_t)geo.N;
+        V.alloc(P * 3 * N);
+        BH.alloc(P * 3 * N);
+        WP.alloc(P * 3 * N);
+        BP.alloc(P * 3 * N);
+        G.alloc(P * 3 * N);
+        D.alloc(P * N);
+        I0.alloc(P * N);
+        I1.alloc(P * N);
+        PHI0.alloc(P * 3 * N);
+        PHI1.alloc(P * 3 * N);
+        W0.alloc(P * N);
+        W1.alloc(P * N);
+        S.alloc((size_t)P * 3 * geo.hx * geo.lines);
+        st.alloc(P);
+        part.alloc((size_t)P * 3 * kMaxPartials);
+        energy.alloc(P);
+        stage_t.alloc(P * N);
+        stage_s.alloc(P * N);
+        stage3.alloc(P * 3 * N);
+        phi_soa.alloc(P * 3 * N);
+        warped.alloc(P * N);
+        tgt_tab.alloc(P);
+        src_tab.alloc(P);
+        phi_tab.alloc(P);
+        warped_tab.alloc(P);
+        counter.alloc(4);
+        CK(cudaMemset(counter.p, 0, sizeof(unsigned int) * 4));
+        CK(cudaMemset(st.p, 0, sizeof(PairState) * P));
+        scal.alloc(8);
+        fscal.alloc(2 + 2 * kMaxPartials);
+        clear_graphs();
+    }
+
+    void ensure_diag(int iters) {
+        if (iters > diag_iters) {
+            diag.alloc((size_t)P * iters * 3);
+            diag_iters = iters;
+            clear_graphs();
+        }
+    }
+
+    Fields fields(bool with_diag) const {
+        Fields F{};
+        F.M = geo.M;
+        F.Ny = geo.Ny;
+        F.Nz = geo.Nz;
+        F.hx = geo.hx;
+        F.N = geo.N;
+        F.lines = geo.lines;
+        F.V = V.p;
+        F.BH = BH.p;
+        F.WP = WP.p;
+        F.BP = BP.p;
+        F.G = G.p;
+        F.D = D.p;
+        F.S = S.p;
+        F.st = st.p;
+        F.part = part.p;
+        F.diag = with_diag ? diag.p : nullptr;
+        F.diag_stride = diag_iters;
+        return F;
+    }
+
+    RegBuffers regbufs() const {
+        RegBuffers R{};
+        R.I0 = I0.p;
+        R.I1 = I1.p;
+        R.PHI[0] = PHI0.p;
+        R.PHI[1] = PHI1.p;
+        R.WARPED[0] = W0.p;
+        R.WARPED[1] = W1.p;
+        R.tgt_in = tgt_tab.p;
+        R.src_in = src_tab.p;
+        R.phi_out = phi_tab.p;
+        R.warped_out = warped_tab.p;
+        R.tmpA = D.p;   // prep scratch aliases D / G (free before the first solve)
+        R.tmpB = G.p;
+        return R;
+    }
+
+    VolGeom vg() const { return VolGeom{geo.M, geo.Ny, geo.Nz, geo.N}; }
+};
+
+bool same_dims(const Geometry& g, dreg_dims3 d) { return g.M == d.x && g.Ny == d.y && g.Nz == d.z; }
+
+}  // namespace
+
+struct dreg_cuda_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    int chunk = 0;
+    int use_graphs = 1;
+    std::unique_ptr<Workspace> ws;
+    // pinned host staging for pointer tables and pair states
+    const float** h_tgt = nullptr;
+    const float** h_src = nullptr;
+    float** h_phi = nullptr;
+    float** h_warped = nullptr;
+    PairState* h_st = nullptr;
+    int h_cap = 0;
+
+    void ensure_host(int P) {
+        if (P <= h_cap) return;
+        free_host();
+        CK(cudaMallocHost((void**)&h_tgt, sizeof(void*) * P));
+        CK(cudaMallocHost((void**)&h_src, sizeof(void*) * P));
+        CK(cudaMallocHost((void**)&h_phi, sizeof(void*) * P));
+        CK(cudaMallocHost((void**)&h_warped, sizeof(void*) * P));
+        CK(cudaMallocHost((void**)&h_st, sizeof(PairState) * P));
+        h_cap = P;
+    }
+    void free_host() {
+        if (h_tgt) cudaFreeHost(h_tgt);
+        if (h_src) cudaFreeHost(h_src);
+        if (h_phi) cudaFreeHost(h_phi);
+        if (h_warped) cudaFreeHost(h_warped);
+        if (h_st) cudaFreeHost(h_st);
+        h_tgt = h_src = nullptr;
+        h_phi = h_warped = nullptr;
+        h_st = nullptr;
+        h_cap = 0;
+    }
+
+    Workspace& workspace(dreg_dims3 d, int pairs) {
+        if (!ws || !same_dims(ws->geo, d) || ws->P < pairs) {
+            ws.reset();
+            CK(cudaStreamSynchronize(stream));
+            auto w = std::make_unique<Workspace>();
+            w->alloc(d, pairs);
+            ws = std::move(w);
+        }
+        return *ws;
+    }
+};
+
+namespace {
+
+int fail(dreg_cuda_ctx* c, int code, const std::string& m) {
+    if (c) c->err = m;
+    return code;
+}
+
+template <class F>
+int guarded(dreg_cuda_ctx* c, F&& f) {
+    if (!c) return DREG_INVALID_ARGUMENT;
+    try {
+        CK(cudaSetDevice(c->device));
+        const int r = f();
+        if (r == DREG_OK) c->err.clear();
+        return r;
+    } catch (const ArgFail& e) {
+        return fail(c, DREG_INVALID_ARGUMENT, e.msg);
+    } catch (const NumFail& e) {
+        return fail(c, DREG_NUMERIC, e.msg);
+    } catch (const CudaFail& e) {
+        return fail(c, DREG_RUNTIME, e.msg);
+    } catch (const std::bad_alloc&) {
+        return fail(c, DREG_RUNTIME, "host allocation failed");
+    }
+}
+
+void check_solver(const dreg_solver_cfg* s) {
+    if (!s) throw ArgFail("solver config is null");
+    const int r = dreg_validate_solver_cfg(s);
+    if (r != DREG_OK) {
+        if (s->data_term != 1 && s->data_term != 2) throw ArgFail("solver: data term exponent must be 1 or 2");
+        if (s->order < 1 || s->order > 6) throw ArgFail("solver: regulariser order must be in [1, 6]");
+        if (!(s->lambda >= 0.0)) throw ArgFail("solver: lambda must be >= 0");
+        if (!(s->theta > 0.0)) throw ArgFail("solver: theta must be > 0");
+        if (!(s->epsilon > 0.0)) throw ArgFail("solver: epsilon must be > 0");
+        if (s->max_iters < 1) throw ArgFail("solver: max_iters must be >= 1");
+        throw ArgFail("solver: tol must be >= 0");
+    }
+}
+
+void check_dims(dreg_dims3 d, int min_extent, const char* what) {
+    if (d.x < 1 || d.y < 1 || d.z < 1) throw ArgFail("volume dims must be positive");
+    if (d.x < min_extent || d.y < min_extent || d.z < min_extent)
+        throw ArgFail(std::string(what) + ": every axis must have size >= " + std::to_string(min_extent));
+}
+
+SolverParams solver_params(const dreg_solver_cfg& s) {
+    SolverParams sp{};
+    sp.theta = s.theta;
+    sp.epsilon = s.epsilon;
+    sp.lambda = s.lambda;
+    sp.tol = s.tol;
+    sp.data_term = s.data_term;
+    sp.order = s.order;
+    sp.log_objective = s.log_objective;
+    sp.accelerate = s.accelerate;
+    return sp;
+}
+
+// Nesterov coefficients c_k = (alpha_k - 1) / alpha_{k+1}, alpha_0 = 1
+// (admm.cpp:198-200, :294-295).  Data-independent, so precomputed.
+std::vector<double> nesterov_coefs(int iters, bool accelerate) {
+    std::vector<double> c(std::max(iters, 1), 0.0);
+    double alpha = 1.0;
+    for (int k = 0; k < iters; ++k) {
+        const double next = dreg_nesterov_next_alpha(alpha);
+        c[k] = accelerate ? (alpha - 1.0) / next : 0.0;
+        alpha = next;
+    }
+    return c;
+}
+
+struct Launcher {
+    dreg_cuda_ctx* c;
+    int count = 0;
+    void operator()(cudaError_t e, int kernels = 1) {
+        if (e != cudaSuccess) throw CudaFail(std::string("kernel launch: ") + cudaGetErrorString(e));
+        count += kernels;
+    }
+};
+
+XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag) {
+    XArgs a{};
+    a.F = w.fields(diag);
+    a.px = w.geo.px;
+    a.twx = w.geo.twx.p;
+    a.xtw = w.geo.xtw.p;
+    a.xpos = w.geo.xpos.p;
+    a.sp = sp;
+    a.TL = w.geo.TL;
+    a.PM = w.geo.PM;
+    a.odd = w.geo.odd;
+    return a;
+}
+
+PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag) {
+    PArgs p{};
+    p.F = w.fields(diag);
+    p.py = w.geo.py;
+    p.pz = w.geo.pz;
+    p.twy = w.geo.twy.p;
+    p.twz = w.geo.twz.p;
+    p.sx = w.geo.sx.p;
+    p.sy = w.geo.sy.p;
+    p.sz = w.geo.sz.p;
+    p.lambda = (float)sp.lambda;
+    p.theta = (float)sp.theta;
+    p.scale = (float)(sp.theta / (double)w.geo.N);
+    p.order = sp.order;
+    p.PY = w.geo.PY;
+    p.energy_out = w.energy.p;
+    return p;
+}
+
+// One accelerated-ADMM velocity solve for all active pairs (admm.cpp:252-314):
+// grad/diff setup, then I iterations of (plane, xpass).  need_tail adds the last
+// w-update (only the constraint-residual diagnostic depends on it).
+void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, bool diag, bool need_tail,
+                   bool with_setup, cudaStream_t st) {
+    const bool log_obj = diag && s.log_objective;
+    SolverParams sp = solver_params(s);
+    sp.log_objective = log_obj ? 1 : 0;
+    const int I = s.max_iters;
+    const std::vector<double> coef = nesterov_coefs(I, s.accelerate != 0);
+    if (with_setup) L(launch_grad_diff(w.vg(), w.regbufs(), w.fields(diag), P, st));
+    XArgs xa = make_xargs(w, sp, diag);
+    PArgs pa = make_pargs(w, sp, diag);
+    pa.need_tail = need_tail ? 1 : 0;
+    auto energy = [&](int k) {
+        // objective_k = data term + lambda * spectral_energy(v_k)   (admm.cpp:288-292)
+        XArgs fa = xa;
+        fa.k = k;
+        fa.add_bh = 0;
+        PArgs ea = pa;
+        ea.k = k;
+        ea.F.S = w.S.p;
+        L(launch_xpass(fa, X_FWD, P, st));
+        L(launch_plane(ea, 1, P, st));
+    };
+    xa.k = 0;
+    xa.coef = 0.0;
+    // With the objective logged, each iteration's S = r2c(u_k) is briefly replaced by
+    // r2c(v_k) for the energy and then rebuilt (identical bits: u_k = v_k + b_hat_k).
+    L(launch_xpass(xa, X_FIRST, P, st));
+    if (log_obj) {
+        energy(0);
+        xa.k = 0;
+        xa.add_bh = 1;
+        L(launch_xpass(xa, X_FWD, P, st));  // restore S = r2c(u_0)
+        L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, 0, P, st));
+    }
+    for (int k = 1; k < I; ++k) {
+        pa.k = k - 1;
+        L(launch_plane(pa, 0, P, st));
+        xa.k = k;
+        xa.coef = coef[k - 1];
+        L(launch_xpass(xa, k == 1 ? X_SECOND : X_GENERAL, P, st));
+        if (log_obj) {
+            energy(k);
+            xa.add_bh = 1;
+            L(launch_xpass(xa, X_FWD, P, st));
+            L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, k, P, st));
+        }
+    }
+    if (need_tail) {
+        pa.k = I - 1;
+        L(launch_plane(pa, 0, P, st));
+        xa.k = I;
+        L(launch_xpass(xa, X_TAIL, P, st));
+    }
+}
+
+// register_pair for levels == 1 (registration.cpp:180-283), all pairs of the chunk.
+void enqueue_registration(Launcher& L, Workspace& w, int P, const dreg_reg_cfg& cfg, cudaStream_t st) {
+    const VolGeom g = w.vg();
+    const RegBuffers R = w.regbufs();
+    const Fields F = w.fields(false);
+    L(launch_prep_normalize(g, R, F, P, st), 3);
+    if (cfg.smooth_levels) {
+        L(launch_smooth_axis(g, R.tmpA, R.I0, 0, P, st));
+        L(launch_smooth_axis(g, R.I0, R.tmpA, 1, P, st));
+        L(launch_smooth_axis(g, R.tmpA, R.I0, 2, P, st));
+        L(launch_smooth_axis(g, R.tmpB, R.I1, 0, P, st));
+        L(launch_smooth_axis(g, R.I1, R.tmpB, 1, P, st));
+        L(launch_smooth_axis(g, R.tmpB, R.I1, 2, P, st));
+    } else {
+        CK(cudaMemcpyAsync(R.I0, R.tmpA, sizeof(float) * g.N * P, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(R.I1, R.tmpB, sizeof(float) * g.N * P, cudaMemcpyDeviceToDevice, st));
+    }
+    L(launch_level_init(g, R, F, 0, P, st));
+    dreg_solver_cfg s = cfg.solver;
+    s.max_iters = cfg.max_admm_iters_per_level[0];
+    const int K = cfg.max_warps_per_level[0];
+    for (int wi = 0; wi < K; ++wi) {
+        enqueue_solve(L, w, P, s, false, false, true, st);
+        L(launch_compose_decide(g, R, F, cfg.warp_improvement_threshold, K, P, st));
+    }
+    L(launch_finalize(g, R, F, P, st));
+}
+
+std::string graph_key(int P, const dreg_reg_cfg& c) {
+    char buf[512];
+    std::snprintf(buf, sizeof buf, "%d|%d|%d|%.17g|%.17g|%.17g|%d|%.17g|%d|%d|%d|%d|%.17g|%d", P,
+                  c.solver.data_term, c.solver.order, c.solver.lambda, c.solver.theta, c.solver.epsilon,
+                  c.solver.max_iters, c.solver.tol, c.solver.accelerate, c.levels, c.max_warps_per_level[0],
+                  c.max_admm_iters_per_level[0], c.warp_improvement_threshold, c.smooth_levels);
+    return buf;
+}
+
+void run_registration(dreg_cuda_ctx* c, Workspace& w, int P, const dreg_reg_cfg& cfg) {
+    cudaStream_t st = c->stream;
+    if (!c->use_graphs) {
+        Launcher L{c};
+        enqueue_registration(L, w, P, cfg, st);
+        c->launches += L.count;
+        return;
+    }
+    const std::string key = graph_key(P, cfg);
+    auto it = w.graphs.find(key);
+    if (it == w.graphs.end()) {
+        Launcher L{c};
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_registration(L, w, P, cfg, st);
+        } catch (...) {
+            cudaStreamEndCapture(st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        CK(cudaStreamEndCapture(st, &graph));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(e);
+        it = w.graphs.emplace(key, std::make_pair(exec, L.count)).first;
+    }
+    CK(cudaGraphLaunch(it->second.first, st));
+    c->launches += it->second.second;
+}
+
+void validate_reg(const dreg_reg_cfg* cfg, dreg_dims3 d) {
+    if (!cfg) throw ArgFail("registration config is null");
+    check_solver(&cfg->solver);
+    if (cfg->levels < 1) throw ArgFail("register_pair: levels must be >= 1");
+    if (cfg->levels > DREG_MAX_LEVELS) throw ArgFail("register_pair: per-level caps must list one entry per level");
+    if (!(cfg->warp_improvement_threshold > 0.0 && cfg->warp_improvement_threshold < 1.0))
+        throw ArgFail("register_pair: warp improvement threshold must be in (0,1)");
+    const int min_extent = 4 << (cfg->levels - 1);
+    if (d.x < 1 || d.y < 1 || d.z < 1) throw ArgFail("volume dims must be positive");
+    if (d.x < min_extent || d.y < min_extent || d.z < min_extent)
+        throw ArgFail("register_pair: dims too small for the level count");
+    for (int l = 0; l < cfg->levels; ++l) {
+        if (cfg->max_admm_iters_per_level[l] < 1) throw ArgFail("solver: max_iters must be >= 1");
+        if (cfg->max_warps_per_level[l] < 0) throw ArgFail("register_pair: negative warp cap");
+        if (cfg->max_warps_per_level[l] > DREG_MAX_WARPS) throw ArgFail("register_pair: warp cap above 64");
+    }
+    if (cfg->levels != 1)
+        throw ArgFail("register_pair: levels > 1 (pyramid) is not implemented on the B200 path yet");
+}
+
+void fill_results(const PairState* hs, int P, const Workspace& w, dreg_pair_result* out, double elapsed) {
+    for (int p = 0; p < P; ++p) {
+        dreg_pair_result& r = out[p];
+        std::memset(&r, 0, sizeof r);
+        const PairState& s = hs[p];
+        r.status = s.status;
+        r.velocity_count = s.velocity_count;
+        r.levels = 1;
+        dreg_level_log& lg = r.per_level[0];
+        lg.dims = {w.geo.M, w.geo.Ny, w.geo.Nz};
+        lg.warps = s.level_warps[0];
+        for (int i = 0; i <= lg.warps && i <= DREG_MAX_WARPS; ++i) lg.mean_sad[i] = s.mean_sad[0][i];
+        for (int i = 0; i < lg.warps && i < DREG_MAX_WARPS; ++i) lg.solver_iterations[i] = s.solver_iterations[0][i];
+        r.elapsed_seconds = elapsed;
+    }
+}
+
+int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs) {
+    if (c->chunk > 0) return std::min(c->chunk, n_pairs);
+    Geometry tmp;
+    tmp.M = d.x;
+    tmp.Ny = d.y;
+    tmp.Nz = d.z;
+    tmp.hx = d.x / 2 + 1;
+    tmp.N = (long long)d.x * d.y * d.z;
+    tmp.lines = (long long)d.y * d.z;
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t per = Workspace::bytes_per_pair(tmp);
+    size_t fit = (size_t)(0.6 * (double)free_b) / std::max<size_t>(per, 1);
+    if (c->ws && same_dims(c->ws->geo, d)) fit = std::max<size_t>(fit, (size_t)c->ws->P);
+    int P = (int)std::min<size_t>(fit, 32);
+    return std::max(1, std::min(P, n_pairs));
+}
+
+}  // namespace
+
+// =================================== C ABI ======================================
+extern "C" {
+
+void dreg_solver_cfg_default(dreg_solver_cfg* c) {
+    if (!c) return;
+    c->data_term = 1;
+    c->order = 2;
+    c->lambda = 0.0;
+    c->theta = 0.1;
+    c->epsilon = 1e-6;
+    c->max_iters = 100;
+    c->tol = 0.0;
+    c->accelerate = 1;
+    c->log_objective = 1;
+}
+
+int dreg_validate_solver_cfg(const dreg_solver_cfg* c) {
+    if (!c) return DREG_INVALID_ARGUMENT;
+    if (c->data_term != 1 && c->data_term != 2) return DREG_INVALID_ARGUMENT;
+    if (c->order < 1 || c->order > 6) return DREG_INVALID_ARGUMENT;
+    if (!(c->lambda >= 0.0)) return DREG_INVALID_ARGUMENT;
+    if (!(c->theta > 0.0)) return DREG_INVALID_ARGUMENT;
+    if (!(c->epsilon > 0.0)) return DREG_INVALID_ARGUMENT;
+    if (c->max_iters < 1) return DREG_INVALID_ARGUMENT;
+    if (!(c->tol >= 0.0)) return DREG_INVALID_ARGUMENT;
+    return DREG_OK;
+}
+
+int dreg_make_registration_config(int profile, const dreg_solver_cfg* solver, int levels, dreg_reg_cfg* out) {
+    if (!solver || !out || levels < 1 || levels > DREG_MAX_LEVELS) return DREG_INVALID_ARGUMENT;
+    std::memset(out, 0, sizeof *out);
+    out->solver = *solver;
+    out->levels = levels;
+    out->profile = profile;
+    out->warp_improvement_threshold = 0.02;
+    out->smooth_levels = 1;
+    if (profile == DREG_PROFILE_CAPPED) {
+        for (int l = 0; l < levels; ++l) {
+            out->max_admm_iters_per_level[l] = 5;
+            out->max_warps_per_level[l] = 10;
+        }
+        out->max_admm_iters_per_level[0] = 10;
+        out->max_warps_per_level[levels - 1] = 5;
+    } else {
+        for (int l = 0; l < levels; ++l) {
+            out->max_admm_iters_per_level[l] = 200;
+            out->max_warps_per_level[l] = 50;
+        }
+        if (out->solver.tol <= 0.0) out->solver.tol = 0.01;
+    }
+    return DREG_OK;
+}
+
+double dreg_nesterov_next_alpha(double alpha) { return 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * alpha * alpha)); }
+
+int dreg_laplacian_symbol(int order, dreg_dims3 d, double* out) {
+    if (order < 1 || order > 6 || d.x < 2 || d.y < 2 || d.z < 2 || !out) return DREG_INVALID_ARGUMENT;
+    std::vector<double> cx(d.x), cy(d.y), cz(d.z);
+    for (int k = 0; k < d.x; ++k) cx[k] = std::cos(2.0 * kPi * k / d.x);
+    for (int k = 0; k < d.y; ++k) cy[k] = std::cos(2.0 * kPi * k / d.y);
+    for (int k = 0; k < d.z; ++k) cz[k] = std::cos(2.0 * kPi * k / d.z);
+    cx[0] = cy[0] = cz[0] = 1.0;
+    size_t i = 0;
+    for (int r = 0; r < d.z; ++r)
+        for (int q = 0; q < d.y; ++q) {
+            const double yz = 3.0 - cy[q] - cz[r];
+            for (int p = 0; p < d.x; ++p, ++i) {
+                const double base = 2.0 * (yz - cx[p]);
+                double v = base;
+                for (int e = 1; e < order; ++e) v *= base;
+                out[i] = v;
+            }
+        }
+    return DREG_OK;
+}
+
+int dreg_cuda_ctx_create(int device, dreg_cuda_ctx** out) {
+    if (!out) return DREG_INVALID_ARGUMENT;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) return DREG_RUNTIME;
+    if (device < 0 || device >= n) return DREG_INVALID_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return DREG_RUNTIME;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return DREG_RUNTIME;
+    if (prop.major < 10) return DREG_RUNTIME;  // sm_100a binary only
+    auto* c = new dreg_cuda_ctx();
+    c->device = device;
+    if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+        delete c;
+        return DREG_RUNTIME;
+    }
+    c->stream = c->own;
+    *out = c;
+    return DREG_OK;
+}
+
+void dreg_cuda_ctx_destroy(dreg_cuda_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->ws.reset();
+    c->free_host();
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+}
+
+const char* dreg_cuda_last_error(const dreg_cuda_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int dreg_cuda_set_stream(dreg_cuda_ctx* c, void* stream) {
+    if (!c) return DREG_INVALID_ARGUMENT;
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+    return DREG_OK;
+}
+
+int64_t dreg_cuda_kernel_launches(const dreg_cuda_ctx* c) { return c ? c->launches : 0; }
+
+int dreg_cuda_set_batch_chunk(dreg_cuda_ctx* c, int pairs) {
+    if (!c || pairs < 0) return DREG_INVALID_ARGUMENT;
+    c->chunk = pairs;
+    return DREG_OK;
+}
+
+int dreg_cuda_set_use_graphs(dreg_cuda_ctx* c, int enable) {
+    if (!c) return DREG_INVALID_ARGUMENT;
+    c->use_graphs = enable ? 1 : 0;
+    return DREG_OK;
+}
+
+static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_host, const float* const* src_host,
+                         const float* tgt_dev, const float* src_dev, dreg_dims3 d, const dreg_reg_cfg* cfg,
+                         float* const* phi_host, float* const* warped_host, float* phi_dev, float* warped_dev,
+                         dreg_pair_result* results) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (n_pairs < 0) throw ArgFail("n_pairs must be >= 0");
+    validate_reg(cfg, d);
+    if (n_pairs == 0) return DREG_OK;
+    const bool host = tgt_host != nullptr;
+    const int chunk = pick_chunk(c, d, n_pairs);
+    Workspace& w = c->workspace(d, chunk);
+    c->ensure_host(w.P);
+    const size_t N = (size_t)w.geo.N;
+    cudaStream_t st = c->stream;
+    int first_bad = DREG_OK;
+    std::vector<PairState> states(n_pairs);
+    for (int p0 = 0; p0 < n_pairs; p0 += chunk) {
+        const int P = std::min(chunk, n_pairs - p0);
+        CK(cudaStreamSynchronize(st));  // host pointer tables are reused
+        for (int p = 0; p < P; ++p) {
+            const int q = p0 + p;
+            if (host) {
+                if (!tgt_host[q] || !src_host[q]) throw ArgFail("null input volume");
+                CK(cudaMemcpyAsync(w.stage_t.p + p * N, tgt_host[q], sizeof(float) * N, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(w.stage_s.p + p * N, src_host[q], sizeof(float) * N, cudaMemcpyHostToDevice, st));
+                c->h_tgt[p] = w.stage_t.p + p * N;
+                c->h_src[p] = w.stage_s.p + p * N;
+                c->h_phi[p] = (phi_host && phi_host[q]) ? w.phi_soa.p + p * 3 * N : nullptr;
+                c->h_warped[p] = (warped_host && warped_host[q]) ? w.warped.p + p * N : nullptr;
+            } else {
+                c->h_tgt[p] = tgt_dev + (size_t)q * N;
+                c->h_src[p] = src_dev + (size_t)q * N;
+                c->h_phi[p] = phi_dev ? phi_dev + (size_t)q * 3 * N : nullptr;
+                c->h_warped[p] = warped_dev ? warped_dev + (size_t)q * N : nullptr;
+            }
+        }
+        CK(cudaMemcpyAsync(w.tgt_tab.p, c->h_tgt, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.src_tab.p, c->h_src, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.phi_tab.p, c->h_phi, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.warped_tab.p, c->h_warped, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        run_registration(c, w, P, *cfg);
+        if (host) {
+            for (int p = 0; p < P; ++p) {
+                const int q = p0 + p;
+                if (phi_host && phi_host[q]) {
+                    CK(launch_soa_to_aos((long long)N, w.phi_soa.p + p * 3 * N, w.stage3.p + p * 3 * N, st));
+                    c->launches += 1;
+                    CK(cudaMemcpyAsync(phi_host[q], w.stage3.p + p * 3 * N, sizeof(float) * 3 * N,
+                                       cudaMemcpyDeviceToHost, st));
+                }
+                if (warped_host && warped_host[q])
+                    CK(cudaMemcpyAsync(warped_host[q], w.warped.p + p * N, sizeof(float) * N, cudaMemcpyDeviceToHost, st));
+            }
+        }
+        CK(cudaMemcpyAsync(c->h_st, w.st.p, sizeof(PairState) * P, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int p = 0; p < P; ++p) states[p0 + p] = c->h_st[p];
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (int q = 0; q < n_pairs; ++q) {
+        if (states[q].status != DREG_OK && first_bad == DREG_OK) first_bad = states[q].status;
+    }
+    if (results) fill_results(states.data(), n_pairs, w, results, el);
+    if (first_bad != DREG_OK) {
+        c->err = "register_pair: non-finite values (input volumes, velocity or deformation)";
+        return first_bad;
+    }
+    return DREG_OK;
+}
+
+int dreg_cuda_register_pair(dreg_cuda_ctx* c, const float* target, const float* source, dreg_dims3 dims,
+                            dreg_spacing3 spacing, const dreg_reg_cfg* cfg, float* phi_out, float* warped_out,
+                            dreg_pair_result* result) {
+    (void)spacing;
+    const float* t[1] = {target};
+    const float* s[1] = {source};
+    float* po[1] = {phi_out};
+    float* wo[1] = {warped_out};
+    return guarded(c, [&] {
+        if (!target || !source) throw ArgFail("null input volume");
+        return register_impl(c, 1, t, s, nullptr, nullptr, dims, cfg, po, wo, nullptr, nullptr, result);
+    });
+}
+
+int dreg_cuda_register_batch(dreg_cuda_ctx* c, int n_pairs, const float* const* targets,
+                             const float* const* sources, dreg_dims3 dims, dreg_spacing3 spacing,
+                             const dreg_reg_cfg* cfg, float* const* phi_out, float* const* warped_out,
+                             dreg_pair_result* results) {
+    (void)spacing;
+    return guarded(c, [&] {
+        if (n_pairs > 0 && (!targets || !sources)) throw ArgFail("null input arrays");
+        return register_impl(c, n_pairs, targets, sources, nullptr, nullptr, dims, cfg, phi_out, warped_out,
+                             nullptr, nullptr, results);
+    });
+}
+
+int dreg_cuda_register_batch_device(dreg_cuda_ctx* c, int n_pairs, const float* targets_dev,
+                                    const float* sources_dev, dreg_dims3 dims, dreg_spacing3 spacing,
+                                    const dreg_reg_cfg* cfg, float* phi_dev_out, float* warped_dev_out,
+                                    dreg_pair_result* results) {
+    (void)spacing;
+    return guarded(c, [&] {
+        if (n_pairs > 0 && (!targets_dev || !sources_dev)) throw ArgFail("null input arrays");
+        return register_impl(c, n_pairs, nullptr, nullptr, targets_dev, sources_dev, dims, cfg, nullptr, nullptr,
+                             phi_dev_out, warped_dev_out, results);
+    });
+}
+
+// ---- single solve ---------------------------------------------------------------
+int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float* warped_source, dreg_dims3 d,
+                             const dreg_solver_cfg* cfg, float* velocity_out, dreg_solver_diag* diag) {
+    return guarded(c, [&] {
+        check_solver(cfg);
+        check_dims(d, 2, "image_gradient");
+        if (!target || !warped_source || !velocity_out) throw ArgFail("null buffer");
+        Workspace& w = c->workspace(d, 1);
+        w.ensure_diag(cfg->max_iters);
+        const size_t N = (size_t)w.geo.N;
+        cudaStream_t st = c->stream;
+        Launcher L{c};
+        CK(cudaMemcpyAsync(w.I0.p, target, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.W0.p, warped_source, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(w.diag.p, 0, sizeof(double) * 3 * w.diag_iters, st));
+        L(launch_state_reset(w.st.p, 1, st));
+        enqueue_solve(L, w, 1, *cfg, true, true, true, st);
+        L(launch_soa_to_aos((long long)N, w.V.p, w.stage3.p, st));
+        c->launches += L.count;
+        CK(cudaMemcpyAsync(velocity_out, w.stage3.p, sizeof(float) * 3 * N, cudaMemcpyDeviceToHost, st));
+        PairState hs;
+        CK(cudaMemcpyAsync(&hs, w.st.p, sizeof(PairState), cudaMemcpyDeviceToHost, st));
+        std::vector<double> dg((size_t)3 * w.diag_iters);
+        CK(cudaMemcpyAsync(dg.data(), w.diag.p, sizeof(double) * dg.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (diag) {
+            diag->iterations = hs.iterations;
+            diag->final_change = hs.final_change;
+            diag->converged = hs.solve_done;
+            for (int k = 0; k < hs.iterations; ++k) {
+                if (diag->constraint_residual) diag->constraint_residual[k] = dg[3 * k + 1];
+                if (diag->objective && cfg->log_objective) diag->objective[k] = dg[3 * k + 2];
+            }
+        }
+        for (size_t i = 0; i < 3 * N; ++i)
+            if (!std::isfinite(velocity_out[i]))
+                throw NumFail("solve_velocity: velocity field contains non-finite values");
+        return DREG_OK;
+    });
+}
+
+// ---- building blocks ------------------------------------------------------------
+static void upload_aos(dreg_cuda_ctx* c, Workspace& w, const float* host_aos, float* dev_soa) {
+    const size_t N = (size_t)w.geo.N;
+    CK(cudaMemcpyAsync(w.stage3.p, host_aos, sizeof(float) * 3 * N, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_aos_to_soa((long long)N, w.stage3.p, dev_soa, c->stream));
+    c->launches += 1;
+}
+
+static void download_aos(dreg_cuda_ctx* c, Workspace& w, const float* dev_soa, float* host_aos) {
+    const size_t N = (size_t)w.geo.N;
+    CK(launch_soa_to_aos((long long)N, dev_soa, w.stage3.p, c->stream));
+    c->launches += 1;
+    CK(cudaMemcpyAsync(host_aos, w.stage3.p, sizeof(float) * 3 * N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+}
+
+int dreg_cuda_v_update(dreg_cuda_ctx* c, const float* target, const float* warped, const float* grad,
+                       const float* w_hat, const float* b_hat, dreg_dims3 d, const dreg_solver_cfg* cfg, float* out) {
+    return guarded(c, [&] {
+        if (!cfg) throw ArgFail("null config");
+        if (cfg->data_term == 1 && !(cfg->epsilon > 0.0)) throw ArgFail("v_update_l1: epsilon must be > 0");
+        check_dims(d, 1, "v_update");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.I0.p, target, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(w.I1.p, warped, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        upload_aos(c, w, grad, w.G.p);
+        upload_aos(c, w, w_hat, w.WP.p);
+        upload_aos(c, w, b_hat, w.BH.p);
+        CK(launch_v_update(w.vg(), cfg->data_term, w.I0.p, w.I1.p, w.G.p, w.WP.p, w.BH.p, cfg->theta, cfg->epsilon,
+                           w.V.p, c->stream));
+        c->launches += 1;
+        download_aos(c, w, w.V.p, out);
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_w_update(dreg_cuda_ctx* c, const float* v, const float* b_hat, dreg_dims3 d, const dreg_solver_cfg* cfg,
+                       float* out) {
+    return guarded(c, [&] {
+        if (!cfg) throw ArgFail("null config");
+        if (cfg->order < 1 || cfg->order > 6) throw ArgFail("laplacian_symbol: order must be in [1, 6]");
+        check_dims(d, 2, "laplacian_symbol");
+        Workspace& w = c->workspace(d, 1);
+        upload_aos(c, w, v, w.V.p);
+        upload_aos(c, w, b_hat, w.BH.p);
+        Launcher L{c};
+        L(launch_state_reset(w.st.p, 1, c->stream));
+        const SolverParams sp = solver_params(*cfg);
+        XArgs xa = make_xargs(w, sp, false);
+        xa.add_bh = 1;
+        L(launch_xpass(xa, X_FWD, 1, c->stream));
+        PArgs pa = make_pargs(w, sp, false);
+        L(launch_plane(pa, 0, 1, c->stream));
+        L(launch_xpass(xa, X_INV, 1, c->stream));
+        c->launches += L.count;
+        download_aos(c, w, w.WP.p, out);
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_regulariser_energy(dreg_cuda_ctx* c, const float* wfield, dreg_dims3 d, int order, double* out) {
+    return guarded(c, [&] {
+        if (order < 1 || order > 6) throw ArgFail("laplacian_symbol: order must be in [1, 6]");
+        check_dims(d, 2, "laplacian_symbol");
+        Workspace& w = c->workspace(d, 1);
+        upload_aos(c, w, wfield, w.V.p);
+        Launcher L{c};
+        L(launch_state_reset(w.st.p, 1, c->stream));
+        dreg_solver_cfg s;
+        dreg_solver_cfg_default(&s);
+        s.order = order;
+        const SolverParams sp = solver_params(s);
+        XArgs xa = make_xargs(w, sp, false);
+        xa.add_bh = 0;
+        L(launch_xpass(xa, X_FWD, 1, c->stream));
+        PArgs pa = make_pargs(w, sp, false);
+        L(launch_plane(pa, 1, 1, c->stream));
+        c->launches += L.count;
+        CK(cudaMemcpyAsync(out, w.energy.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_warp_image(dreg_cuda_ctx* c, const float* img, const float* disp, dreg_dims3 d, float* out) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "warp_image");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.I1.p, img, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        upload_aos(c, w, disp, w.PHI0.p);
+        CK(launch_warp_image(w.vg(), w.I1.p, w.PHI0.p, w.W0.p, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, w.W0.p, sizeof(float) * N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_image_gradient(dreg_cuda_ctx* c, const float* img, dreg_dims3 d, float* out) {
+    return guarded(c, [&] {
+        check_dims(d, 2, "image_gradient");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.W0.p, img, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_gradient(w.vg(), w.W0.p, w.G.p, c->stream));
+        c->launches += 1;
+        download_aos(c, w, w.G.p, out);
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_compose_deformation(dreg_cuda_ctx* c, const float* disp, const float* v, dreg_dims3 d, float* out) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "compose_deformation");
+        Workspace& w = c->workspace(d, 1);
+        upload_aos(c, w, disp, w.PHI0.p);
+        upload_aos(c, w, v, w.V.p);
+        CK(launch_compose(w.vg(), w.PHI0.p, w.V.p, w.PHI1.p, c->stream));
+        c->launches += 1;
+        download_aos(c, w, w.PHI1.p, out);
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_jacobian(dreg_cuda_ctx* c, const float* disp, dreg_dims3 d, float* det_out, dreg_jacobian_stats* stats) {
+    return guarded(c, [&] {
+        check_dims(d, 3, "jacobian_determinant");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        upload_aos(c, w, disp, w.PHI0.p);
+        CK(launch_jacobian(w.vg(), w.PHI0.p, w.W0.p, w.part.p, w.scal.p, w.counter.p, c->stream));
+        c->launches += 1;
+        double h[3];
+        CK(cudaMemcpyAsync(h, w.scal.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        if (det_out) CK(cudaMemcpyAsync(det_out, w.W0.p, sizeof(float) * N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (stats) {
+            stats->nonpositive = (int64_t)h[0];
+            stats->interior = (int64_t)h[1];
+            stats->min_det = h[2];
+            stats->pct_nonpositive = 100.0 * h[0] / h[1];
+        }
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_normalize_intensity_pair(dreg_cuda_ctx* c, const float* a, const float* b, dreg_dims3 d, float* oa,
+                                       float* ob) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "normalize_intensity_pair");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.I0.p, a, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(w.I1.p, b, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_minmax_normalize(w.vg(), w.I0.p, w.I1.p, w.W0.p, w.W1.p, w.fscal.p, w.counter.p, c->stream));
+        c->launches += 2;
+        CK(cudaMemcpyAsync(oa, w.W0.p, sizeof(float) * N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(ob, w.W1.p, sizeof(float) * N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_binomial_smooth(dreg_cuda_ctx* c, const float* img, dreg_dims3 d, float* out) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "binomial_smooth");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.W0.p, img, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_smooth_axis(w.vg(), w.W0.p, w.W1.p, 0, 1, c->stream));
+        CK(launch_smooth_axis(w.vg(), w.W1.p, w.W0.p, 1, 1, c->stream));
+        CK(launch_smooth_axis(w.vg(), w.W0.p, w.W1.p, 2, 1, c->stream));
+        c->launches += 3;
+        CK(cudaMemcpyAsync(out, w.W1.p, sizeof(float) * N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_mean_sad(dreg_cuda_ctx* c, const float* a, const float* b, dreg_dims3 d, double* out) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "mean_sad");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.W0.p, a, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(w.W1.p, b, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_sad(w.vg(), w.W0.p, w.W1.p, w.part.p, w.scal.p, w.counter.p, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_downsample(dreg_cuda_ctx* c, const float* img, dreg_dims3 d, float* out) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "downsample");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        const VolGeom src = w.vg();
+        const int ox = (d.x + 1) / 2, oy = (d.y + 1) / 2, oz = (d.z + 1) / 2;
+        const VolGeom dst{ox, oy, oz, (long long)ox * oy * oz};
+        CK(cudaMemcpyAsync(w.W0.p, img, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_downsample(src, dst, w.W0.p, w.W1.p, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, w.W1.p, sizeof(float) * dst.N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_upsample_velocity(dreg_cuda_ctx* c, const float* v, dreg_dims3 sd, dreg_dims3 dd, float* out) {
+    return guarded(c, [&] {
+        check_dims(sd, 1, "upsample_velocity");
+        check_dims(dd, 1, "upsample_velocity");
+        if (dd.x < sd.x || dd.y < sd.y || dd.z < sd.z)
+            throw ArgFail("upsample_velocity: target dims smaller than source");
+        Workspace& w = c->workspace(dd, 1);  // destination-sized buffers hold both
+        const VolGeom src{sd.x, sd.y, sd.z, (long long)sd.x * sd.y * sd.z};
+        const VolGeom dst = w.vg();
+        CK(cudaMemcpyAsync(w.stage3.p, v, sizeof(float) * 3 * src.N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_aos_to_soa(src.N, w.stage3.p, w.PHI0.p, c->stream));
+        CK(launch_upsample(src, dst, w.PHI0.p, w.PHI1.p, 3, c->stream));
+        c->launches += 2;
+        download_aos(c, w, w.PHI1.p, out);
+        return DREG_OK;
+    });
+}
+
+}  // extern "C"

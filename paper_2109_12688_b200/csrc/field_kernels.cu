@@ -1,0 +1,650 @@
+// Deformation-side kernels: warp + gradient, composition + warp + SAD + the
+// accept/revert/stop decision, Jacobian folding check, intensity preparation.
+// All gathers use software trilinear interpolation in fp64 with the reference's
+// clamp-then-floor rule (volume.cpp:36-99); no texture filtering (its 8-bit
+// weights would break parity).
+#include <cfloat>
+
+#include "kernels.cuh"
+#include "launch.h"
+#include "pointwise.cuh"
+
+namespace dregb {
+
+constexpr int kVT = 256;  // threads per voxel-kernel block
+
+static unsigned voxel_blocks(long long N) {
+    long long b = (N + kVT - 1) / kVT;
+    if (b > 1184) b = 1184;  // 148 SMs x 8 resident blocks; grid-stride beyond
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+__device__ __forceinline__ void unflat(long long i, int M, int Ny, int& x, int& y, int& z) {
+    const long long row = i / M;
+    x = (int)(i - row * M);
+    z = (int)(row / Ny);
+    y = (int)(row - (long long)z * Ny);
+}
+
+// ---- per-solve setup: grad(warped) + (warped - target) -------------------------
+__global__ void __launch_bounds__(kVT) grad_diff_kernel(VolGeom g, RegBuffers R, Fields F) {
+    const int pair = blockIdx.y;
+    PairState* st = F.st + pair;
+    if (!st->active || st->status) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->solve_done = 0;
+        st->iterations = 0;
+        st->done_iter = -1;
+    }
+    const long long N = g.N;
+    const float* W = R.WARPED[st->cur] + (size_t)pair * N;
+    const float* T = R.I0 + (size_t)pair * N;
+    float* G = F.G + (size_t)pair * 3 * N;
+    float* D = F.D + (size_t)pair * N;
+    const size_t sy = (size_t)g.M, sz = (size_t)g.M * g.Ny;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        G[i] = (float)diff1(W, i, x, g.M, 1);
+        G[N + i] = (float)diff1(W, i, y, g.Ny, sy);
+        G[2 * N + i] = (float)diff1(W, i, z, g.Nz, sz);
+        D[i] = (float)((double)W[i] - (double)T[i]);
+    }
+}
+
+cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s) {
+    grad_diff_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F);
+    return cudaGetLastError();
+}
+
+// ---- compose + warp + SAD + decide -------------------------------------------
+__global__ void __launch_bounds__(kVT) compose_decide_kernel(VolGeom g, RegBuffers R, Fields F, double thr,
+                                                             int max_warps) {
+    __shared__ double red[32];
+    const int pair = blockIdx.y;
+    PairState* st = F.st + pair;
+    if (!st->active || st->status) return;
+    const long long N = g.N;
+    const int cur = st->cur;
+    const float* phi = R.PHI[cur] + (size_t)pair * 3 * N;
+    float* phin = R.PHI[cur ^ 1] + (size_t)pair * 3 * N;
+    float* wn = R.WARPED[cur ^ 1] + (size_t)pair * N;
+    const float* I1 = R.I1 + (size_t)pair * N;
+    const float* I0 = R.I0 + (size_t)pair * N;
+    const float* V = F.V + (size_t)pair * 3 * N;
+    double sad = 0.0, bad = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        const float v0 = V[i], v1 = V[N + i], v2 = V[2 * N + i];
+        if (!(isfinite(v0) && isfinite(v1) && isfinite(v2))) bad += 1.0;
+        // compose_deformation: disp'(x) = v(x) + disp(x + v(x))   (volume.cpp:161-181)
+        double s[3];
+        trilinear3(phi, (size_t)N, g.M, g.Ny, g.Nz, x + (double)v0, y + (double)v1, z + (double)v2, s);
+        const float p0 = (float)((double)v0 + s[0]);
+        const float p1 = (float)((double)v1 + s[1]);
+        const float p2 = (float)((double)v2 + s[2]);
+        phin[i] = p0;
+        phin[N + i] = p1;
+        phin[2 * N + i] = p2;
+        // warp_image(level_source, phi_candidate)   (registration.cpp:253)
+        const float w = (float)trilinear(I1, g.M, g.Ny, g.Nz, x + (double)p0, y + (double)p1, z + (double)p2);
+        wn[i] = w;
+        sad += fabs((double)w - (double)I0[i]);  // mean_sad (registration.cpp:145-152)
+    }
+    const double ts = block_sum<kVT>(sad, red);
+    const double tb = block_sum<kVT>(bad, red);
+    if (threadIdx.x == 0) {
+        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
+        part[blockIdx.x] = ts;
+        part[kMaxPartials + blockIdx.x] = tb;
+        if (last_block_ticket(&st->counter, gridDim.x)) {
+            double sum = 0.0, nbad = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                sum += part[b];
+                nbad += part[kMaxPartials + b];
+            }
+            if (nbad > 0.0) {
+                // solve_velocity's all_finite(v) -> numeric_error (admm.cpp:310-312)
+                st->status = DREG_NUMERIC;
+                st->active = 0;
+                return;
+            }
+            const double sad_new = sum / (double)N;
+            const int lvl = st->level;
+            if (sad_new > st->sad_prev) {  // revert (registration.cpp:256-258)
+                st->active = 0;
+                return;
+            }
+            st->cur = cur ^ 1;
+            const int w = st->warps;
+            if (w < DREG_MAX_WARPS) {
+                st->mean_sad[lvl][w + 1] = sad_new;
+                st->solver_iterations[lvl][w] = st->iterations;
+            }
+            st->warps = w + 1;
+            st->level_warps[lvl] = w + 1;
+            st->velocity_count += 1;
+            const double prev = st->sad_prev;
+            const double improvement = (prev - sad_new) / fmax(prev, DBL_MIN);  // :266-267
+            st->sad_prev = sad_new;
+            if (improvement < thr || st->warps >= max_warps) st->active = 0;
+        }
+    }
+}
+
+cudaError_t launch_compose_decide(VolGeom g, const RegBuffers& R, Fields F, double thr, int max_warps,
+                                  int npairs, cudaStream_t s) {
+    compose_decide_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F, thr, max_warps);
+    return cudaGetLastError();
+}
+
+// ---- intensity preparation ----------------------------------------------------
+// Pass 1: shared min/max of target and source + all_finite (registration.cpp:199-201,
+// :157-166); the last block of each pair stores the range.
+__global__ void __launch_bounds__(kVT) minmax_kernel(VolGeom g, RegBuffers R, Fields F) {
+    __shared__ double red[32];
+    const int pair = blockIdx.y;
+    PairState* st = F.st + pair;
+    const long long N = g.N;
+    const float* A = R.tgt_in[pair];
+    const float* B = R.src_in[pair];
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    double bad = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float a = A[i], b = B[i];
+        if (!isfinite(a) || !isfinite(b)) bad += 1.0;
+        lo = fminf(lo, fminf(a, b));
+        hi = fmaxf(hi, fmaxf(a, b));
+    }
+    const double tlo = block_min<kVT>((double)lo, red);
+    const double thi = -block_min<kVT>(-(double)hi, red);
+    const double tb = block_sum<kVT>(bad, red);
+    if (threadIdx.x == 0) {
+        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
+        part[blockIdx.x] = tlo;
+        part[kMaxPartials + blockIdx.x] = thi;
+        part[2 * kMaxPartials + blockIdx.x] = tb;
+        if (last_block_ticket(&st->counter, gridDim.x)) {
+            double l = 1e300, h = -1e300, nb = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                l = fmin(l, part[b]);
+                h = fmax(h, part[kMaxPartials + b]);
+                nb += part[2 * kMaxPartials + b];
+            }
+            st->lo = (float)l;
+            st->hi = (float)h;
+            if (nb > 0.0) {
+                st->status = DREG_NUMERIC;
+                st->active = 0;
+            }
+        }
+    }
+}
+
+// Pass 2: affine map onto [0,1] with the scale computed in fp64.
+__global__ void __launch_bounds__(kVT) normalize_kernel(VolGeom g, RegBuffers R, Fields F) {
+    const int pair = blockIdx.y;
+    const PairState* st = F.st + pair;
+    if (st->status) return;
+    const long long N = g.N;
+    const float* A = R.tgt_in[pair];
+    const float* B = R.src_in[pair];
+    float* oa = R.tmpA + (size_t)pair * N;
+    float* ob = R.tmpB + (size_t)pair * N;
+    const double lo = st->lo;
+    const double range = (double)st->hi - lo;
+    const double scale = range > 0.0 ? 1.0 / range : 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        oa[i] = (float)(((double)A[i] - lo) * scale);
+        ob[i] = (float)(((double)B[i] - lo) * scale);
+    }
+}
+
+__global__ void state_reset_kernel(PairState* st, int npairs) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npairs) return;
+    PairState& s = st[p];
+    s.active = 1;
+    s.cur = 0;
+    s.solve_done = 0;
+    s.iterations = 0;
+    s.status = DREG_OK;
+    s.velocity_count = 0;
+    s.warps = 0;
+    s.level = 0;
+    s.counter = 0;
+    s.done_iter = -1;
+    s.sad_prev = 0.0;
+    s.final_change = 0.0;
+    for (int l = 0; l < DREG_MAX_LEVELS; ++l) s.level_warps[l] = 0;
+}
+
+cudaError_t launch_state_reset(PairState* st, int npairs, cudaStream_t s) {
+    state_reset_kernel<<<(npairs + 127) / 128, 128, 0, s>>>(st, npairs);
+    return cudaGetLastError();
+}
+
+__global__ void objective_acc_kernel(Fields F, const double* energy, double lambda, int k, int npairs) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npairs) return;
+    const PairState* st = F.st + p;
+    if (!st->active || st->status) return;
+    if (st->solve_done && k > st->done_iter) return;
+    F.diag[((size_t)p * F.diag_stride + k) * 3 + 2] += lambda * energy[p];
+}
+
+cudaError_t launch_objective_accumulate(Fields F, const double* energy, double lambda, int k, int npairs,
+                                        cudaStream_t s) {
+    objective_acc_kernel<<<(npairs + 127) / 128, 128, 0, s>>>(F, energy, lambda, k, npairs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prep_normalize(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s) {
+    state_reset_kernel<<<(npairs + 127) / 128, 128, 0, s>>>(F.st, npairs);
+    minmax_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F);
+    normalize_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F);
+    return cudaGetLastError();
+}
+
+// ---- separable [1 2 1]/4 with edge clamping (registration.cpp:32-58) ----------
+__global__ void __launch_bounds__(kVT) smooth_axis_kernel(VolGeom g, const float* in, float* out, int axis) {
+    const long long N = g.N;
+    const float* f = in + (size_t)blockIdx.y * N;
+    float* o = out + (size_t)blockIdx.y * N;
+    const int extent = axis == 0 ? g.M : (axis == 1 ? g.Ny : g.Nz);
+    const size_t stride = axis == 0 ? 1 : (axis == 1 ? (size_t)g.M : (size_t)g.M * g.Ny);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        const int pos = axis == 0 ? x : (axis == 1 ? y : z);
+        const double lo = f[pos > 0 ? i - stride : i];
+        const double hi = f[pos < extent - 1 ? i + stride : i];
+        o[i] = (float)(0.25 * (lo + hi) + 0.5 * (double)f[i]);
+    }
+}
+
+cudaError_t launch_smooth_axis(VolGeom g, const float* in, float* out, int axis, int npairs, cudaStream_t s) {
+    smooth_axis_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, in, out, axis);
+    return cudaGetLastError();
+}
+
+// ---- level start: phi = identity, warped = source, initial mean SAD ------------
+__global__ void __launch_bounds__(kVT) level_init_kernel(VolGeom g, RegBuffers R, Fields F, int level) {
+    __shared__ double red[32];
+    const int pair = blockIdx.y;
+    PairState* st = F.st + pair;
+    if (st->status) return;
+    const long long N = g.N;
+    float* phi = R.PHI[0] + (size_t)pair * 3 * N;
+    float* W = R.WARPED[0] + (size_t)pair * N;
+    const float* I1 = R.I1 + (size_t)pair * N;
+    const float* I0 = R.I0 + (size_t)pair * N;
+    double sad = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        phi[i] = 0.f;
+        phi[N + i] = 0.f;
+        phi[2 * N + i] = 0.f;
+        const float w = I1[i];  // trilinear at integer coordinates is exact
+        W[i] = w;
+        sad += fabs((double)w - (double)I0[i]);
+    }
+    const double ts = block_sum<kVT>(sad, red);
+    if (threadIdx.x == 0) {
+        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
+        part[blockIdx.x] = ts;
+        if (last_block_ticket(&st->counter, gridDim.x)) {
+            double sum = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) sum += part[b];
+            st->sad_prev = sum / (double)N;
+            st->mean_sad[level][0] = st->sad_prev;
+            st->cur = 0;
+            st->warps = 0;
+            st->level = level;
+            st->active = 1;
+        }
+    }
+}
+
+cudaError_t launch_level_init(VolGeom g, const RegBuffers& R, Fields F, int level, int npairs, cudaStream_t s) {
+    level_init_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F, level);
+    return cudaGetLastError();
+}
+
+// ---- end of registration: finiteness of phi, phi out, warp of the ORIGINAL source
+__global__ void __launch_bounds__(kVT) finalize_kernel(VolGeom g, RegBuffers R, Fields F) {
+    __shared__ double red[32];
+    const int pair = blockIdx.y;
+    PairState* st = F.st + pair;
+    if (st->status) return;
+    const long long N = g.N;
+    const float* phi = R.PHI[st->cur] + (size_t)pair * 3 * N;
+    const float* src = R.src_in[pair];
+    float* po = R.phi_out ? R.phi_out[pair] : nullptr;
+    float* wo = R.warped_out ? R.warped_out[pair] : nullptr;
+    double bad = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        const float u0 = phi[i], u1 = phi[N + i], u2 = phi[2 * N + i];
+        if (!(isfinite(u0) && isfinite(u1) && isfinite(u2))) bad += 1.0;
+        if (po) {
+            po[i] = u0;
+            po[N + i] = u1;
+            po[2 * N + i] = u2;
+        }
+        if (wo) wo[i] = (float)trilinear(src, g.M, g.Ny, g.Nz, x + (double)u0, y + (double)u1, z + (double)u2);
+    }
+    const double tb = block_sum<kVT>(bad, red);
+    if (threadIdx.x == 0) {
+        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
+        part[blockIdx.x] = tb;
+        if (last_block_ticket(&st->counter, gridDim.x)) {
+            double nb = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) nb += part[b];
+            if (nb > 0.0) st->status = DREG_NUMERIC;  // registration.cpp:275-277
+        }
+    }
+}
+
+cudaError_t launch_finalize(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s) {
+    finalize_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F);
+    return cudaGetLastError();
+}
+
+// ---- Jacobian determinant + interior folding statistics ------------------------
+__global__ void __launch_bounds__(kVT) jacobian_kernel(VolGeom g, const float* __restrict__ u, float* det,
+                                                       double* part, double* out3, unsigned int* counter) {
+    __shared__ double red[32];
+    const long long N = g.N;
+    const size_t sy = (size_t)g.M, sz = (size_t)g.M * g.Ny;
+    double nonpos = 0.0, mind = 1e300;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        double j[3][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float* uc = u + (size_t)c * N;
+            j[c][0] = diff1(uc, i, x, g.M, 1) + (c == 0 ? 1.0 : 0.0);
+            j[c][1] = diff1(uc, i, y, g.Ny, sy) + (c == 1 ? 1.0 : 0.0);
+            j[c][2] = diff1(uc, i, z, g.Nz, sz) + (c == 2 ? 1.0 : 0.0);
+        }
+        // cofactor expansion along row 0 (volume.cpp:221-223), stored as fp32 (:224)
+        const double value = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
+                             j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
+                             j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
+        const float dv = (float)value;
+        if (det) det[i] = dv;
+        if (x >= 1 && x < g.M - 1 && y >= 1 && y < g.Ny - 1 && z >= 1 && z < g.Nz - 1) {
+            const double d = (double)dv;  // metrics.cpp:217-227 compares the fp32 value
+            mind = fmin(mind, d);
+            nonpos += d <= 0.0 ? 1.0 : 0.0;
+        }
+    }
+    const double tn = block_sum<kVT>(nonpos, red);
+    const double tm = block_min<kVT>(mind, red);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = tn;
+        part[kMaxPartials + blockIdx.x] = tm;
+        if (last_block_ticket(counter, gridDim.x)) {
+            double n = 0.0, m = 1e300;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                n += part[b];
+                m = fmin(m, part[kMaxPartials + b]);
+            }
+            out3[0] = n;
+            out3[1] = (double)(g.M - 2) * (double)(g.Ny - 2) * (double)(g.Nz - 2);
+            out3[2] = m;
+        }
+    }
+}
+
+cudaError_t launch_jacobian(VolGeom g, const float* phi_soa, float* det, double* part, double* out3,
+                            unsigned int* counter, cudaStream_t s) {
+    jacobian_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, phi_soa, det, part, out3, counter);
+    return cudaGetLastError();
+}
+
+// ---- building blocks -------------------------------------------------------------
+__global__ void warp_image_kernel(VolGeom g, const float* img, const float* disp, float* out) {
+    const long long N = g.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        out[i] = (float)trilinear(img, g.M, g.Ny, g.Nz, x + (double)disp[i], y + (double)disp[N + i],
+                                  z + (double)disp[2 * N + i]);
+    }
+}
+
+cudaError_t launch_warp_image(VolGeom g, const float* img, const float* disp, float* out, cudaStream_t s) {
+    warp_image_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, img, disp, out);
+    return cudaGetLastError();
+}
+
+__global__ void gradient_kernel(VolGeom g, const float* W, float* G) {
+    const long long N = g.N;
+    const size_t sy = (size_t)g.M, sz = (size_t)g.M * g.Ny;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        G[i] = (float)diff1(W, i, x, g.M, 1);
+        G[N + i] = (float)diff1(W, i, y, g.Ny, sy);
+        G[2 * N + i] = (float)diff1(W, i, z, g.Nz, sz);
+    }
+}
+
+cudaError_t launch_gradient(VolGeom g, const float* img, float* out, cudaStream_t s) {
+    gradient_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, img, out);
+    return cudaGetLastError();
+}
+
+__global__ void compose_kernel(VolGeom g, const float* phi, const float* V, float* out) {
+    const long long N = g.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, g.M, g.Ny, x, y, z);
+        const float v0 = V[i], v1 = V[N + i], v2 = V[2 * N + i];
+        double s[3];
+        trilinear3(phi, (size_t)N, g.M, g.Ny, g.Nz, x + (double)v0, y + (double)v1, z + (double)v2, s);
+        out[i] = (float)((double)v0 + s[0]);
+        out[N + i] = (float)((double)v1 + s[1]);
+        out[2 * N + i] = (float)((double)v2 + s[2]);
+    }
+}
+
+cudaError_t launch_compose(VolGeom g, const float* disp, const float* v, float* out, cudaStream_t s) {
+    compose_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, disp, v, out);
+    return cudaGetLastError();
+}
+
+template <int DT>
+__global__ void v_update_kernel(VolGeom g, const float* T, const float* W, const float* G, const float* WH,
+                                const float* BH, double theta, double eps, float* out) {
+    const long long N = g.N;
+    const double inv_theta = 1.0 / theta;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float wh[3] = {WH[i], WH[N + i], WH[2 * N + i]};
+        const float bh[3] = {BH[i], BH[N + i], BH[2 * N + i]};
+        const float gg[3] = {G[i], G[N + i], G[2 * N + i]};
+        float v[3];
+        v_update_voxel<DT>(wh, bh, gg, (double)W[i] - (double)T[i], theta, inv_theta, eps, v);
+        out[i] = v[0];
+        out[N + i] = v[1];
+        out[2 * N + i] = v[2];
+    }
+}
+
+cudaError_t launch_v_update(VolGeom g, int data_term, const float* target, const float* warped,
+                            const float* grad, const float* w_hat, const float* b_hat, double theta,
+                            double eps, float* out, cudaStream_t s) {
+    if (data_term == 1)
+        v_update_kernel<1><<<voxel_blocks(g.N), kVT, 0, s>>>(g, target, warped, grad, w_hat, b_hat, theta, eps, out);
+    else
+        v_update_kernel<2><<<voxel_blocks(g.N), kVT, 0, s>>>(g, target, warped, grad, w_hat, b_hat, theta, eps, out);
+    return cudaGetLastError();
+}
+
+__global__ void sad_kernel(VolGeom g, const float* a, const float* b, double* part, double* out,
+                           unsigned int* counter) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.N;
+         i += (long long)gridDim.x * blockDim.x)
+        s += fabs((double)a[i] - (double)b[i]);
+    const double t = block_sum<kVT>(s, red);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = t;
+        if (last_block_ticket(counter, gridDim.x)) {
+            double sum = 0.0;
+            for (unsigned k = 0; k < gridDim.x; ++k) sum += part[k];
+            *out = sum / (double)g.N;
+        }
+    }
+}
+
+cudaError_t launch_sad(VolGeom g, const float* a, const float* b, double* part, double* out,
+                       unsigned int* counter, cudaStream_t s) {
+    sad_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, a, b, part, out, counter);
+    return cudaGetLastError();
+}
+
+__global__ void minmax1_kernel(VolGeom g, const float* a, const float* b, float* part, unsigned int* counter) {
+    __shared__ double red[32];
+    float lo = FLT_MAX, hi = -FLT_MAX;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        lo = fminf(lo, fminf(a[i], b[i]));
+        hi = fmaxf(hi, fmaxf(a[i], b[i]));
+    }
+    const double tl = block_min<kVT>((double)lo, red);
+    const double th = -block_min<kVT>(-(double)hi, red);
+    if (threadIdx.x == 0) {
+        part[2 + 2 * blockIdx.x] = (float)tl;
+        part[3 + 2 * blockIdx.x] = (float)th;
+        if (last_block_ticket(counter, gridDim.x)) {
+            float l = FLT_MAX, h = -FLT_MAX;
+            for (unsigned k = 0; k < gridDim.x; ++k) {
+                l = fminf(l, part[2 + 2 * k]);
+                h = fmaxf(h, part[3 + 2 * k]);
+            }
+            part[0] = l;
+            part[1] = h;
+        }
+    }
+}
+
+__global__ void normalize1_kernel(VolGeom g, const float* a, const float* b, float* oa, float* ob,
+                                  const float* part) {
+    const double lo = part[0];
+    const double range = (double)part[1] - lo;
+    const double scale = range > 0.0 ? 1.0 / range : 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        oa[i] = (float)(((double)a[i] - lo) * scale);
+        ob[i] = (float)(((double)b[i] - lo) * scale);
+    }
+}
+
+cudaError_t launch_minmax_normalize(VolGeom g, const float* a, const float* b, float* oa, float* ob,
+                                    float* part, unsigned int* counter, cudaStream_t s) {
+    minmax1_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, a, b, part, counter);
+    normalize1_kernel<<<voxel_blocks(g.N), kVT, 0, s>>>(g, a, b, oa, ob, part);
+    return cudaGetLastError();
+}
+
+// registration.cpp:85-112: 2x2x2 mean with clamped (edge-replicated) reads
+__global__ void downsample_kernel(VolGeom gs, VolGeom gd, const float* in, float* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, gd.M, gd.Ny, x, y, z);
+        double sum = 0.0;
+        for (int dz = 0; dz < 2; ++dz)
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    const int xx = min(2 * x + dx, gs.M - 1), yy = min(2 * y + dy, gs.Ny - 1),
+                              zz = min(2 * z + dz, gs.Nz - 1);
+                    sum += in[xx + (size_t)gs.M * (yy + (size_t)gs.Ny * zz)];
+                }
+        out[i] = (float)(sum / 8.0);
+    }
+}
+
+cudaError_t launch_downsample(VolGeom src, VolGeom dst, const float* in, float* out, cudaStream_t s) {
+    downsample_kernel<<<voxel_blocks(dst.N), kVT, 0, s>>>(src, dst, in, out);
+    return cudaGetLastError();
+}
+
+// registration.cpp:114-135: corner-aligned trilinear resample, x2 on every component
+__device__ __forceinline__ double source_coord(int i, int te, int se) {
+    if (te <= 1) return 0.0;
+    return (double)i * (double)(se - 1) / (double)(te - 1);
+}
+
+__global__ void upsample_kernel(VolGeom gs, VolGeom gd, const float* in, float* out, int ncomp) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, gd.M, gd.Ny, x, y, z);
+        const double px = source_coord(x, gd.M, gs.M), py = source_coord(y, gd.Ny, gs.Ny),
+                     pz = source_coord(z, gd.Nz, gs.Nz);
+        for (int c = 0; c < ncomp; ++c)
+            out[(size_t)c * gd.N + i] = (float)(2.0 * trilinear(in + (size_t)c * gs.N, gs.M, gs.Ny, gs.Nz, px, py, pz));
+    }
+}
+
+cudaError_t launch_upsample(VolGeom src, VolGeom dst, const float* in, float* out, int ncomp, cudaStream_t s) {
+    upsample_kernel<<<voxel_blocks(dst.N), kVT, 0, s>>>(src, dst, in, out, ncomp);
+    return cudaGetLastError();
+}
+
+__global__ void aos_to_soa_kernel(long long N, const float* aos, float* soa) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        soa[i] = aos[3 * i];
+        soa[N + i] = aos[3 * i + 1];
+        soa[2 * N + i] = aos[3 * i + 2];
+    }
+}
+__global__ void soa_to_aos_kernel(long long N, const float* soa, float* aos) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        aos[3 * i] = soa[i];
+        aos[3 * i + 1] = soa[N + i];
+        aos[3 * i + 2] = soa[2 * N + i];
+    }
+}
+__global__ void add_kernel(long long n, const float* a, const float* b, float* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = a[i] + b[i];
+}
+
+cudaError_t launch_aos_to_soa(long long N, const float* aos, float* soa, cudaStream_t s) {
+    aos_to_soa_kernel<<<voxel_blocks(N), kVT, 0, s>>>(N, aos, soa);
+    return cudaGetLastError();
+}
+cudaError_t launch_soa_to_aos(long long N, const float* soa, float* aos, cudaStream_t s) {
+    soa_to_aos_kernel<<<voxel_blocks(N), kVT, 0, s>>>(N, soa, aos);
+    return cudaGetLastError();
+}
+cudaError_t launch_add(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
+    add_kernel<<<voxel_blocks(n), kVT, 0, s>>>(n, a, b, out);
+    return cudaGetLastError();
+}
+
+}  // namespace dregb

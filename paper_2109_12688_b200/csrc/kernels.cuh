@@ -1,0 +1,49 @@
+// Kernel argument blocks and launch declarations (dreg B200 path).
+#pragma once
+
+#include "common.cuh"
+
+namespace dregb {
+
+// Device-resident per-chunk state.  Every buffer is [pair][component][voxels]
+// (SoA planes) so each kernel's per-pair tile is a contiguous, coalesced range.
+struct Fields {
+    int M, Ny, Nz;     // grid (x fastest)
+    int hx;            // M/2 + 1 stored x bins
+    long long N;       // voxels
+    long long lines;   // Ny * Nz x-lines
+    float* V;          // v_k                 [P][3][N]
+    float* BH;         // b_hat_k             [P][3][N]
+    float* WP;         // w_{k-1} (w_prev)    [P][3][N]
+    float* BP;         // b_{k-1} (b_prev)    [P][3][N]
+    float* G;          // grad(warped)        [P][3][N]
+    float* D;          // warped - target     [P][N]
+    float2* S;         // x-spectrum, plane-major [P][3][hx][lines]
+    PairState* st;     // [P]
+    double* part;      // partial sums        [P][3][kMaxPartials]
+    double* diag;      // per-iteration diagnostics [P][max_iters][3] (nullable)
+    int diag_stride;   // max_iters
+};
+
+// Registration-level buffers.
+struct RegBuffers {
+    float* I0;          // smoothed normalised target [P][N]
+    float* I1;          // smoothed normalised source [P][N]
+    float* PHI[2];      // displacement SoA [P][3][N] x2
+    float* WARPED[2];   // warped level source [P][N] x2
+    const float* const* tgt_in;  // [P] raw target pointers (device)
+    const float* const* src_in;  // [P] raw source pointers (device)
+    float* const* phi_out;       // [P] SoA outputs (nullable entries)
+    float* const* warped_out;    // [P] (nullable entries)
+    float* tmpA;        // scratch [P][N]
+    float* tmpB;        // scratch [P][N]
+};
+
+struct SolverParams {
+    double theta, epsilon, lambda, tol;
+    int data_term, order;
+    int log_objective;
+    int accelerate;
+};
+
+}  // namespace dregb

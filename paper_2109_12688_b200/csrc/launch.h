@@ -1,0 +1,96 @@
+// Host-side launch interface between the engine (engine.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace dregb {
+
+// X_FIRST/SECOND/GENERAL: ADMM iteration k = 0 / 1 / >= 2; X_TAIL: w and residual of the
+// last iteration only (diagnostics); X_FWD: r2c of V (+ BH when add_bh) into S;
+// X_INV: c2r of S into WP.
+enum XMode { X_FIRST = 0, X_SECOND = 1, X_GENERAL = 2, X_TAIL = 3, X_FWD = 4, X_INV = 5 };
+
+struct XArgs {
+    Fields F;
+    AxisPlan px;        // line plan of length M/2 (M even) or M (M odd)
+    const float2* twx;  // W_L^e, e in [0, L)
+    const float2* xtw;  // W_M^k, k in [0, hx]
+    const int* xpos;    // position of frequency k in the digit-reversed line, k in [0, L)
+    SolverParams sp;
+    double coef;        // Nesterov coefficient c_{k-1} (admm.cpp:294-295)
+    int k;              // iteration index
+    int TL;             // x-lines per CTA
+    int PM;             // shared-memory line pitch (complex, odd)
+    int odd;            // M odd
+    int add_bh;         // X_FWD: transform V + BH instead of V
+};
+
+struct PArgs {
+    Fields F;
+    AxisPlan py, pz;
+    const float2* twy;
+    const float2* twz;
+    const float* sx;    // [hx]  1 - cos(2 pi p / M)
+    const float* sy;    // [Ny]  1 - cos(2 pi q / N) at digit-reversed positions
+    const float* sz;    // [Nz]
+    float lambda, theta, scale;  // scale = theta / voxels
+    int order;
+    int PY;             // plane row pitch (complex, odd)
+    int k;
+    int need_tail;
+    double* energy_out; // [P] (mode 1)
+};
+
+size_t xpass_smem_bytes(int L, int hx, int TL, int PM);
+size_t plane_smem_bytes(int Ny, int Nz, int PY);
+cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
+cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s);
+
+// ---- field kernels (field_kernels.cu) ----
+struct VolGeom {
+    int M, Ny, Nz;
+    long long N;
+};
+
+cudaError_t launch_state_reset(PairState* st, int npairs, cudaStream_t s);
+// diag[k].objective += lambda * energy (admm.cpp:288-292)
+cudaError_t launch_objective_accumulate(Fields F, const double* energy, double lambda, int k, int npairs,
+                                        cudaStream_t s);
+// Per-solve setup: grad(warped[cur]) and warped - target (volume.cpp:123-159).
+cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s);
+// compose + warp + SAD + accept/revert/stop (volume.cpp:161-181, registration.cpp:250-271)
+cudaError_t launch_compose_decide(VolGeom g, const RegBuffers& R, Fields F, double thr, int max_warps,
+                                  int npairs, cudaStream_t s);
+// normalise (registration.cpp:154-178) into R.tmpA (target) / R.tmpB (source)
+cudaError_t launch_prep_normalize(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s);
+// separable [1 2 1]/4 (registration.cpp:32-58): in -> out along axis, [P][N]
+cudaError_t launch_smooth_axis(VolGeom g, const float* in, float* out, int axis, int npairs, cudaStream_t s);
+// initial level state: phi = 0, warped = I1, sad_prev (registration.cpp:245-247)
+cudaError_t launch_level_init(VolGeom g, const RegBuffers& R, Fields F, int level, int npairs, cudaStream_t s);
+// final warp of the original source + finiteness of phi (registration.cpp:275-281)
+cudaError_t launch_finalize(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s);
+// Jacobian determinant + interior stats (volume.cpp:183-230, metrics.cpp:211-228)
+cudaError_t launch_jacobian(VolGeom g, const float* phi_soa, float* det, double* part, double* out3,
+                            unsigned int* counter, cudaStream_t s);
+
+// building blocks on single volumes (SoA device buffers)
+cudaError_t launch_warp_image(VolGeom g, const float* img, const float* disp, float* out, cudaStream_t s);
+cudaError_t launch_gradient(VolGeom g, const float* img, float* out, cudaStream_t s);
+cudaError_t launch_compose(VolGeom g, const float* disp, const float* v, float* out, cudaStream_t s);
+cudaError_t launch_v_update(VolGeom g, int data_term, const float* target, const float* warped,
+                            const float* grad, const float* w_hat, const float* b_hat, double theta,
+                            double eps, float* out, cudaStream_t s);
+cudaError_t launch_sad(VolGeom g, const float* a, const float* b, double* part, double* out,
+                       unsigned int* counter, cudaStream_t s);
+cudaError_t launch_minmax_normalize(VolGeom g, const float* a, const float* b, float* oa, float* ob,
+                                    float* part, unsigned int* counter, cudaStream_t s);
+cudaError_t launch_downsample(VolGeom src, VolGeom dst, const float* in, float* out, cudaStream_t s);
+cudaError_t launch_upsample(VolGeom src, VolGeom dst, const float* in, float* out, int ncomp,
+                            cudaStream_t s);
+cudaError_t launch_aos_to_soa(long long N, const float* aos, float* soa, cudaStream_t s);
+cudaError_t launch_soa_to_aos(long long N, const float* soa, float* aos, cudaStream_t s);
+cudaError_t launch_add(long long n, const float* a, const float* b, float* out, cudaStream_t s);
+
+}  // namespace dregb

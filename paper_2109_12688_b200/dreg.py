@@ -1,0 +1,370 @@
+"""Python mirror of the reference `dreg` hot-path API over the C ABI (include/dreg_cuda.h).
+
+Same function names, argument meaning and error behaviour as the reference C++
+library (proj/core/include/dreg/*.hpp):
+
+  ValueError    <- std::invalid_argument   (status DREG_INVALID_ARGUMENT)
+  NumericError  <- dreg::numeric_error     (status DREG_NUMERIC, errors.hpp:15-17)
+  RuntimeError  <- CUDA / allocation       (status DREG_RUNTIME)
+
+Volumes are numpy float32 arrays shaped (z, y, x) (x fastest, volume.hpp:10) and
+vector fields (z, y, x, 3) interleaved like the reference VectorField.  Every compute
+call runs sm_100a kernels from paper_2109_12688_b200/lib/libdreg_cuda.so; there is no
+CPU fallback -- a missing library or GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+from .abi import (  # noqa: F401  (re-exported config helpers)
+    DREG_PROFILE_CAPPED,
+    DREG_PROFILE_CONVERGED,
+    Dims3,
+    JacobianStats,
+    PairResult,
+    RegCfg,
+    SolverCfg,
+    Spacing3,
+    level_logs,
+    reg_cfg,
+    solver_cfg,
+)
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdreg_cuda.so")
+_F = C.POINTER(C.c_float)
+_D = C.POINTER(C.c_double)
+_lib = None
+
+
+class NumericError(RuntimeError):
+    """dreg::numeric_error: non-finite values produced or encountered."""
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library() -> C.CDLL:
+    """Load libdreg_cuda.so (built by __graft_entry__.build()); raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(_LIB_PATH)
+    P, V = C.c_void_p, C.c_void_p
+    L.dreg_cuda_ctx_create.argtypes = [C.c_int, C.POINTER(P)]
+    L.dreg_cuda_ctx_destroy.argtypes = [P]
+    L.dreg_cuda_ctx_destroy.restype = None
+    L.dreg_cuda_last_error.argtypes = [P]
+    L.dreg_cuda_last_error.restype = C.c_char_p
+    L.dreg_cuda_set_stream.argtypes = [P, V]
+    L.dreg_cuda_kernel_launches.argtypes = [P]
+    L.dreg_cuda_kernel_launches.restype = C.c_int64
+    L.dreg_cuda_set_batch_chunk.argtypes = [P, C.c_int]
+    L.dreg_cuda_set_use_graphs.argtypes = [P, C.c_int]
+    L.dreg_nesterov_next_alpha.argtypes = [C.c_double]
+    L.dreg_nesterov_next_alpha.restype = C.c_double
+    L.dreg_validate_solver_cfg.argtypes = [C.POINTER(SolverCfg)]
+    L.dreg_make_registration_config.argtypes = [C.c_int, C.POINTER(SolverCfg), C.c_int, C.POINTER(RegCfg)]
+    L.dreg_laplacian_symbol.argtypes = [C.c_int, Dims3, _D]
+    L.dreg_cuda_register_pair.argtypes = [P, _F, _F, Dims3, Spacing3, C.POINTER(RegCfg), _F, _F, C.POINTER(PairResult)]
+    L.dreg_cuda_register_batch.argtypes = [
+        P, C.c_int, C.POINTER(_F), C.POINTER(_F), Dims3, Spacing3, C.POINTER(RegCfg),
+        C.POINTER(_F), C.POINTER(_F), C.POINTER(PairResult),
+    ]
+    L.dreg_cuda_register_batch_device.argtypes = [
+        P, C.c_int, V, V, Dims3, Spacing3, C.POINTER(RegCfg), V, V, C.POINTER(PairResult),
+    ]
+    L.dreg_cuda_solve_velocity.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F, C.POINTER(abi.SolverDiag)]
+    L.dreg_cuda_v_update.argtypes = [P, _F, _F, _F, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
+    L.dreg_cuda_w_update.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
+    L.dreg_cuda_regulariser_energy.argtypes = [P, _F, Dims3, C.c_int, _D]
+    L.dreg_cuda_warp_image.argtypes = [P, _F, _F, Dims3, _F]
+    L.dreg_cuda_image_gradient.argtypes = [P, _F, Dims3, _F]
+    L.dreg_cuda_compose_deformation.argtypes = [P, _F, _F, Dims3, _F]
+    L.dreg_cuda_jacobian.argtypes = [P, _F, Dims3, _F, C.POINTER(JacobianStats)]
+    L.dreg_cuda_normalize_intensity_pair.argtypes = [P, _F, _F, Dims3, _F, _F]
+    L.dreg_cuda_binomial_smooth.argtypes = [P, _F, Dims3, _F]
+    L.dreg_cuda_mean_sad.argtypes = [P, _F, _F, Dims3, _D]
+    L.dreg_cuda_downsample.argtypes = [P, _F, Dims3, _F]
+    L.dreg_cuda_upsample_velocity.argtypes = [P, _F, Dims3, Dims3, _F]
+    _lib = L
+    return L
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(_F)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _raise(status: int, msg: str):
+    if status == abi.DREG_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == abi.DREG_NUMERIC:
+        raise NumericError(msg)
+    raise RuntimeError(msg or f"dreg_cuda status {status}")
+
+
+# ---- pure host helpers (no device work) --------------------------------------------
+def nesterov_next_alpha(alpha: float) -> float:
+    """admm.cpp:198-200."""
+    return load_library().dreg_nesterov_next_alpha(alpha)
+
+
+def validate(cfg: SolverCfg) -> None:
+    """admm.cpp:174-196: raises ValueError when a field is out of range."""
+    if load_library().dreg_validate_solver_cfg(C.byref(cfg)) != abi.DREG_OK:
+        raise ValueError("solver: invalid configuration")
+
+
+def make_registration_config(profile: int, solver: SolverCfg, levels: int = 3) -> RegCfg:
+    """registration.cpp:62-83."""
+    out = RegCfg()
+    if load_library().dreg_make_registration_config(profile, C.byref(solver), levels, C.byref(out)):
+        raise ValueError("registration: levels must be in [1, 8]")
+    return out
+
+
+def laplacian_symbol(order: int, dims) -> np.ndarray:
+    """regularizer.cpp:51-79 (full grid, fp64)."""
+    d = abi.dims3(dims)
+    out = np.zeros(d.shape(), np.float64)
+    if load_library().dreg_laplacian_symbol(order, d, out.ctypes.data_as(_D)):
+        raise ValueError("laplacian_symbol: order must be in [1, 6] and every axis >= 2")
+    return out
+
+
+class Context:
+    """One CUDA device context (dreg_cuda_ctx).  Not thread-safe; one per thread/GPU."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = C.c_void_p()
+        st = self.lib.dreg_cuda_ctx_create(int(device), C.byref(h))
+        if st != abi.DREG_OK:
+            raise RuntimeError(f"dreg_cuda_ctx_create(device={device}) failed with status {st} (no sm_100 GPU?)")
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.dreg_cuda_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st: int) -> None:
+        if st != abi.DREG_OK:
+            _raise(st, self.lib.dreg_cuda_last_error(self.h).decode())
+
+    # ---- context knobs ---------------------------------------------------------
+    def kernel_launches(self) -> int:
+        return int(self.lib.dreg_cuda_kernel_launches(self.h))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        self._check(self.lib.dreg_cuda_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def set_batch_chunk(self, pairs: int) -> None:
+        self._check(self.lib.dreg_cuda_set_batch_chunk(self.h, pairs))
+
+    def set_use_graphs(self, enable: bool) -> None:
+        self._check(self.lib.dreg_cuda_set_use_graphs(self.h, int(enable)))
+
+    # ---- hot path ----------------------------------------------------------------
+    def register_pair(self, target, source, cfg: RegCfg, spacing=(1.0, 1.0, 1.0)):
+        """registration.hpp:74-75 -> (phi (z,y,x,3), warped (z,y,x), PairResult)."""
+        target, source = _f32(target), _f32(source)
+        if target.shape != source.shape:
+            raise ValueError("register_pair: dimension mismatch")
+        phi = np.zeros(target.shape + (3,), np.float32)
+        warped = np.zeros_like(target)
+        res = PairResult()
+        self._check(
+            self.lib.dreg_cuda_register_pair(
+                self.h, _fp(target), _fp(source), abi.dims3(target), Spacing3(*spacing), C.byref(cfg),
+                _fp(phi), _fp(warped), C.byref(res),
+            )
+        )
+        return phi, warped, res
+
+    def register_batch(self, targets, sources, cfg: RegCfg, want_phi=True, want_warped=True, spacing=(1.0, 1.0, 1.0)):
+        """n independent registrations (same dims/cfg) from host buffers."""
+        targets = [_f32(t) for t in targets]
+        sources = [_f32(s) for s in sources]
+        n = len(targets)
+        if n == 0:
+            return [], [], []
+        shape = targets[0].shape
+        if any(t.shape != shape for t in targets) or any(s.shape != shape for s in sources):
+            raise ValueError("register_batch: dimension mismatch")
+        phis = [np.zeros(shape + (3,), np.float32) for _ in range(n)] if want_phi else None
+        warps = [np.zeros(shape, np.float32) for _ in range(n)] if want_warped else None
+        T = (_F * n)(*[_fp(t) for t in targets])
+        S = (_F * n)(*[_fp(s) for s in sources])
+        PO = (_F * n)(*[_fp(p) for p in phis]) if phis else None
+        WO = (_F * n)(*[_fp(w) for w in warps]) if warps else None
+        res = (PairResult * n)()
+        self._check(
+            self.lib.dreg_cuda_register_batch(
+                self.h, n, T, S, abi.dims3(shape), Spacing3(*spacing), C.byref(cfg), PO, WO, res
+            )
+        )
+        return phis, warps, list(res)
+
+    def register_batch_device(self, n: int, targets_ptr: int, sources_ptr: int, dims, cfg: RegCfg,
+                              phi_ptr: int = 0, warped_ptr: int = 0):
+        """Device-resident batch: [n][voxels] inputs, [n][3][voxels] SoA phi output."""
+        res = (PairResult * n)()
+        self._check(
+            self.lib.dreg_cuda_register_batch_device(
+                self.h, n, C.c_void_p(targets_ptr), C.c_void_p(sources_ptr), abi.dims3(dims), Spacing3(1, 1, 1),
+                C.byref(cfg), C.c_void_p(phi_ptr or 0), C.c_void_p(warped_ptr or 0), res,
+            )
+        )
+        return list(res)
+
+    def solve_velocity(self, target, warped_source, cfg: SolverCfg):
+        """admm.hpp:76-77 -> (velocity (z,y,x,3), diagnostics dict)."""
+        target, warped_source = _f32(target), _f32(warped_source)
+        if target.shape != warped_source.shape:
+            raise ValueError("solve_velocity: dimension mismatch")
+        v = np.zeros(target.shape + (3,), np.float32)
+        n = max(cfg.max_iters, 1)
+        obj = np.zeros(n, np.float64)
+        res = np.zeros(n, np.float64)
+        diag = abi.SolverDiag(0, 0.0, 0, obj.ctypes.data_as(_D), res.ctypes.data_as(_D))
+        self._check(
+            self.lib.dreg_cuda_solve_velocity(
+                self.h, _fp(target), _fp(warped_source), abi.dims3(target), C.byref(cfg), _fp(v), C.byref(diag)
+            )
+        )
+        it = diag.iterations
+        return v, {
+            "iterations": it,
+            "final_change": diag.final_change,
+            "converged": bool(diag.converged),
+            "objective": obj[:it].copy() if cfg.log_objective else np.zeros(0),
+            "constraint_residual": res[:it].copy(),
+        }
+
+    # ---- building blocks ---------------------------------------------------------
+    def v_update(self, target, warped, grad, w_hat, b_hat, cfg: SolverCfg) -> np.ndarray:
+        target, warped, grad, w_hat, b_hat = map(_f32, (target, warped, grad, w_hat, b_hat))
+        out = np.zeros_like(grad)
+        self._check(
+            self.lib.dreg_cuda_v_update(
+                self.h, _fp(target), _fp(warped), _fp(grad), _fp(w_hat), _fp(b_hat), abi.dims3(target),
+                C.byref(cfg), _fp(out),
+            )
+        )
+        return out
+
+    def v_update_l1(self, target, warped, grad, w_hat, b_hat, cfg: SolverCfg) -> np.ndarray:
+        c = SolverCfg.from_buffer_copy(cfg)
+        c.data_term = 1
+        return self.v_update(target, warped, grad, w_hat, b_hat, c)
+
+    def v_update_l2(self, target, warped, grad, w_hat, b_hat, cfg: SolverCfg) -> np.ndarray:
+        c = SolverCfg.from_buffer_copy(cfg)
+        c.data_term = 2
+        return self.v_update(target, warped, grad, w_hat, b_hat, c)
+
+    def w_update(self, v, b_hat, cfg: SolverCfg) -> np.ndarray:
+        v, b_hat = _f32(v), _f32(b_hat)
+        out = np.zeros_like(v)
+        self._check(self.lib.dreg_cuda_w_update(self.h, _fp(v), _fp(b_hat), abi.dims3(v), C.byref(cfg), _fp(out)))
+        return out
+
+    def regulariser_energy(self, w, order: int) -> float:
+        w = _f32(w)
+        out = C.c_double()
+        self._check(self.lib.dreg_cuda_regulariser_energy(self.h, _fp(w), abi.dims3(w), order, C.byref(out)))
+        return out.value
+
+    def warp_image(self, img, disp) -> np.ndarray:
+        img, disp = _f32(img), _f32(disp)
+        if disp.shape[:3] != img.shape:
+            raise ValueError("warp_image: dimension mismatch")
+        out = np.zeros_like(img)
+        self._check(self.lib.dreg_cuda_warp_image(self.h, _fp(img), _fp(disp), abi.dims3(img), _fp(out)))
+        return out
+
+    def image_gradient(self, img) -> np.ndarray:
+        img = _f32(img)
+        out = np.zeros(img.shape + (3,), np.float32)
+        self._check(self.lib.dreg_cuda_image_gradient(self.h, _fp(img), abi.dims3(img), _fp(out)))
+        return out
+
+    def compose_deformation(self, disp, v) -> np.ndarray:
+        disp, v = _f32(disp), _f32(v)
+        if disp.shape != v.shape:
+            raise ValueError("compose_deformation: dimension mismatch")
+        out = np.zeros_like(disp)
+        self._check(self.lib.dreg_cuda_compose_deformation(self.h, _fp(disp), _fp(v), abi.dims3(disp), _fp(out)))
+        return out
+
+    def jacobian_determinant(self, disp) -> np.ndarray:
+        disp = _f32(disp)
+        out = np.zeros(disp.shape[:3], np.float32)
+        self._check(self.lib.dreg_cuda_jacobian(self.h, _fp(disp), abi.dims3(disp), _fp(out), None))
+        return out
+
+    def jacobian_stats(self, disp) -> JacobianStats:
+        disp = _f32(disp)
+        st = JacobianStats()
+        self._check(self.lib.dreg_cuda_jacobian(self.h, _fp(disp), abi.dims3(disp), None, C.byref(st)))
+        return st
+
+    def normalize_intensity_pair(self, a, b):
+        a, b = _f32(a), _f32(b)
+        if a.shape != b.shape:
+            raise ValueError("normalize_intensity_pair: dimension mismatch")
+        oa, ob = np.zeros_like(a), np.zeros_like(b)
+        self._check(self.lib.dreg_cuda_normalize_intensity_pair(self.h, _fp(a), _fp(b), abi.dims3(a), _fp(oa), _fp(ob)))
+        return oa, ob
+
+    def binomial_smooth(self, img) -> np.ndarray:
+        img = _f32(img)
+        out = np.zeros_like(img)
+        self._check(self.lib.dreg_cuda_binomial_smooth(self.h, _fp(img), abi.dims3(img), _fp(out)))
+        return out
+
+    def mean_sad(self, a, b) -> float:
+        a, b = _f32(a), _f32(b)
+        if a.shape != b.shape:
+            raise ValueError("mean_sad: dimension mismatch")
+        out = C.c_double()
+        self._check(self.lib.dreg_cuda_mean_sad(self.h, _fp(a), _fp(b), abi.dims3(a), C.byref(out)))
+        return out.value
+
+    def downsample(self, img) -> np.ndarray:
+        img = _f32(img)
+        z, y, x = img.shape
+        out = np.zeros(((z + 1) // 2, (y + 1) // 2, (x + 1) // 2), np.float32)
+        self._check(self.lib.dreg_cuda_downsample(self.h, _fp(img), abi.dims3(img), _fp(out)))
+        return out
+
+    def upsample_velocity(self, v, dst_dims) -> np.ndarray:
+        v = _f32(v)
+        dd = abi.dims3(dst_dims)
+        out = np.zeros(dd.shape() + (3,), np.float32)
+        self._check(self.lib.dreg_cuda_upsample_velocity(self.h, _fp(v), abi.dims3(v), dd, _fp(out)))
+        return out

@@ -1,0 +1,231 @@
+"""GPU parity: the sm_100a path (C ABI via paper_2109_12688_b200.dreg) against the CPU
+oracle (oracle/dreg_oracle.c, itself pinned bit-exact to the unmodified reference in
+tests/test_oracle_pin.py) on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star): displacement fields max-abs <= 1e-3 voxel and
+relative L2 <= 1e-4; folding counts (det J <= 0) exactly equal.  Point-wise fp64
+building blocks are held to fp32 rounding (a few ulp); the fp32 spectral solve to
+1e-5 * max|ref| like the reference's own w-update pin (test_admm.cpp:184-211).
+"""
+import numpy as np
+import pytest
+
+from conftest import max_abs, random_field, random_volume, rel_l2, smooth_random_field
+from paper_2109_12688_b200 import abi, dreg, synth
+
+pytestmark = pytest.mark.gpu
+
+PHI_MAX_ABS = 1e-3
+PHI_REL_L2 = 1e-4
+
+
+def ulp_close(a, b, rel=4e-7, abs_=1e-30):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    tol = rel * np.maximum(np.abs(b), 1.0) + abs_
+    return bool(np.all(np.abs(a - b) <= tol))
+
+
+# ---- building blocks (volume.cpp / admm.cpp point-wise) ---------------------------
+@pytest.mark.parametrize("shape", [(8, 8, 8), (5, 7, 6), (16, 32, 24)])
+def test_warp_image(ctx, oracle, shape):
+    img = random_volume(shape, 21)
+    disp = random_field(shape, 22, 1.5)  # test_volume.cpp:79-97 (amplitude 1.5)
+    assert ulp_close(ctx.warp_image(img, disp), oracle.warp_image(img, disp))
+
+
+def test_identity_warp_bit_exact(ctx):
+    img = random_volume((8, 8, 8), 21)
+    out = ctx.warp_image(img, np.zeros(img.shape + (3,), np.float32))
+    assert np.array_equal(out, img)  # test_volume.cpp:72-77
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 8), (2, 3, 5), (16, 32, 24)])
+def test_image_gradient(ctx, oracle, shape):
+    img = random_volume(shape, 31)
+    assert ulp_close(ctx.image_gradient(img), oracle.image_gradient(img))
+
+
+def test_compose(ctx, oracle):
+    shape = (8, 8, 8)
+    a = smooth_random_field(shape, 51, 0.4, oracle)
+    b = smooth_random_field(shape, 52, 0.4, oracle)
+    assert ulp_close(ctx.compose_deformation(a, b), oracle.compose_deformation(a, b))
+    zero = np.zeros_like(b)
+    assert np.array_equal(ctx.compose_deformation(a, zero), a)  # test_volume.cpp:148-160
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 8), (16, 32, 24)])
+def test_jacobian(ctx, oracle, shape):
+    u = random_field(shape, 61, 0.6)
+    det = ctx.jacobian_determinant(u)
+    assert ulp_close(det, oracle.jacobian_determinant(u), rel=2e-6)
+    st, so = ctx.jacobian_stats(u), oracle.jacobian_stats(u)
+    assert st.nonpositive == so.nonpositive and st.interior == so.interior
+    assert abs(st.min_det - so.min_det) <= 1e-6 * max(1.0, abs(so.min_det))
+
+
+@pytest.mark.parametrize("data_term", [1, 2])
+@pytest.mark.parametrize("theta", [0.03, 0.12])
+def test_v_update(ctx, oracle, data_term, theta):
+    shape = (10, 10, 10)  # acceptance crit 2 (acceptance_main.cpp:120-159)
+    s0 = int(theta * 1000)
+    t, w = random_volume(shape, s0), random_volume(shape, s0 + 1)
+    g, wh, bh = random_field(shape, s0 + 2, 1.0), random_field(shape, s0 + 3, 1.0), random_field(shape, s0 + 4, 1.0)
+    cfg = abi.solver_cfg(data_term=data_term, theta=theta)
+    assert ulp_close(ctx.v_update(t, w, g, wh, bh, cfg), oracle.v_update(t, w, g, wh, bh, cfg), rel=1e-6)
+
+
+def test_normalize_smooth_sad(ctx, oracle):
+    a = random_volume((12, 20, 16), 71, -3.0, 7.0)
+    b = random_volume((12, 20, 16), 72, -1.0, 9.0)
+    oa, ob = ctx.normalize_intensity_pair(a, b)
+    ra, rb = oracle.normalize_intensity_pair(a, b)
+    assert np.array_equal(oa, ra) and np.array_equal(ob, rb)
+    assert ulp_close(ctx.binomial_smooth(a), oracle.binomial_smooth(a))
+    assert abs(ctx.mean_sad(a, b) - oracle.mean_sad(a, b)) <= 1e-12 * oracle.mean_sad(a, b)
+
+
+def test_downsample_upsample(ctx, oracle):
+    a = random_volume((9, 12, 7), 81)
+    assert ulp_close(ctx.downsample(a), oracle.downsample(a))
+    v = random_field((5, 6, 4), 82, 1.0)
+    assert ulp_close(ctx.upsample_velocity(v, (9, 11, 10)), oracle.upsample_velocity(v, (9, 11, 10)))
+
+
+# ---- spectral w-update (admm.cpp:66-101) -------------------------------------------
+W_SHAPES = [(4, 4, 4), (4, 6, 4), (4, 4, 5), (6, 5, 7), (8, 8, 8), (12, 10, 9), (16, 16, 16),
+            (32, 64, 64), (64, 128, 128), (30, 36, 42), (16, 20, 96)]
+
+
+@pytest.mark.parametrize("shape", W_SHAPES)
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_w_update(ctx, oracle, shape, order):
+    v = random_field(shape, 40 + order, 1.0)
+    bh = random_field(shape, 50 + order, 1.0)
+    cfg = abi.solver_cfg(order=order, lambda_=2.0, theta=0.1)
+    out, ref = ctx.w_update(v, bh, cfg), oracle.w_update(v, bh, cfg)
+    assert max_abs(out, ref) <= 1e-5 * np.abs(ref).max(), max_abs(out, ref)
+
+
+def test_w_update_lambda0_passthrough(ctx):
+    v, bh = random_field((6, 6, 6), 60, 1.0), random_field((6, 6, 6), 61, 1.0)
+    out = ctx.w_update(v, bh, abi.solver_cfg(order=2, lambda_=0.0, theta=0.1))
+    assert max_abs(out, v.astype(np.float64) + bh) <= 1e-5  # test_admm.cpp:213-227
+
+
+@pytest.mark.parametrize("shape", [(4, 4, 4), (6, 5, 7), (32, 64, 64)])
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_regulariser_energy(ctx, oracle, shape, order):
+    w = random_field(shape, 90 + order, 1.0)
+    e, r = ctx.regulariser_energy(w, order), oracle.regulariser_energy(w, order)
+    assert abs(e - r) <= 2e-6 * abs(r)
+
+
+# ---- solve_velocity (admm.cpp:252-314) ----------------------------------------------
+@pytest.mark.parametrize("data_term", [1, 2])
+@pytest.mark.parametrize("shape", [(16, 16, 16), (32, 64, 64)])
+def test_solve_velocity(ctx, oracle, data_term, shape):
+    f, m = synth.make_pair(1, 5, shape)
+    cfg = abi.solver_cfg(data_term=data_term, order=2, lambda_=0.1, theta=1.0, max_iters=50, log_objective=True)
+    v, d = ctx.solve_velocity(f, m, cfg)
+    vo, do = oracle.solve_velocity(f, m, cfg)
+    assert d["iterations"] == do["iterations"] == 50
+    assert max_abs(v, vo) <= PHI_MAX_ABS and rel_l2(v, vo) <= PHI_REL_L2, (max_abs(v, vo), rel_l2(v, vo))
+    assert np.allclose(d["constraint_residual"], do["constraint_residual"], rtol=1e-4, atol=1e-6)
+    assert np.allclose(d["objective"], do["objective"], rtol=1e-4, atol=1e-8)
+    assert abs(d["final_change"] - do["final_change"]) <= 1e-4 * max(do["final_change"], 1e-12)
+
+
+def test_solve_velocity_tol_early_exit(ctx, oracle):
+    f, m = synth.make_pair(1, 6, (16, 16, 16))
+    cfg = abi.solver_cfg(data_term=2, order=1, lambda_=2.0, theta=0.05, max_iters=200, tol=1e-4, log_objective=False)
+    v, d = ctx.solve_velocity(f, m, cfg)
+    vo, do = oracle.solve_velocity(f, m, cfg)
+    assert d["converged"] and do["converged"]
+    assert abs(d["iterations"] - do["iterations"]) <= 1
+    assert max_abs(v, vo) <= PHI_MAX_ABS
+
+
+def test_solve_identical_images_is_zero(ctx):
+    img = random_volume((12, 12, 12), 3)
+    cfg = abi.solver_cfg(data_term=1, order=1, lambda_=1.0, theta=0.1, max_iters=50, tol=1e-7)
+    v, d = ctx.solve_velocity(img, img, cfg)
+    assert np.abs(v).mean() <= 1e-4  # test_admm.cpp:250-266
+
+
+# ---- register_pair (registration.cpp:180-283), levels = 1 ----------------------------
+def _reg_parity(ctx, oracle, f, m, cfg):
+    phi, warped, res = ctx.register_pair(f, m, cfg)
+    phi_o, warped_o, res_o = oracle.register_pair(f, m, cfg)
+    assert res.status == 0
+    assert res.velocity_count == res_o.velocity_count
+    lg, lo = abi.level_logs(res)[0], abi.level_logs(res_o)[0]
+    assert lg["solver_iterations"] == lo["solver_iterations"]
+    assert np.allclose(lg["mean_sad"], lo["mean_sad"], rtol=1e-5, atol=1e-9)
+    assert max_abs(phi, phi_o) <= PHI_MAX_ABS, max_abs(phi, phi_o)
+    assert rel_l2(phi, phi_o) <= PHI_REL_L2, rel_l2(phi, phi_o)
+    assert ctx.jacobian_stats(phi).nonpositive == oracle.jacobian_stats(phi_o).nonpositive
+    assert max_abs(warped, warped_o) <= 1e-3
+    return phi, res
+
+
+@pytest.mark.parametrize("data_term", [1, 2])
+def test_register_small(ctx, oracle, data_term):
+    f, m = synth.make_pair(1, 7, (16, 32, 32))
+    s = abi.solver_cfg(data_term=data_term, order=2, lambda_=0.1, theta=1.0, max_iters=50, log_objective=False)
+    _reg_parity(ctx, oracle, f, m, abi.reg_cfg(s, 1, (5,), (50,)))
+
+
+def test_register_config1(ctx, oracle):
+    c = synth.CONFIGS["config1"]
+    f, m = synth.make_pair(c["synth"], c["seed"], c["shape"])
+    _reg_parity(ctx, oracle, f, m, synth.config_cfg("config1"))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_register_config2(ctx, oracle, order):
+    c = synth.CONFIGS["config2"]
+    f, m = synth.make_pair(c["synth"], c["seed"], c["shape"])
+    _reg_parity(ctx, oracle, f, m, synth.config_cfg("config2", order=order))
+
+
+def test_batch_matches_single_and_is_deterministic(ctx):
+    F, M = synth.make_batch(1, 300, 3, (16, 32, 32))
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=30, log_objective=False)
+    cfg = abi.reg_cfg(s, 1, (4,), (30,))
+    phis, warps, res = ctx.register_batch(list(F), list(M), cfg)
+    for i in range(3):
+        p1, w1, r1 = ctx.register_pair(F[i], M[i], cfg)
+        assert np.array_equal(p1, phis[i]) and np.array_equal(w1, warps[i])
+        assert r1.velocity_count == res[i].velocity_count
+    phis2, _, _ = ctx.register_batch(list(F), list(M), cfg)
+    assert all(np.array_equal(a, b) for a, b in zip(phis, phis2))
+
+
+def test_register_nonfinite_input_raises(ctx):
+    f, m = synth.make_pair(1, 8, (16, 16, 16))
+    m[3, 4, 5] = np.nan
+    s = abi.solver_cfg(data_term=2, max_iters=5)
+    with pytest.raises(dreg.NumericError):
+        ctx.register_pair(f, m, abi.reg_cfg(s, 1, (2,), (5,)))
+
+
+def test_register_invalid_config_raises(ctx):
+    f, m = synth.make_pair(1, 8, (16, 16, 16))
+    with pytest.raises(ValueError):
+        ctx.register_pair(f, m, abi.reg_cfg(abi.solver_cfg(data_term=3), 1, (2,), (5,)))
+    with pytest.raises(ValueError):
+        ctx.register_pair(f, m, abi.reg_cfg(abi.solver_cfg(theta=0.0), 1, (2,), (5,)))
+    with pytest.raises(ValueError):
+        ctx.register_pair(f, m, abi.reg_cfg(abi.solver_cfg(), 1, (2,), (5,), warp_improvement_threshold=1.5))
+    with pytest.raises(ValueError):
+        ctx.register_pair(f[:3], m[:3], abi.reg_cfg(abi.solver_cfg(), 1, (2,), (5,)))
+
+
+def test_identity_pair(ctx):
+    f, _ = synth.make_pair(1, 9, (32, 32, 32))
+    s = abi.solver_cfg(data_term=1, order=2, lambda_=5.0, theta=0.05, max_iters=10, log_objective=False)
+    phi, warped, res = ctx.register_pair(f, f, abi.reg_cfg(s, 1, (5,), (10,)))
+    assert np.abs(phi).mean() <= 0.05  # test_registration.cpp:197-210
