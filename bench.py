@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark: 3-D registrations/s on 64x128x128 fp32 pairs (BASELINE.json metric).
+
+Workload (config["workload"]): config-3 phantoms -- the config-2 cardiac-shaped pair
+(nested-ellipsoid ventricle, Rician noise, radial contraction + smooth displacement)
+with seeds 1000 + i -- registered with the config-2 solver (SSD data term, n = 2,
+lambda 0.1, theta (rho) 1.0, 7 composed velocity fields, 10 ADMM x 5 Nesterov = 50
+accelerated iterations per field, levels = 1).  A step registers `--pairs-per-gpu`
+pairs on every GPU (weak scaling; at 8 GPUs x 32 pairs it is config 3's 256 pairs).
+
+  value : registrations/s over all ranks, inputs resident in HBM before the timed
+          region (dreg_cuda_register_batch_device), L2 flushed between steps.
+  e2e   : same metric through the host-buffer C ABI (dreg_cuda_register_batch):
+          H2D of both volumes and D2H of phi (AoS) + warped image inside the timed region.
+  roofline: the dominant kernel (fused x-pass) timed with CUDA events on its stream,
+          algorithmic bytes / time vs MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline: the unmodified reference (oracle/_ref) on this box's host cores.
+
+`--impl reference` times the reference CPU implementation alone (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = (64, 128, 128)  # numpy (z, y, x) of "64x128x128" -> Dims3{128,128,64}
+METRIC = "3D registrations/sec (64x128x128 fp32)"
+UNIT = "registrations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--pairs-per-gpu", type=int, default=32)
+    ap.add_argument("--order", type=int, default=2)
+    ap.add_argument("--chunk", type=int, default=0, help="pairs per device launch (0 = auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    return ap.parse_args()
+
+
+def reg_cfg(order):
+    from paper_2109_12688_b200 import synth
+
+    return synth.config_cfg("config3", order=order)
+
+
+# ---- clocks -------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+# ---- CPU reference --------------------------------------------------------------------
+def cpu_reference_sample(order: int, threads: int, seed0: int = 1000):
+    """`threads` concurrent single-threaded reference solves (one config-2 velocity
+    field, 50 accelerated ADMM iterations each) on distinct config-3 pairs.
+    Returns (seconds, threads)."""
+    from oracle.oracle import CpuLib
+    from paper_2109_12688_b200 import abi, synth
+
+    ref = CpuLib("reference")
+    ref.set_threads(1)
+    F, M = synth.make_batch(3, seed0, threads, SHAPE)
+    cfg = reg_cfg(order).solver
+    s = abi.SolverCfg.from_buffer_copy(cfg)
+    s.log_objective = 0
+    # the solve runs on the normalised, smoothed pair exactly as inside register_pair
+    prepped = []
+    for i in range(threads):
+        a, b = ref.normalize_intensity_pair(F[i], M[i])
+        prepped.append((ref.binomial_smooth(a), ref.binomial_smooth(b)))
+    errs = []
+
+    def work(i):
+        try:
+            ref.solve_velocity(prepped[i][0], prepped[i][1], s)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    if errs:
+        raise errs[0]
+    return dt, threads
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle.oracle import available
+
+    cores = args.cpu_threads or os.cpu_count() or 1
+    cfgd = reg_cfg(args.order)
+    K = cfgd.max_warps_per_level[0]
+    if not available("reference"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdreg_ref.so not built"}))
+        return
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.order, cores)
+    times = []
+    for _ in range(args.steps):
+        dt, _ = cpu_reference_sample(args.order, cores)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = cores / (t * K)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t * 1000.0,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded config-3 phantoms)",
+        "config": {"workload": "config3 pairs (64x128x128), config-2 solver n=%d, 7 fields x 50 iterations" % args.order,
+                   "impl_detail": "unmodified reference core (oracle/_ref, FFTW3 API shim), one thread per pair"},
+        "cpu_baseline": {
+            "value": value,
+            "unit": UNIT,
+            "cores": cores,
+            "kind": "reference",
+            "sample": f"per step: {cores} concurrent single-threaded reference solve_velocity calls (one config-2 "
+                      f"velocity field, 50 accelerated ADMM iterations) on distinct pairs; registrations/s = "
+                      f"cores / (step_time x {K} fields per registration, the config's cap)",
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- our arm ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2109_12688_b200 import dreg, synth
+
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    B = args.pairs_per_gpu
+    N = SHAPE[0] * SHAPE[1] * SHAPE[2]
+    cfg = reg_cfg(args.order)
+    seeds0 = 1000 + (rank * B) % 256
+    F, M = synth.make_batch(3, seeds0, B, SHAPE)
+    tgt = torch.from_numpy(F.reshape(B, N)).to(dev)
+    src = torch.from_numpy(M.reshape(B, N)).to(dev)
+    phi = torch.empty((B, 3, N), dtype=torch.float32, device=dev)
+    warped = torch.empty((B, N), dtype=torch.float32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    ctx = dreg.Context(local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    if args.chunk:
+        ctx.set_batch_chunk(args.chunk)
+
+    def step():
+        res = ctx.register_batch_device(B, tgt.data_ptr(), src.data_ptr(), SHAPE[::-1], cfg,
+                                        phi.data_ptr(), warped.data_ptr())
+        return res
+
+    for _ in range(args.warmup):
+        res = step()
+        flush.zero_()
+    torch.cuda.synchronize(dev)
+    if dist:
+        tdist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    n0 = ctx.kernel_launches()
+    torch.cuda.synchronize(dev)
+    if dist:
+        tdist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        res = step()
+        if i + 1 < args.steps:
+            flush.zero_()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        tdist.barrier()
+    launches = ctx.kernel_launches() - n0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1000.0)
+
+    # per-pair records (status, velocity_count, solves, folding count, final SAD) -> NCCL all-gather
+    recs = []
+    for p in range(B):
+        js = ctx.jacobian_stats_device(phi[p].data_ptr(), SHAPE[::-1])
+        r = res[p]
+        lg = r.per_level[0]
+        recs.append([r.status, r.velocity_count, r.solves, js.nonpositive, lg.mean_sad[lg.warps], js.min_det])
+    rec = torch.tensor(recs, dtype=torch.float64, device=dev)
+    if dist:
+        allrec = torch.empty((world * B, rec.shape[1]), dtype=torch.float64, device=dev)
+        tdist.all_gather_into_tensor(allrec, rec)
+        rec = allrec
+    rec = rec.cpu().numpy()
+
+    # roofline of the dominant kernel (fused x-pass), CUDA events on the launching stream
+    tk = ctx.time_kernels(20)
+
+    # e2e through the host-buffer C ABI (pinned host memory)
+    e2e = None
+    if not args.no_e2e:
+        hT = torch.from_numpy(F.reshape(B, *SHAPE)).pin_memory()
+        hS = torch.from_numpy(M.reshape(B, *SHAPE)).pin_memory()
+        hP = torch.empty((B, *SHAPE, 3), dtype=torch.float32).pin_memory()
+        hW = torch.empty((B, *SHAPE), dtype=torch.float32).pin_memory()
+        tl, sl = [x.numpy() for x in hT], [x.numpy() for x in hS]
+        pl, wl = [x.numpy() for x in hP], [x.numpy() for x in hW]
+        import ctypes as C
+
+        from paper_2109_12688_b200 import abi
+
+        Fp = C.POINTER(C.c_float)
+        Ta = (Fp * B)(*[C.cast(a.ctypes.data, Fp) for a in tl])
+        Sa = (Fp * B)(*[C.cast(a.ctypes.data, Fp) for a in sl])
+        Pa = (Fp * B)(*[C.cast(a.ctypes.data, Fp) for a in pl])
+        Wa = (Fp * B)(*[C.cast(a.ctypes.data, Fp) for a in wl])
+        resb = (abi.PairResult * B)()
+
+        def estep():
+            st = ctx.lib.dreg_cuda_register_batch(ctx.h, B, Ta, Sa, abi.dims3(SHAPE[::-1]), abi.Spacing3(1, 1, 1),
+                                                  C.byref(cfg), Pa, Wa, resb)
+            ctx._check(st)
+
+        estep()
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        if dist:
+            tdist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            estep()  # synchronous: returns after the D2H of phi / warped completed
+            if i + 1 < args.steps:
+                flush.zero_()
+                torch.cuda.synchronize(dev)
+        et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if dist:
+            tdist.all_reduce(et, op=tdist.ReduceOp.MAX)
+        e2e = {
+            "value": world * B * args.steps / float(et.item()),
+            "unit": UNIT,
+            "h2d_bytes_per_step": B * 2 * N * 4,
+            "d2h_bytes_per_step": B * (3 * N + N) * 4,
+        }
+
+    if rank != 0:
+        return
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    achieved = tk["xpass_bytes"] / (tk["xpass_ms"] / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "xpass_dram_bytes.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            pj = json.load(f)
+        if pj.get("pairs"):
+            traffic = pj["dram_bytes_per_launch"] / pj["pairs"] * tk["pairs"]
+    it_ms = tk["xpass_ms"] + tk["plane_ms"]
+    solves = rec[:, 2]
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded config-3 phantoms, inputs generated on host then resident in HBM)",
+        "config": {
+            "workload": "config3 pairs at config-2 settings: 64x128x128, SSD, n=%d, lambda 0.1, theta 1.0, "
+                        "7 fields x 50 ADMM iterations, levels 1" % args.order,
+            "pairs_per_gpu_per_step": B,
+            "l2": "flushed between timed steps (512 MiB write); per-step working set >> L2",
+            "parallelism": f"pairs sharded over {world} GPU(s); NCCL all-gather of per-pair records only",
+        },
+        "gpu_launches": int(launches),
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "xpass (fused c2r + dual/Nesterov + v-update + r2c)",
+            "achieved": achieved,
+            "peak": peak,
+            "peak_source": peak_src,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "xpass_ms": tk["xpass_ms"],
+            "plane_ms": tk["plane_ms"],
+            "plane_GBps": tk["plane_bytes"] / (tk["plane_ms"] / 1e3) / 1e9,
+            "iteration_ms_per_pair": it_ms / tk["pairs"],
+            "iteration_frac": (tk["xpass_bytes"] + tk["plane_bytes"]) / (it_ms / 1e3) / 1e9 / peak,
+        },
+        "clocks": clk,
+        "e2e": e2e,
+        "pairs": {
+            "count": int(rec.shape[0]),
+            "status_ok": int((rec[:, 0] == 0).sum()),
+            "mean_velocity_count": float(rec[:, 1].mean()),
+            "mean_solves": float(solves.mean()),
+            "folding_voxels_total": int(rec[:, 3].sum()),
+            "mean_final_sad": float(rec[:, 4].mean()),
+            "min_det": float(rec[:, 5].min()),
+        },
+    }
+    if world == 1 and not args.no_cpu:
+        from oracle.oracle import available
+
+        if available("reference"):
+            cores = args.cpu_threads or os.cpu_count() or 1
+            dt, thr = cpu_reference_sample(args.order, cores)
+            S = float(solves.mean())
+            line["cpu_baseline"] = {
+                "value": thr / (dt * S),
+                "unit": UNIT,
+                "cores": thr,
+                "kind": "reference",
+                "sample": f"{thr} concurrent single-threaded reference solve_velocity calls (one velocity field, 50 "
+                          f"iterations) on distinct config-3 pairs took {dt:.2f} s; scaled by the {S:.2f} solves "
+                          f"per registration the GPU run executed on the same seeds",
+            }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as tdist
+
+            tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

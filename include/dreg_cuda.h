@@ -99,6 +99,7 @@ typedef struct {
 typedef struct {
     int status;          /* per-pair DREG_* status */
     int velocity_count;
+    int solves;          /* solve_velocity calls, including a reverted last one */
     int levels;
     dreg_level_log per_level[DREG_MAX_LEVELS];
     double elapsed_seconds;
@@ -170,6 +171,13 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* ctx, const float* target,
                              const dreg_solver_cfg* cfg, float* velocity_out,
                              dreg_solver_diag* diag);
 
+/* ---- measurement -----------------------------------------------------------------
+ * Times the two per-iteration kernels (fused x-pass, yz-plane spectral pass) on the
+ * current workspace (after a registration call), `reps` launches each, with CUDA
+ * events on the context stream.  out[0] = x-pass ms/launch, out[1] = plane ms/launch,
+ * out[2] / out[3] = their algorithmic HBM bytes per launch, out[4] = pairs per launch. */
+int dreg_cuda_time_kernels(dreg_cuda_ctx* ctx, int reps, double* out);
+
 /* ---- building blocks (host AoS buffers; each a GPU launch) ---------------------- */
 /* v_update_l1 / v_update_l2 (admm.hpp:49-58); data_term selects which */
 int dreg_cuda_v_update(dreg_cuda_ctx* ctx, const float* target, const float* warped_source,
@@ -193,6 +201,9 @@ int dreg_cuda_compose_deformation(dreg_cuda_ctx* ctx, const float* disp, const f
 /* jacobian_determinant (volume.hpp:125); det_out nullable; stats nullable */
 int dreg_cuda_jacobian(dreg_cuda_ctx* ctx, const float* disp, dreg_dims3 dims,
                        float* det_out, dreg_jacobian_stats* stats);
+/* Same on a device-resident SoA field [3][voxels] (e.g. register_batch_device output). */
+int dreg_cuda_jacobian_device(dreg_cuda_ctx* ctx, const float* disp_soa_dev, dreg_dims3 dims,
+                              float* det_dev_out, dreg_jacobian_stats* stats);
 /* normalize_intensity_pair (registration.hpp:65-66) */
 int dreg_cuda_normalize_intensity_pair(dreg_cuda_ctx* ctx, const float* a, const float* b,
                                        dreg_dims3 dims, float* out_a, float* out_b);

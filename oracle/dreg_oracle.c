@@ -689,7 +689,7 @@ int dro_register_pair(const float* target, const float* source, dreg_dims3 d,
     }
     float* phi = NULL;
     dreg_dims3 phi_dims = dims[0];
-    int velocity_count = 0;
+    int velocity_count = 0, solves = 0;
     st = DREG_OK;
     for (int l = 0; l < L && st == DREG_OK; ++l) {
         const dreg_dims3 dl = dims[l];
@@ -718,6 +718,7 @@ int dro_register_pair(const float* target, const float* source, dreg_dims3 d,
             dreg_solver_diag diag = {0, 0.0, 0, NULL, NULL};
             st = dro_solve_velocity(pt[l], warped, dl, &solver, v, &diag);
             if (st) break;
+            solves += 1;
             dro_compose_deformation(phi, v, dl, phi_c);
             dro_warp_image(ps[l], phi_c, dl, warped_c);
             const double sad_new = mean_sad(warped_c, pt[l], nl);
@@ -759,6 +760,7 @@ int dro_register_pair(const float* target, const float* source, dreg_dims3 d,
     if (res) {
         res->status = st;
         res->velocity_count = velocity_count;
+        res->solves = solves;
         res->elapsed_seconds = (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
     }
     return st;

@@ -98,6 +98,7 @@ class PairResult(C.Structure):
     _fields_ = [
         ("status", C.c_int),
         ("velocity_count", C.c_int),
+        ("solves", C.c_int),
         ("levels", C.c_int),
         ("per_level", LevelLog * DREG_MAX_LEVELS),
         ("elapsed_seconds", C.c_double),
@@ -116,7 +117,8 @@ class JacobianStats(C.Structure):
 
 
 def dims3(d) -> Dims3:
-    """Accept Dims3, (x, y, z) tuple, or a numpy array of shape (z, y, x)."""
+    """Accept Dims3, an (x, y, z) tuple (reference Dims3 order, NOT a numpy shape),
+    or a numpy array of shape (z, y, x) / (z, y, x, 3)."""
     if isinstance(d, Dims3):
         return d
     if hasattr(d, "shape"):

@@ -15,6 +15,7 @@
 #include "kernels.cuh"
 #include "launch.h"
 #include "pointwise.cuh"
+#include "plane_fast.cuh"
 
 namespace dregb {
 
@@ -73,7 +74,7 @@ __device__ __forceinline__ void stv(float* p, const float* in) {
 }
 
 template <int MODE, int DT, int VEC>
-__global__ void __launch_bounds__(kXThreads) xpass_kernel(XArgs a) {
+__global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArgs a) {
     const int pair = blockIdx.y;
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
@@ -104,6 +105,24 @@ __global__ void __launch_bounds__(kXThreads) xpass_kernel(XArgs a) {
     const float* G = a.F.G + (size_t)pair * 3 * N;
     const float* Dd = a.F.D + (size_t)pair * N;
     float2* S = a.F.S + (size_t)pair * 3 * hx * lines;
+
+    if (a.prefetch && (MODE == X_GENERAL || MODE == X_SECOND)) {
+        // Stream this tile's field rows into L2 while the spectrum loads and the
+        // inverse x-FFT run (cp.async.bulk.prefetch: no registers, no smem).
+        const unsigned bytes = (unsigned)(nl * M * sizeof(float));
+        const size_t off = (size_t)L0 * M;
+        if (tid < 16) {
+            const float* base;
+            const int f = tid / 3, c = tid - 3 * (tid / 3);
+            if (tid == 15) base = Dd + off;
+            else if (f == 0) base = V + (size_t)c * N + off;
+            else if (f == 1) base = G + (size_t)c * N + off;
+            else if (f == 2) base = (MODE == X_GENERAL ? BH : V) + (size_t)c * N + off;
+            else if (f == 3) base = (MODE == X_GENERAL ? WP : V) + (size_t)c * N + off;
+            else base = (MODE == X_GENERAL ? BP : V) + (size_t)c * N + off;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base), "r"(bytes) : "memory");
+        }
+    }
 
     // ---- phase 1: x c2r of the filtered spectrum -> w_{k-1} (real, in smem) ----
     if (MODE != X_FIRST && MODE != X_FWD) {
@@ -143,7 +162,7 @@ __global__ void __launch_bounds__(kXThreads) xpass_kernel(XArgs a) {
             }
             __syncthreads();
         }
-        fft_lines<true>(sm.buf, 3 * TL, PM, 1, a.px, sm.twx, tid, nthr);
+        fft_lines<true>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
     }
 
     if constexpr (UTIL) {
@@ -298,7 +317,7 @@ __global__ void __launch_bounds__(kXThreads) xpass_kernel(XArgs a) {
             }
         }
         __syncthreads();
-        fft_lines<false>(sm.buf, 3 * TL, PM, 1, a.px, sm.twx, tid, nthr);
+        fft_lines<false>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
         for (int idx = tid; idx < 3 * hx * TL; idx += nthr) {
             const int c = idx / (hx * TL);
             const int rem = idx - c * hx * TL;
@@ -404,8 +423,8 @@ __global__ void __launch_bounds__(kPThreads) plane_kernel(PArgs a) {
         }
     }
     __syncthreads();
-    fft_lines<false>(plane, Nz, PY, 1, a.py, twy, tid, nthr);  // y lines (rows)
-    fft_lines<false>(plane, Ny, 1, PY, a.pz, twz, tid, nthr);  // z lines (columns)
+    fft_lines<false>(plane, Nz, a.fd_nz, PY, 1, a.py, twy, tid, nthr);  // y lines (rows)
+    fft_lines<false>(plane, Ny, a.fd_ny, 1, PY, a.pz, twz, tid, nthr);  // z lines (columns)
 
     const float sxp = a.sx[p];
     if (MODE == 0) {
@@ -420,8 +439,8 @@ __global__ void __launch_bounds__(kPThreads) plane_kernel(PArgs a) {
             plane[z * PY + y] = make_float2(v.x * m, v.y * m);
         }
         __syncthreads();
-        fft_lines<true>(plane, Ny, 1, PY, a.pz, twz, tid, nthr);
-        fft_lines<true>(plane, Nz, PY, 1, a.py, twy, tid, nthr);
+        fft_lines<true>(plane, Ny, a.fd_ny, 1, PY, a.pz, twz, tid, nthr);
+        fft_lines<true>(plane, Nz, a.fd_nz, PY, 1, a.py, twy, tid, nthr);
         if ((Ny & 1) == 0) {
             const int half = Ny / 2;
             for (int idx = tid; idx < half * Nz; idx += nthr) {
@@ -461,28 +480,35 @@ __global__ void __launch_bounds__(kPThreads) plane_kernel(PArgs a) {
 }
 
 // ---- host launchers -----------------------------------------------------------
-template <int MODE>
-static cudaError_t launch_x_mode(const XArgs& a, int npairs, cudaStream_t s, int data_term, bool vec4) {
+template <int MODE, int DT>
+static cudaError_t launch_x_mode(const XArgs& a, int npairs, cudaStream_t s) {
     const dim3 grid((unsigned)((a.F.lines + a.TL - 1) / a.TL), (unsigned)npairs);
     const size_t smem = xpass_smem_bytes(a.px.n, a.F.hx, a.TL, a.PM);
-    void (*k)(XArgs);
-    if (data_term == 1) k = vec4 ? xpass_kernel<MODE, 1, 4> : xpass_kernel<MODE, 1, 1>;
-    else k = vec4 ? xpass_kernel<MODE, 2, 4> : xpass_kernel<MODE, 2, 1>;
+    int vec = a.vec;
+    if (vec == 4 && a.F.M % 4) vec = 2;
+    if (vec == 2 && a.F.M % 2) vec = 1;
+    void (*k)(XArgs) = vec == 4 ? xpass_kernel<MODE, DT, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2> : xpass_kernel<MODE, DT, 1>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     k<<<grid, kXThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
+template <int MODE>
+static cudaError_t launch_x_dt(const XArgs& a, int npairs, cudaStream_t s) {
+    return a.sp.data_term == 1 ? launch_x_mode<MODE, 1>(a, npairs, s) : launch_x_mode<MODE, 2>(a, npairs, s);
+}
+
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s) {
-    const bool vec4 = (a.F.M % 4) == 0;
     switch (mode) {
-        case X_FIRST: return launch_x_mode<X_FIRST>(a, npairs, s, a.sp.data_term, vec4);
-        case X_SECOND: return launch_x_mode<X_SECOND>(a, npairs, s, a.sp.data_term, vec4);
-        case X_GENERAL: return launch_x_mode<X_GENERAL>(a, npairs, s, a.sp.data_term, vec4);
-        case X_TAIL: return launch_x_mode<X_TAIL>(a, npairs, s, a.sp.data_term, vec4);
-        case X_FWD: return launch_x_mode<X_FWD>(a, npairs, s, 2, false);
-        default: return launch_x_mode<X_INV>(a, npairs, s, 2, false);
+        case X_FIRST: return launch_x_dt<X_FIRST>(a, npairs, s);
+        case X_SECOND: return launch_x_dt<X_SECOND>(a, npairs, s);
+        case X_GENERAL: return launch_x_dt<X_GENERAL>(a, npairs, s);
+        case X_TAIL: return launch_x_dt<X_TAIL>(a, npairs, s);
+        case X_FWD: return launch_x_mode<X_FWD, 2>(a, npairs, s);
+        default: return launch_x_mode<X_INV, 2>(a, npairs, s);
     }
 }
 
@@ -490,11 +516,56 @@ size_t plane_smem_bytes(int Ny, int Nz, int PY) {
     return sizeof(float2) * ((size_t)PY * Nz + Ny + Nz) + sizeof(float) * (Ny + Nz + 2) + sizeof(double) * 32 + 16;
 }
 
+int plane_fast_r1(int n) {
+    switch (n) {
+        case 16: return 4;
+        case 32: return 4;
+        case 64: return 8;
+        case 128: return 8;
+        case 256: return 16;
+        default: return 0;
+    }
+}
+
+template <int NY, int NZ>
+static cudaError_t launch_fast(const PArgs& a, int mode, int npairs, cudaStream_t s) {
+    constexpr int R1Y = NY == 256 ? 16 : (NY >= 64 ? 8 : 4);
+    constexpr int R1Z = NZ == 256 ? 16 : (NZ >= 64 ? 8 : 4);
+    constexpr int NT = 256;
+    using Lay = PlaneLayout<NY, NY / R1Y>;
+    const size_t smem = sizeof(float2) * NZ * Lay::P + sizeof(double) * 32;
+    void (*k)(PArgs) = mode == 0 ? plane_fast_kernel<NY, NZ, R1Y, R1Z, NT, 0> : plane_fast_kernel<NY, NZ, R1Y, R1Z, NT, 1>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    k<<<dim3((unsigned)(3 * a.F.hx), (unsigned)npairs), NT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define DREG_FAST_CASES(X) \
+    X(32, 16) X(32, 32) X(32, 64) X(32, 128) X(64, 16) X(64, 32) X(64, 64) X(64, 128) \
+    X(128, 16) X(128, 32) X(128, 64) X(128, 128) X(256, 16) X(256, 32) X(256, 64)
+
+bool plane_fast_supported(int Ny, int Nz) {
+#define X(a, b) if (Ny == a && Nz == b) return true;
+    DREG_FAST_CASES(X)
+#undef X
+    return false;
+}
+
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s) {
+    if (a.fast) {
+#define X(ny, nz) if (a.F.Ny == ny && a.F.Nz == nz) return launch_fast<ny, nz>(a, mode, npairs, s);
+        DREG_FAST_CASES(X)
+#undef X
+    }
     const dim3 grid((unsigned)(3 * a.F.hx), (unsigned)npairs);
     const size_t smem = plane_smem_bytes(a.F.Ny, a.F.Nz, a.PY);
     void (*k)(PArgs) = mode == 0 ? plane_kernel<0> : plane_kernel<1>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     k<<<grid, kPThreads, smem, s>>>(a);
     return cudaGetLastError();

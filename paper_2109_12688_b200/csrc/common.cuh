@@ -15,12 +15,28 @@ constexpr int kMaxPartials = 4096;  // per-pair partial-sum slots per reduction
 // Per-axis line-FFT plan (host-built, passed by value).  Stage s of the DIF
 // forward transform uses radix[s] on sub-blocks of n1[s]*radix[s] elements;
 // twiddle W_{n_s}^{j1 k} = W_n^{j1 k tws[s]} is read from the axis table.
+// Division by a run-time constant via multiply-high (valid for x < 2^31).
+struct FastDiv {
+    unsigned int d, mul, shift;
+    void init(unsigned int dv) {
+        d = dv;
+        unsigned int l = 0;
+        while ((1u << l) < dv) ++l;
+        mul = (unsigned int)((((unsigned long long)1 << 32) * (((unsigned long long)1 << l) - dv)) / dv + 1);
+        shift = l;
+    }
+    __device__ __forceinline__ unsigned int div(unsigned int x) const {
+        return (__umulhi(x, mul) + x) >> shift;
+    }
+};
+
 struct AxisPlan {
     int n;
     int nst;
     int radix[kMaxStages];
     int n1[kMaxStages];
     int tws[kMaxStages];
+    FastDiv fn1[kMaxStages];
 };
 
 // Per-pair device state driving the warp loop of register_pair
@@ -34,6 +50,7 @@ struct PairState {
     int velocity_count;  // registration.hpp:42
     int warps;           // accepted warps at the current level
     int level;
+    int solves;            // compose/decide passes (= solve_velocity calls)
     unsigned int counter;  // last-block reduction ticket
     int done_iter;         // iteration at which solve_done was raised
     double sad_prev;

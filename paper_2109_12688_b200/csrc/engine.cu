@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -96,6 +97,7 @@ AxisPlan make_plan(int n) {
     for (int i = 0; i < s; ++i) {
         P.n1[i] = ns / P.radix[i];
         P.tws[i] = n / ns;
+        P.fn1[i].init((unsigned)P.n1[i]);
         ns = P.n1[i];
     }
     return P;
@@ -111,6 +113,11 @@ int freq_of_pos(const AxisPlan& P, int pos) {
         mult *= P.radix[s];
     }
     return f;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
 }
 
 float2 w_of(long num, long den) {  // exp(-2 pi i num/den), computed in double
@@ -130,11 +137,12 @@ float one_minus_cos(int k, int n) {  // 1 - cos(2 pi k / n) = 2 sin^2(pi k / n);
 struct Geometry {
     int M = 0, Ny = 0, Nz = 0, hx = 0;
     long long N = 0, lines = 0;
-    int L = 0, odd = 0, TL = 0, PM = 0, PY = 0;
+    int L = 0, odd = 0, TL = 0, PM = 0, PY = 0, xvec = 1;
     AxisPlan px{}, py{}, pz{};
     DevArray<float2> twx, xtw, twy, twz;
     DevArray<int> xpos;
-    DevArray<float> sx, sy, sz;
+    DevArray<float> sx, sy, sz, sy_fast, sz_fast;
+    int fast = 0, prefetch = 1;
     size_t xsmem = 0, psmem = 0;
 
     void build(dreg_dims3 d) {
@@ -151,7 +159,8 @@ struct Geometry {
         pz = make_plan(Nz);
         PM = (L % 2 == 0) ? L + 1 : L;
         PY = (Ny % 2 == 0) ? Ny + 1 : Ny;
-        TL = 32;
+        TL = env_int("DREG_TL", 32);
+        xvec = env_int("DREG_XVEC", 2);
         while (TL > 4 && xpass_smem_bytes(L, hx, TL, PM) > 110 * 1024) TL /= 2;
         xsmem = xpass_smem_bytes(L, hx, TL, PM);
         psmem = plane_smem_bytes(Ny, Nz, PY);
@@ -185,6 +194,28 @@ struct Geometry {
         s.assign(Nz, 0.f);
         for (int pos = 0; pos < Nz; ++pos) s[pos] = one_minus_cos(freq_of_pos(pz, pos), Nz);
         up(sz, s);
+        fast = plane_fast_supported(Ny, Nz) && env_int("DREG_FAST_PLANE", 1);
+        prefetch = env_int("DREG_PREFETCH", 1);
+        if (fast) {
+            // tables for the two-stage split R1 x R2 of the specialised kernel
+            auto split = [](int n) {
+                AxisPlan q{};
+                q.n = n;
+                q.nst = 2;
+                q.radix[0] = plane_fast_r1(n);
+                q.radix[1] = n / q.radix[0];
+                q.n1[0] = q.radix[1];
+                q.n1[1] = 1;
+                return q;
+            };
+            const AxisPlan fy = split(Ny), fz = split(Nz);
+            s.assign(Ny, 0.f);
+            for (int pos = 0; pos < Ny; ++pos) s[pos] = one_minus_cos(freq_of_pos(fy, pos), Ny);
+            up(sy_fast, s);
+            s.assign(Nz, 0.f);
+            for (int pos = 0; pos < Nz; ++pos) s[pos] = one_minus_cos(freq_of_pos(fz, pos), Nz);
+            up(sz_fast, s);
+        }
     }
 
     template <class T>
@@ -456,6 +487,9 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag) {
     a.TL = w.geo.TL;
     a.PM = w.geo.PM;
     a.odd = w.geo.odd;
+    a.vec = w.geo.xvec;
+    a.prefetch = w.geo.prefetch && (w.geo.M % 4 == 0);
+    a.fd_lines.init((unsigned)(3 * w.geo.TL));
     return a;
 }
 
@@ -475,6 +509,11 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag) {
     p.order = sp.order;
     p.PY = w.geo.PY;
     p.energy_out = w.energy.p;
+    p.sy_fast = w.geo.sy_fast.p;
+    p.sz_fast = w.geo.sz_fast.p;
+    p.fast = w.geo.fast;
+    p.fd_ny.init((unsigned)w.geo.Ny);
+    p.fd_nz.init((unsigned)w.geo.Nz);
     return p;
 }
 
@@ -511,7 +550,7 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     if (log_obj) {
         energy(0);
         xa.k = 0;
-        xa.add_bh = 1;
+        xa.add_bh = 0;  // b_hat_0 = 0 is implicit (never stored): u_0 = v_0
         L(launch_xpass(xa, X_FWD, P, st));  // restore S = r2c(u_0)
         L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, 0, P, st));
     }
@@ -632,6 +671,7 @@ void fill_results(const PairState* hs, int P, const Workspace& w, dreg_pair_resu
         const PairState& s = hs[p];
         r.status = s.status;
         r.velocity_count = s.velocity_count;
+        r.solves = s.solves;
         r.levels = 1;
         dreg_level_log& lg = r.per_level[0];
         lg.dims = {w.geo.M, w.geo.Ny, w.geo.Nz};
@@ -940,6 +980,58 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
     });
 }
 
+// ---- measurement ----------------------------------------------------------------
+int dreg_cuda_time_kernels(dreg_cuda_ctx* c, int reps, double* out) {
+    return guarded(c, [&] {
+        if (!c->ws) throw ArgFail("time_kernels: no workspace yet (run a registration first)");
+        if (reps < 1 || !out) throw ArgFail("time_kernels: reps >= 1 and out required");
+        Workspace& w = *c->ws;
+        const int P = w.P;
+        cudaStream_t st = c->stream;
+        dreg_solver_cfg s;
+        dreg_solver_cfg_default(&s);
+        s.data_term = 2;
+        s.lambda = 0.1;
+        s.theta = 1.0;
+        const SolverParams sp = solver_params(s);
+        XArgs xa = make_xargs(w, sp, false);
+        xa.k = 5;
+        xa.coef = 0.5;
+        PArgs pa = make_pargs(w, sp, false);
+        Launcher L{c};
+        L(launch_state_reset(w.st.p, P, st));
+        cudaEvent_t e[4];
+        for (auto& ev : e) CK(cudaEventCreate(&ev));
+        // warm-up
+        L(launch_plane(pa, 0, P, st));
+        L(launch_xpass(xa, X_GENERAL, P, st));
+        float tx = 0.f, tp = 0.f;
+        for (int r = 0; r < reps; ++r) {
+            CK(cudaEventRecord(e[0], st));
+            L(launch_plane(pa, 0, P, st));
+            CK(cudaEventRecord(e[1], st));
+            L(launch_xpass(xa, X_GENERAL, P, st));
+            CK(cudaEventRecord(e[2], st));
+            CK(cudaEventSynchronize(e[2]));
+            float a = 0.f, b = 0.f;
+            CK(cudaEventElapsedTime(&a, e[0], e[1]));
+            CK(cudaEventElapsedTime(&b, e[1], e[2]));
+            tp += a;
+            tx += b;
+        }
+        for (auto& ev : e) cudaEventDestroy(ev);
+        c->launches += L.count;
+        const double N = (double)w.geo.N;
+        const double spec = 2.0 * 3.0 * (double)w.geo.hx * (double)w.geo.lines * 8.0;  // read + write
+        out[0] = tx / reps;
+        out[1] = tp / reps;
+        out[2] = P * (28.0 * 4.0 * N + spec);  // 16 field words read + 12 written, spectrum in/out
+        out[3] = P * spec;
+        out[4] = P;
+        return DREG_OK;
+    });
+}
+
 // ---- building blocks ------------------------------------------------------------
 static void upload_aos(dreg_cuda_ctx* c, Workspace& w, const float* host_aos, float* dev_soa) {
     const size_t N = (size_t)w.geo.N;
@@ -1077,6 +1169,28 @@ int dreg_cuda_jacobian(dreg_cuda_ctx* c, const float* disp, dreg_dims3 d, float*
         double h[3];
         CK(cudaMemcpyAsync(h, w.scal.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         if (det_out) CK(cudaMemcpyAsync(det_out, w.W0.p, sizeof(float) * N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (stats) {
+            stats->nonpositive = (int64_t)h[0];
+            stats->interior = (int64_t)h[1];
+            stats->min_det = h[2];
+            stats->pct_nonpositive = 100.0 * h[0] / h[1];
+        }
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_jacobian_device(dreg_cuda_ctx* c, const float* disp, dreg_dims3 d, float* det_out,
+                              dreg_jacobian_stats* stats) {
+    return guarded(c, [&] {
+        check_dims(d, 3, "jacobian_determinant");
+        if (!disp) throw ArgFail("null field");
+        Workspace& w = c->workspace(d, 1);
+        const VolGeom g{d.x, d.y, d.z, (long long)d.x * d.y * d.z};
+        CK(launch_jacobian(g, disp, det_out, w.part.p, w.scal.p, w.counter.p, c->stream));
+        c->launches += 1;
+        double h[3];
+        CK(cudaMemcpyAsync(h, w.scal.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (stats) {
             stats->nonpositive = (int64_t)h[0];

@@ -153,7 +153,7 @@ __device__ void butterfly_dyn(float2* p, int step, int j1, int tws, const float2
 // Batched in-place line transform over `nlines` lines.  All threads of the block
 // participate; ends with __syncthreads().
 template <bool INV>
-__device__ void fft_lines(float2* buf, int nlines, int ls, int es, const AxisPlan& P,
+__device__ void fft_lines(float2* buf, int nlines, const FastDiv& fdl, int ls, int es, const AxisPlan& P,
                           const float2* __restrict__ tw, int tid, int nthr) {
     for (int si = 0; si < P.nst; ++si) {
         const int s = INV ? P.nst - 1 - si : si;
@@ -162,10 +162,11 @@ __device__ void fft_lines(float2* buf, int nlines, int ls, int es, const AxisPla
         const int nb = P.n / r;
         const int total = nlines * nb;
         const int step = n1 * es;
+        const FastDiv fd1 = P.fn1[s];
         for (int w = tid; w < total; w += nthr) {
-            const int line = w % nlines;
-            const int b = w / nlines;
-            const int blk = b / n1;
+            const int b = (int)fdl.div((unsigned)w);
+            const int line = w - b * nlines;
+            const int blk = (int)fd1.div((unsigned)b);
             const int j1 = b - blk * n1;
             float2* p = buf + line * ls + (blk * ns + j1) * es;
             switch (r) {

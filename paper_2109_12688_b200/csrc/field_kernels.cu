@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kVT) compose_decide_kernel(VolGeom g, RegBuffe
                 st->active = 0;
                 return;
             }
+            st->solves += 1;
             const double sad_new = sum / (double)N;
             const int lvl = st->level;
             if (sad_new > st->sad_prev) {  // revert (registration.cpp:256-258)
@@ -218,6 +219,7 @@ __global__ void state_reset_kernel(PairState* st, int npairs) {
     s.velocity_count = 0;
     s.warps = 0;
     s.level = 0;
+    s.solves = 0;
     s.counter = 0;
     s.done_iter = -1;
     s.sad_prev = 0.0;

@@ -25,6 +25,9 @@ struct XArgs {
     int PM;             // shared-memory line pitch (complex, odd)
     int odd;            // M odd
     int add_bh;         // X_FWD: transform V + BH instead of V
+    int vec;            // point-wise vector width (1, 2 or 4; 4/2 need M % 4 / M % 2 == 0)
+    int prefetch;       // L2 bulk prefetch of the tile's field rows at kernel start
+    FastDiv fd_lines;   // divide by 3 * TL
 };
 
 struct PArgs {
@@ -35,16 +38,23 @@ struct PArgs {
     const float* sx;    // [hx]  1 - cos(2 pi p / M)
     const float* sy;    // [Ny]  1 - cos(2 pi q / N) at digit-reversed positions
     const float* sz;    // [Nz]
+    const float* sy_fast;  // [Ny] position table of the specialised plane kernel (radix split R1 x R2)
+    const float* sz_fast;  // [Nz]
+    int fast;              // use plane_fast_kernel
     float lambda, theta, scale;  // scale = theta / voxels
     int order;
     int PY;             // plane row pitch (complex, odd)
     int k;
     int need_tail;
     double* energy_out; // [P] (mode 1)
+    FastDiv fd_ny, fd_nz;
 };
 
 size_t xpass_smem_bytes(int L, int hx, int TL, int PM);
 size_t plane_smem_bytes(int Ny, int Nz, int PY);
+// radix split used by the specialised plane kernel for an axis of length n (0 = unsupported)
+int plane_fast_r1(int n);
+bool plane_fast_supported(int Ny, int Nz);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s);
 

@@ -1,0 +1,213 @@
+// Compile-time-specialised yz-plane spectral kernel (the w-update core,
+// admm.cpp:83-95) for power-of-two planes that fit one CTA's shared memory.
+//
+// Each axis transform is two register-resident DIF stages (radix R1, then R2 on
+// contiguous blocks), so a plane makes 6 shared-memory round trips per w-update:
+//   global -> [y1] -> smem -> [y2] -> smem -> [z1] -> smem
+//          -> [z2 * m z2^-1] -> smem -> [z1^-1] -> smem -> [y2^-1] -> smem -> [y1^-1] -> global
+// The forward z2 stage, the regulariser multiply and the adjoint z2 stage touch the
+// same elements, so they fuse in registers.  Outputs stay digit-reversed between the
+// forward and adjoint halves; the multiplier is indexed through position tables.
+//
+// Shared layout: element (y, z) at z*P + y + y/R2y, P = NY + NY/R2y rounded to 8 mod 16
+// complex: conflict-free for the strided stage-1 rows, the contiguous stage-2 blocks
+// (one pad per block) and for column access (consecutive y per half-warp).
+#pragma once
+
+#include "fft_device.cuh"
+#include "launch.h"
+
+namespace dregb {
+
+template <bool INV>
+__device__ __forceinline__ float2 cmul_tw(float2 a, float2 w) {
+    return INV ? cmulc(a, w) : cmul(a, w);
+}
+
+// 16-point DFT in natural order: j = j1 + 4 j2, k = k2 + 4 k1.
+template <bool INV>
+__device__ __forceinline__ void dft16(float2* x) {
+    constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
+    constexpr float h = 0.70710678118654752440f;
+    // W16^e, e = 0..9 (forward sign)
+    const float2 W[10] = {{1.f, 0.f}, {c1, -s1}, {h, -h}, {s1, -c1}, {0.f, -1.f},
+                          {-s1, -c1}, {-h, -h}, {-c1, -s1}, {-1.f, 0.f}, {-c1, s1}};
+    float2 a[4][4];
+#pragma unroll
+    for (int j1 = 0; j1 < 4; ++j1) {
+#pragma unroll
+        for (int j2 = 0; j2 < 4; ++j2) a[j1][j2] = x[j1 + 4 * j2];
+        dft4<INV>(a[j1]);
+    }
+#pragma unroll
+    for (int j1 = 1; j1 < 4; ++j1)
+#pragma unroll
+        for (int k2 = 1; k2 < 4; ++k2) a[j1][k2] = cmul_tw<INV>(a[j1][k2], W[j1 * k2]);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+        float2 b[4] = {a[0][k2], a[1][k2], a[2][k2], a[3][k2]};
+        dft4<INV>(b);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) x[k2 + 4 * k1] = b[k1];
+    }
+}
+
+template <bool INV, int R>
+__device__ __forceinline__ void rdft(float2* x) {
+    if constexpr (R == 2) dft2<INV>(x);
+    else if constexpr (R == 4) dft4<INV>(x);
+    else if constexpr (R == 8) dft8<INV>(x);
+    else dft16<INV>(x);
+}
+
+template <int NY, int R2Y>
+struct PlaneLayout {
+    static constexpr int base = NY + NY / R2Y;
+    static constexpr int P = base + ((8 - (base % 16) + 16) % 16);
+    __device__ static __forceinline__ int at(int y, int z) { return z * P + y + y / R2Y; }
+};
+
+template <int NY, int NZ, int R1Y, int R1Z, int NT, int MODE>
+__global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kernel(PArgs a) {
+    constexpr int R2Y = NY / R1Y, R2Z = NZ / R1Z;
+    using Lay = PlaneLayout<NY, R2Y>;
+    const int pair = blockIdx.y;
+    PairState* st = a.F.st + pair;
+    if (!st->active || st->status) return;
+    if (st->solve_done && (!a.need_tail || a.k > st->done_iter)) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* buf = reinterpret_cast<float2*>(smem);
+    double* red = reinterpret_cast<double*>(buf + NZ * Lay::P);
+    const int tid = threadIdx.x;
+    const int hx = a.F.hx;
+    const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
+    float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)a.F.lines;
+    const float2* __restrict__ twy = a.twy;
+    const float2* __restrict__ twz = a.twz;
+
+    // y stage 1 (DIF radix R1Y, n1 = R2Y), straight from global
+#pragma unroll 2
+    for (int b = tid; b < NZ * R2Y; b += NT) {
+        const int j1 = b % R2Y, z = b / R2Y;
+        float2 x[R1Y];
+#pragma unroll
+        for (int t = 0; t < R1Y; ++t) x[t] = __ldg(Sp + z * NY + j1 + R2Y * t);
+        rdft<false, R1Y>(x);
+#pragma unroll
+        for (int k = 1; k < R1Y; ++k) x[k] = cmul(x[k], __ldg(twy + j1 * k));
+#pragma unroll
+        for (int k = 0; k < R1Y; ++k) buf[Lay::at(j1 + R2Y * k, z)] = x[k];
+    }
+    __syncthreads();
+    // y stage 2 (radix R2Y on contiguous blocks)
+    for (int b = tid; b < NZ * R1Y; b += NT) {
+        const int blk = b % R1Y, z = b / R1Y;
+        float2 x[R2Y];
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) x[e] = buf[Lay::at(blk * R2Y + e, z)];
+        rdft<false, R2Y>(x);
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) buf[Lay::at(blk * R2Y + e, z)] = x[e];
+    }
+    __syncthreads();
+    // z stage 1 (DIF radix R1Z, n1 = R2Z)
+    for (int b = tid; b < NY * R2Z; b += NT) {
+        const int y = b % NY, j1 = b / NY;
+        float2 x[R1Z];
+#pragma unroll
+        for (int t = 0; t < R1Z; ++t) x[t] = buf[Lay::at(y, j1 + R2Z * t)];
+        rdft<false, R1Z>(x);
+#pragma unroll
+        for (int k = 1; k < R1Z; ++k) x[k] = cmul(x[k], __ldg(twz + j1 * k));
+#pragma unroll
+        for (int k = 0; k < R1Z; ++k) buf[Lay::at(y, j1 + R2Z * k)] = x[k];
+    }
+    __syncthreads();
+    // z stage 2 + multiplier + adjoint z stage 2 (or the energy sum)
+    const float sxp = __ldg(a.sx + p);
+    double acc = 0.0;
+    for (int b = tid; b < NY * R1Z; b += NT) {
+        const int y = b % NY, blk = b / NY;
+        float2 x[R2Z];
+#pragma unroll
+        for (int e = 0; e < R2Z; ++e) x[e] = buf[Lay::at(y, blk * R2Z + e)];
+        rdft<false, R2Z>(x);
+        const float sy = __ldg(a.sy_fast + y);
+        if (MODE == 0) {
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) {
+                const float base = 2.0f * (sxp + sy + __ldg(a.sz_fast + blk * R2Z + e));
+                float K = base;
+                for (int q = 1; q < a.order; ++q) K *= base;
+                const float m = a.scale / (a.lambda * K + a.theta);
+                x[e] = make_float2(x[e].x * m, x[e].y * m);
+            }
+            rdft<true, R2Z>(x);
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) buf[Lay::at(y, blk * R2Z + e)] = x[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) {
+                const double base = 2.0 * ((double)sxp + (double)sy + (double)__ldg(a.sz_fast + blk * R2Z + e));
+                double K = base;
+                for (int q = 1; q < a.order; ++q) K *= base;
+                acc += K * ((double)x[e].x * x[e].x + (double)x[e].y * x[e].y);
+            }
+        }
+    }
+    if (MODE == 1) {
+        const bool self_conj = (p == 0) || (2 * p == a.F.M);
+        const double tot = block_sum<NT>(acc, red) * (self_conj ? 1.0 : 2.0);
+        if (tid == 0) {
+            double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
+            part[blockIdx.x] = tot;
+            if (last_block_ticket(&st->counter, gridDim.x)) {
+                double s = 0.0;
+                for (unsigned bb = 0; bb < gridDim.x; ++bb) s += part[bb];
+                a.energy_out[pair] = 0.5 * s / (double)a.F.N;
+            }
+        }
+        return;
+    }
+    __syncthreads();
+    // adjoint z stage 1
+    for (int b = tid; b < NY * R2Z; b += NT) {
+        const int y = b % NY, j1 = b / NY;
+        float2 x[R1Z];
+#pragma unroll
+        for (int k = 0; k < R1Z; ++k) x[k] = buf[Lay::at(y, j1 + R2Z * k)];
+#pragma unroll
+        for (int k = 1; k < R1Z; ++k) x[k] = cmulc(x[k], __ldg(twz + j1 * k));
+        rdft<true, R1Z>(x);
+#pragma unroll
+        for (int t = 0; t < R1Z; ++t) buf[Lay::at(y, j1 + R2Z * t)] = x[t];
+    }
+    __syncthreads();
+    // adjoint y stage 2
+    for (int b = tid; b < NZ * R1Y; b += NT) {
+        const int blk = b % R1Y, z = b / R1Y;
+        float2 x[R2Y];
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) x[e] = buf[Lay::at(blk * R2Y + e, z)];
+        rdft<true, R2Y>(x);
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) buf[Lay::at(blk * R2Y + e, z)] = x[e];
+    }
+    __syncthreads();
+    // adjoint y stage 1, straight to global
+#pragma unroll 2
+    for (int b = tid; b < NZ * R2Y; b += NT) {
+        const int j1 = b % R2Y, z = b / R2Y;
+        float2 x[R1Y];
+#pragma unroll
+        for (int k = 0; k < R1Y; ++k) x[k] = buf[Lay::at(j1 + R2Y * k, z)];
+#pragma unroll
+        for (int k = 1; k < R1Y; ++k) x[k] = cmulc(x[k], __ldg(twy + j1 * k));
+        rdft<true, R1Y>(x);
+#pragma unroll
+        for (int t = 0; t < R1Y; ++t) Sp[z * NY + j1 + R2Y * t] = x[t];
+    }
+}
+
+}  // namespace dregb

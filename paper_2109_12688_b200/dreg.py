@@ -81,6 +81,7 @@ def load_library() -> C.CDLL:
         P, C.c_int, V, V, Dims3, Spacing3, C.POINTER(RegCfg), V, V, C.POINTER(PairResult),
     ]
     L.dreg_cuda_solve_velocity.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F, C.POINTER(abi.SolverDiag)]
+    L.dreg_cuda_time_kernels.argtypes = [P, C.c_int, _D]
     L.dreg_cuda_v_update.argtypes = [P, _F, _F, _F, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
     L.dreg_cuda_w_update.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
     L.dreg_cuda_regulariser_energy.argtypes = [P, _F, Dims3, C.c_int, _D]
@@ -88,6 +89,7 @@ def load_library() -> C.CDLL:
     L.dreg_cuda_image_gradient.argtypes = [P, _F, Dims3, _F]
     L.dreg_cuda_compose_deformation.argtypes = [P, _F, _F, Dims3, _F]
     L.dreg_cuda_jacobian.argtypes = [P, _F, Dims3, _F, C.POINTER(JacobianStats)]
+    L.dreg_cuda_jacobian_device.argtypes = [P, V, Dims3, V, C.POINTER(JacobianStats)]
     L.dreg_cuda_normalize_intensity_pair.argtypes = [P, _F, _F, Dims3, _F, _F]
     L.dreg_cuda_binomial_smooth.argtypes = [P, _F, Dims3, _F]
     L.dreg_cuda_mean_sad.argtypes = [P, _F, _F, Dims3, _D]
@@ -224,7 +226,7 @@ class Context:
         res = (PairResult * n)()
         self._check(
             self.lib.dreg_cuda_register_batch(
-                self.h, n, T, S, abi.dims3(shape), Spacing3(*spacing), C.byref(cfg), PO, WO, res
+                self.h, n, T, S, abi.dims3(targets[0]), Spacing3(*spacing), C.byref(cfg), PO, WO, res
             )
         )
         return phis, warps, list(res)
@@ -264,6 +266,12 @@ class Context:
             "objective": obj[:it].copy() if cfg.log_objective else np.zeros(0),
             "constraint_residual": res[:it].copy(),
         }
+
+    def time_kernels(self, reps: int = 20) -> dict:
+        """CUDA-event timing of the per-iteration kernels on the current workspace."""
+        out = np.zeros(5, np.float64)
+        self._check(self.lib.dreg_cuda_time_kernels(self.h, reps, out.ctypes.data_as(_D)))
+        return {"xpass_ms": out[0], "plane_ms": out[1], "xpass_bytes": out[2], "plane_bytes": out[3], "pairs": int(out[4])}
 
     # ---- building blocks ---------------------------------------------------------
     def v_update(self, target, warped, grad, w_hat, b_hat, cfg: SolverCfg) -> np.ndarray:
@@ -331,6 +339,12 @@ class Context:
         disp = _f32(disp)
         st = JacobianStats()
         self._check(self.lib.dreg_cuda_jacobian(self.h, _fp(disp), abi.dims3(disp), None, C.byref(st)))
+        return st
+
+    def jacobian_stats_device(self, disp_soa_ptr: int, dims) -> JacobianStats:
+        """Folding statistics of a device-resident SoA displacement [3][voxels]."""
+        st = JacobianStats()
+        self._check(self.lib.dreg_cuda_jacobian_device(self.h, C.c_void_p(disp_soa_ptr), abi.dims3(dims), None, C.byref(st)))
         return st
 
     def normalize_intensity_pair(self, a, b):
