@@ -73,8 +73,8 @@ __device__ __forceinline__ void stv(float* p, const float* in) {
     }
 }
 
-template <int MODE, int DT, int VEC>
-__global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArgs a) {
+template <int MODE, int DT, int VEC, bool F64 = false>
+__global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_kernel(XArgs a) {
     const int pair = blockIdx.y;
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
             const float2* Sc = S + (size_t)c * hx * lines;
             for (int idx = tid; idx < hx * TL; idx += nthr) {
                 const int p = idx / TL, l = idx - p * TL;
-                sm.Xs[idx] = l < nl ? Sc[(size_t)p * lines + L0 + l] : make_float2(0.f, 0.f);
+                sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? Sc[(size_t)p * lines + L0 + l] : make_float2(0.f, 0.f);
             }
             __syncthreads();
             float2* bc = sm.buf + (size_t)c * TL * PM;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
             }
             __syncthreads();
         }
-        fft_lines<true>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
+        if (!(a.dbg_skip & 1)) fft_lines<true>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
     }
 
     if constexpr (UTIL) {
@@ -191,7 +191,106 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
     double s_change = 0.0, s_res = 0.0, s_obj = 0.0;
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
-    for (int i0 = tid * VEC; i0 < (UTIL ? 0 : nvox); i0 += nthr * VEC) {
+    if constexpr (!F64) {
+        // fp32 arithmetic, fp32 per-thread partial sums (a thread covers <= ~64 voxels)
+        const float thf = (float)theta, ithf = (float)inv_theta, epsf = (float)eps, cf = (float)coef;
+        float fc = 0.f, fr = 0.f, fo = 0.f;
+#pragma unroll 2
+        for (int i0 = tid * VEC; i0 < (UTIL || (a.dbg_skip & 2) ? 0 : nvox); i0 += nthr * VEC) {
+            const int l = i0 / M, x0 = i0 - l * M;
+            const size_t gi = base + i0;
+            float w[3][VEC], vp[3][VEC], bo[3][VEC], wp[3][VEC], bp[3][VEC], g[3][VEC], dv[VEC];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (MODE != X_FIRST) ldv<VEC>(V + (size_t)c * N + gi, vp[c]);
+                if (MODE == X_GENERAL) ldv<VEC>(BH + (size_t)c * N + gi, bo[c]);
+                if (MODE == X_GENERAL && accel) {
+                    ldv<VEC>(WP + (size_t)c * N + gi, wp[c]);
+                    ldv<VEC>(BP + (size_t)c * N + gi, bp[c]);
+                }
+                if (MODE != X_TAIL) ldv<VEC>(G + (size_t)c * N + gi, g[c]);
+            }
+            if (MODE != X_TAIL) ldv<VEC>(Dd + gi, dv);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    w[c][j] = MODE == X_FIRST ? 0.f : (!a.odd ? reinterpret_cast<const float*>(bl)[x0 + j] : bl[x0 + j].x);
+                    if (MODE == X_FIRST) vp[c][j] = 0.f;
+                    if (MODE != X_GENERAL) bo[c][j] = 0.f;
+                }
+            }
+            if (MODE == X_TAIL) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int j = 0; j < VEC; ++j) {
+                        const float dd = vp[c][j] - w[c][j];
+                        fr = fmaf(dd, dd, fr);
+                    }
+                continue;
+            }
+            float wh[3][VEC], bh[3][VEC], vn[3][VEC];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    if (MODE == X_FIRST) {
+                        wh[c][j] = 0.f;
+                        bh[c][j] = 0.f;
+                        continue;
+                    }
+                    const float dd = vp[c][j] - w[c][j];
+                    fr = fmaf(dd, dd, fr);
+                    const float b = bo[c][j] + dd;  // dual update (admm.cpp:142-153)
+                    if (MODE == X_GENERAL && accel) {
+                        wh[c][j] = fmaf(cf, w[c][j] - wp[c][j], w[c][j]);  // extrapolate (admm.cpp:130-139)
+                        bh[c][j] = fmaf(cf, b - bp[c][j], b);
+                    } else {
+                        wh[c][j] = w[c][j];
+                        bh[c][j] = b;
+                    }
+                    bo[c][j] = b;
+                }
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) {
+                const float whj[3] = {wh[0][j], wh[1][j], wh[2][j]};
+                const float bhj[3] = {bh[0][j], bh[1][j], bh[2][j]};
+                const float gj[3] = {g[0][j], g[1][j], g[2][j]};
+                float vj[3];
+                v_update_voxel_f32<DT>(whj, bhj, gj, dv[j], thf, ithf, epsf, vj);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    vn[c][j] = vj[c];
+                    fc += fabsf(vj[c] - vp[c][j]);
+                }
+                if (a.sp.log_objective) {
+                    const float rho = fmaf(gj[0], vj[0], fmaf(gj[1], vj[1], gj[2] * vj[2])) + dv[j];
+                    fo += DT == 1 ? fabsf(rho) : 0.5f * rho * rho;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                if (MODE != X_FIRST && accel) {
+                    stv<VEC>(WP + (size_t)c * N + gi, w[c]);
+                    stv<VEC>(BP + (size_t)c * N + gi, bo[c]);
+                }
+                stv<VEC>(V + (size_t)c * N + gi, vn[c]);
+                if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bh[c]);
+                float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+#pragma unroll
+                for (int j = 0; j < VEC; ++j) {
+                    if (!a.odd) reinterpret_cast<float*>(bl)[x0 + j] = vn[c][j] + bh[c][j];
+                    else bl[x0 + j] = make_float2(vn[c][j] + bh[c][j], 0.f);
+                }
+            }
+        }
+        s_change = fc;
+        s_res = fr;
+        s_obj = fo;
+    } else {
+    for (int i0 = tid * VEC; i0 < (UTIL || (a.dbg_skip & 2) ? 0 : nvox); i0 += nthr * VEC) {
         const int l = i0 / M, x0 = i0 - l * M;
         const size_t gi = base + i0;
         float w[3][VEC], vp[3][VEC];
@@ -308,6 +407,8 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
         }
     }
 
+    }
+
     // ---- phase 3: r2c along x of u_k, scatter to the plane-major spectrum ----
     if (MODE != X_TAIL) {
         if (nl < TL) {  // zero the unused lines so the batched FFT stays finite
@@ -317,7 +418,7 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
             }
         }
         __syncthreads();
-        fft_lines<false>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
+        if (!(a.dbg_skip & 1)) fft_lines<false>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
         for (int idx = tid; idx < 3 * hx * TL; idx += nthr) {
             const int c = idx / (hx * TL);
             const int rem = idx - c * hx * TL;
@@ -334,7 +435,7 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
             } else {
                 X = bl[sm.xpos[k]];
             }
-            S[((size_t)c * hx + k) * lines + L0 + l] = X;
+            if (!(a.dbg_skip & 4)) S[((size_t)c * hx + k) * lines + L0 + l] = X;
         }
     }
 
@@ -344,35 +445,28 @@ __global__ void __launch_bounds__(kXThreads, VEC == 4 ? 2 : 3) xpass_kernel(XArg
     const double tc = block_sum<kXThreads>(s_change, sm.red);
     const double tr = block_sum<kXThreads>(s_res, sm.red);
     const double to = block_sum<kXThreads>(s_obj, sm.red);
-    if (tid == 0) {
-        double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
-        part[blockIdx.x] = tc;
-        part[kMaxPartials + blockIdx.x] = tr;
-        part[2 * kMaxPartials + blockIdx.x] = to;
-        if (last_block_ticket(&st->counter, gridDim.x)) {
-            double sc = 0.0, sr = 0.0, so = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                sc += part[b];
-                sr += part[kMaxPartials + b];
-                so += part[2 * kMaxPartials + b];
+    const double vals[3] = {tc, tr, to};
+    double tot[3];
+    if (reduce_partials<kXThreads, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot,
+                                  sm.red) &&
+        tid == 0) {
+        const double sc = tot[0], sr = tot[1], so = tot[2];
+        double* dg = a.F.diag ? a.F.diag + (size_t)pair * a.F.diag_stride * 3 : nullptr;
+        if (MODE == X_TAIL) {
+            const int it = st->iterations;
+            if (dg && it >= 1) dg[(it - 1) * 3 + 1] = sqrt(sr);
+        } else {
+            const double change = sc / (3.0 * (double)N);
+            if (dg) {
+                dg[a.k * 3 + 0] = change;
+                if (a.k >= 1) dg[(a.k - 1) * 3 + 1] = sqrt(sr);
+                dg[a.k * 3 + 2] = so;
             }
-            double* dg = a.F.diag ? a.F.diag + (size_t)pair * a.F.diag_stride * 3 : nullptr;
-            if (MODE == X_TAIL) {
-                const int it = st->iterations;
-                if (dg && it >= 1) dg[(it - 1) * 3 + 1] = sqrt(sr);
-            } else {
-                const double change = sc / (3.0 * (double)N);
-                if (dg) {
-                    dg[a.k * 3 + 0] = change;
-                    if (a.k >= 1) dg[(a.k - 1) * 3 + 1] = sqrt(sr);
-                    dg[a.k * 3 + 2] = so;
-                }
-                st->iterations = a.k + 1;
-                st->final_change = change;
-                if (change <= a.sp.tol) {
-                    st->solve_done = 1;
-                    st->done_iter = a.k;
-                }
+            st->iterations = a.k + 1;
+            st->final_change = change;
+            if (change <= a.sp.tol) {
+                st->solve_done = 1;
+                st->done_iter = a.k;
             }
         }
     }
@@ -466,16 +560,12 @@ __global__ void __launch_bounds__(kPThreads) plane_kernel(PArgs a) {
             acc += K * ((double)v.x * v.x + (double)v.y * v.y);
         }
         const bool self_conj = (p == 0) || (2 * p == a.F.M);
-        const double tot = block_sum<kPThreads>(acc, red) * (self_conj ? 1.0 : 2.0);
-        if (tid == 0) {
-            double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
-            part[blockIdx.x] = tot;
-            if (last_block_ticket(&st->counter, gridDim.x)) {
-                double s = 0.0;
-                for (unsigned b = 0; b < gridDim.x; ++b) s += part[b];
-                a.energy_out[pair] = 0.5 * s / (double)a.F.N;
-            }
-        }
+        const double vals[1] = {block_sum<kPThreads>(acc, red) * (self_conj ? 1.0 : 2.0)};
+        double tot[1];
+        if (reduce_partials<kPThreads, 1>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot,
+                                      red) &&
+            tid == 0)
+            a.energy_out[pair] = 0.5 * tot[0] / (double)a.F.N;
     }
 }
 
@@ -487,7 +577,9 @@ static cudaError_t launch_x_mode(const XArgs& a, int npairs, cudaStream_t s) {
     int vec = a.vec;
     if (vec == 4 && a.F.M % 4) vec = 2;
     if (vec == 2 && a.F.M % 2) vec = 1;
-    void (*k)(XArgs) = vec == 4 ? xpass_kernel<MODE, DT, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2> : xpass_kernel<MODE, DT, 1>);
+    void (*k)(XArgs);
+    if (a.f64) k = vec == 4 ? xpass_kernel<MODE, DT, 4, true> : (vec == 2 ? xpass_kernel<MODE, DT, 2, true> : xpass_kernel<MODE, DT, 1, true>);
+    else k = vec == 4 ? xpass_kernel<MODE, DT, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2> : xpass_kernel<MODE, DT, 1>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -502,6 +594,7 @@ static cudaError_t launch_x_dt(const XArgs& a, int npairs, cudaStream_t s) {
 }
 
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s) {
+    if (mode <= X_TAIL && xpass_tma_eligible(a)) return launch_xpass_tma(a, mode, npairs, s);
     switch (mode) {
         case X_FIRST: return launch_x_dt<X_FIRST>(a, npairs, s);
         case X_SECOND: return launch_x_dt<X_SECOND>(a, npairs, s);

@@ -104,6 +104,41 @@ __device__ __forceinline__ double block_min(double v, double* red) {
     return s;
 }
 
+// Deterministic cross-block reduction, K sums per block (fixed per-thread strides +
+// fixed tree => run-to-run bit-identical).  Every thread of the block must call it.
+// Thread 0 writes vals[] as this block's partials into part[k * kMaxPartials + block];
+// the block that arrives last reduces all partials with every thread and returns
+// true (totals valid in thread 0 only).
+template <int NT, int K>
+__device__ __forceinline__ bool reduce_partials(const double (&vals)[K], double* part, unsigned int* counter,
+                                                unsigned int nblocks, double (&tot)[K], double* red,
+                                                unsigned min_mask = 0u, int slot = -1) {
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        const unsigned sl = slot < 0 ? blockIdx.x : (unsigned)slot;
+#pragma unroll
+        for (int k = 0; k < K; ++k) part[(size_t)k * kMaxPartials + sl] = vals[k];
+        __threadfence();
+        const unsigned int t = atomicAdd(counter, 1u);
+        s_last = (t == nblocks - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const bool is_min = (min_mask >> k) & 1u;
+        double acc = is_min ? 1e300 : 0.0;
+        for (unsigned b = threadIdx.x; b < nblocks; b += NT) {
+            const double v = __ldcg(part + (size_t)k * kMaxPartials + b);
+            acc = is_min ? fmin(acc, v) : acc + v;
+        }
+        tot[k] = is_min ? block_min<NT>(acc, red) : block_sum<NT>(acc, red);
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+}
+
 // Last-block ticket: returns true in thread 0 of the block that finishes last
 // among `nblocks` (per pair).  Callers then reduce the partials in fixed order,
 // which keeps every reduction run-to-run bit-deterministic.

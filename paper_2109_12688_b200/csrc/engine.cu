@@ -137,7 +137,7 @@ float one_minus_cos(int k, int n) {  // 1 - cos(2 pi k / n) = 2 sin^2(pi k / n);
 struct Geometry {
     int M = 0, Ny = 0, Nz = 0, hx = 0;
     long long N = 0, lines = 0;
-    int L = 0, odd = 0, TL = 0, PM = 0, PY = 0, xvec = 1;
+    int L = 0, odd = 0, TL = 0, PM = 0, PY = 0, xvec = 1, tma = 0;
     AxisPlan px{}, py{}, pz{};
     DevArray<float2> twx, xtw, twy, twz;
     DevArray<int> xpos;
@@ -159,7 +159,8 @@ struct Geometry {
         pz = make_plan(Nz);
         PM = (L % 2 == 0) ? L + 1 : L;
         PY = (Ny % 2 == 0) ? Ny + 1 : Ny;
-        TL = env_int("DREG_TL", 32);
+        tma = env_int("DREG_TMA", 0) && (M % 4 == 0) && (lines % 2 == 0);
+        TL = tma ? env_int("DREG_TMA_TL", 8) : env_int("DREG_TL", 32);
         xvec = env_int("DREG_XVEC", 2);
         while (TL > 4 && xpass_smem_bytes(L, hx, TL, PM) > 110 * 1024) TL /= 2;
         xsmem = xpass_smem_bytes(L, hx, TL, PM);
@@ -195,7 +196,7 @@ struct Geometry {
         for (int pos = 0; pos < Nz; ++pos) s[pos] = one_minus_cos(freq_of_pos(pz, pos), Nz);
         up(sz, s);
         fast = plane_fast_supported(Ny, Nz) && env_int("DREG_FAST_PLANE", 1);
-        prefetch = env_int("DREG_PREFETCH", 1);
+        prefetch = env_int("DREG_PREFETCH", 0);
         if (fast) {
             // tables for the two-stage split R1 x R2 of the specialised kernel
             auto split = [](int n) {
@@ -489,6 +490,10 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag) {
     a.odd = w.geo.odd;
     a.vec = w.geo.xvec;
     a.prefetch = w.geo.prefetch && (w.geo.M % 4 == 0);
+    a.tma = w.geo.tma;
+    a.tma_ctas_per_sm = env_int("DREG_TMA_CTAS", 1);
+    a.dbg_skip = env_int("DREG_DBG_SKIP", 0);
+    a.f64 = env_int("DREG_F64", 0);
     a.fd_lines.init((unsigned)(3 * w.geo.TL));
     return a;
 }

@@ -95,18 +95,12 @@ __global__ void __launch_bounds__(kVT) compose_decide_kernel(VolGeom g, RegBuffe
         wn[i] = w;
         sad += fabs((double)w - (double)I0[i]);  // mean_sad (registration.cpp:145-152)
     }
-    const double ts = block_sum<kVT>(sad, red);
-    const double tb = block_sum<kVT>(bad, red);
-    if (threadIdx.x == 0) {
-        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
-        part[blockIdx.x] = ts;
-        part[kMaxPartials + blockIdx.x] = tb;
-        if (last_block_ticket(&st->counter, gridDim.x)) {
-            double sum = 0.0, nbad = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                sum += part[b];
-                nbad += part[kMaxPartials + b];
-            }
+    const double vals[2] = {block_sum<kVT>(sad, red), block_sum<kVT>(bad, red)};
+    double tot[2];
+    if (reduce_partials<kVT, 2>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
+        threadIdx.x == 0) {
+        {
+            const double sum = tot[0], nbad = tot[1];
             if (nbad > 0.0) {
                 // solve_velocity's all_finite(v) -> numeric_error (admm.cpp:310-312)
                 st->status = DREG_NUMERIC;
@@ -162,27 +156,17 @@ __global__ void __launch_bounds__(kVT) minmax_kernel(VolGeom g, RegBuffers R, Fi
         lo = fminf(lo, fminf(a, b));
         hi = fmaxf(hi, fmaxf(a, b));
     }
-    const double tlo = block_min<kVT>((double)lo, red);
-    const double thi = -block_min<kVT>(-(double)hi, red);
-    const double tb = block_sum<kVT>(bad, red);
-    if (threadIdx.x == 0) {
-        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
-        part[blockIdx.x] = tlo;
-        part[kMaxPartials + blockIdx.x] = thi;
-        part[2 * kMaxPartials + blockIdx.x] = tb;
-        if (last_block_ticket(&st->counter, gridDim.x)) {
-            double l = 1e300, h = -1e300, nb = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                l = fmin(l, part[b]);
-                h = fmax(h, part[kMaxPartials + b]);
-                nb += part[2 * kMaxPartials + b];
-            }
-            st->lo = (float)l;
-            st->hi = (float)h;
-            if (nb > 0.0) {
-                st->status = DREG_NUMERIC;
-                st->active = 0;
-            }
+    const double vals[3] = {block_min<kVT>((double)lo, red), block_min<kVT>(-(double)hi, red),
+                            block_min<kVT>(-bad, red)};
+    double tot[3];
+    if (reduce_partials<kVT, 3>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red,
+                                0x7u) &&
+        threadIdx.x == 0) {
+        st->lo = (float)tot[0];
+        st->hi = (float)(-tot[1]);
+        if (tot[2] < 0.0) {
+            st->status = DREG_NUMERIC;
+            st->active = 0;
         }
     }
 }
@@ -298,20 +282,16 @@ __global__ void __launch_bounds__(kVT) level_init_kernel(VolGeom g, RegBuffers R
         W[i] = w;
         sad += fabs((double)w - (double)I0[i]);
     }
-    const double ts = block_sum<kVT>(sad, red);
-    if (threadIdx.x == 0) {
-        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
-        part[blockIdx.x] = ts;
-        if (last_block_ticket(&st->counter, gridDim.x)) {
-            double sum = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) sum += part[b];
-            st->sad_prev = sum / (double)N;
-            st->mean_sad[level][0] = st->sad_prev;
-            st->cur = 0;
-            st->warps = 0;
-            st->level = level;
-            st->active = 1;
-        }
+    const double vals[1] = {block_sum<kVT>(sad, red)};
+    double tot[1];
+    if (reduce_partials<kVT, 1>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
+        threadIdx.x == 0) {
+        st->sad_prev = tot[0] / (double)N;
+        st->mean_sad[level][0] = st->sad_prev;
+        st->cur = 0;
+        st->warps = 0;
+        st->level = level;
+        st->active = 1;
     }
 }
 
@@ -345,16 +325,11 @@ __global__ void __launch_bounds__(kVT) finalize_kernel(VolGeom g, RegBuffers R, 
         }
         if (wo) wo[i] = (float)trilinear(src, g.M, g.Ny, g.Nz, x + (double)u0, y + (double)u1, z + (double)u2);
     }
-    const double tb = block_sum<kVT>(bad, red);
-    if (threadIdx.x == 0) {
-        double* part = F.part + (size_t)pair * 3 * kMaxPartials;
-        part[blockIdx.x] = tb;
-        if (last_block_ticket(&st->counter, gridDim.x)) {
-            double nb = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) nb += part[b];
-            if (nb > 0.0) st->status = DREG_NUMERIC;  // registration.cpp:275-277
-        }
-    }
+    const double vals[1] = {block_sum<kVT>(bad, red)};
+    double tot[1];
+    if (reduce_partials<kVT, 1>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
+        threadIdx.x == 0 && tot[0] > 0.0)
+        st->status = DREG_NUMERIC;  // registration.cpp:275-277
 }
 
 cudaError_t launch_finalize(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s) {
@@ -393,21 +368,12 @@ __global__ void __launch_bounds__(kVT) jacobian_kernel(VolGeom g, const float* _
             nonpos += d <= 0.0 ? 1.0 : 0.0;
         }
     }
-    const double tn = block_sum<kVT>(nonpos, red);
-    const double tm = block_min<kVT>(mind, red);
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = tn;
-        part[kMaxPartials + blockIdx.x] = tm;
-        if (last_block_ticket(counter, gridDim.x)) {
-            double n = 0.0, m = 1e300;
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                n += part[b];
-                m = fmin(m, part[kMaxPartials + b]);
-            }
-            out3[0] = n;
-            out3[1] = (double)(g.M - 2) * (double)(g.Ny - 2) * (double)(g.Nz - 2);
-            out3[2] = m;
-        }
+    const double vals[2] = {block_sum<kVT>(nonpos, red), block_min<kVT>(mind, red)};
+    double tot[2];
+    if (reduce_partials<kVT, 2>(vals, part, counter, gridDim.x, tot, red, 0x2u) && threadIdx.x == 0) {
+        out3[0] = tot[0];
+        out3[1] = (double)(g.M - 2) * (double)(g.Ny - 2) * (double)(g.Nz - 2);
+        out3[2] = tot[1];
     }
 }
 
@@ -507,15 +473,10 @@ __global__ void sad_kernel(VolGeom g, const float* a, const float* b, double* pa
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.N;
          i += (long long)gridDim.x * blockDim.x)
         s += fabs((double)a[i] - (double)b[i]);
-    const double t = block_sum<kVT>(s, red);
-    if (threadIdx.x == 0) {
-        part[blockIdx.x] = t;
-        if (last_block_ticket(counter, gridDim.x)) {
-            double sum = 0.0;
-            for (unsigned k = 0; k < gridDim.x; ++k) sum += part[k];
-            *out = sum / (double)g.N;
-        }
-    }
+    const double vals[1] = {block_sum<kVT>(s, red)};
+    double tot[1];
+    if (reduce_partials<kVT, 1>(vals, part, counter, gridDim.x, tot, red) && threadIdx.x == 0)
+        *out = tot[0] / (double)g.N;
 }
 
 cudaError_t launch_sad(VolGeom g, const float* a, const float* b, double* part, double* out,

@@ -27,6 +27,10 @@ struct XArgs {
     int add_bh;         // X_FWD: transform V + BH instead of V
     int vec;            // point-wise vector width (1, 2 or 4; 4/2 need M % 4 / M % 2 == 0)
     int prefetch;       // L2 bulk prefetch of the tile's field rows at kernel start
+    int tma;            // use the TMA-staged x-pass (xpass_tma.cu) when eligible
+    int tma_ctas_per_sm;  // persistent CTAs per SM for the TMA x-pass
+    int f64;            // fp64 point-wise arithmetic in the generic x-pass (DREG_F64)
+    int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
     FastDiv fd_lines;   // divide by 3 * TL
 };
 
@@ -56,6 +60,9 @@ size_t plane_smem_bytes(int Ny, int Nz, int PY);
 int plane_fast_r1(int n);
 bool plane_fast_supported(int Ny, int Nz);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
+bool xpass_tma_eligible(const XArgs& a);
+size_t xpass_tma_smem_bytes(int L, int hx, int TL, int PM, int M);
+cudaError_t launch_xpass_tma(const XArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s);
 
 // ---- field kernels (field_kernels.cu) ----

@@ -158,16 +158,12 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
     }
     if (MODE == 1) {
         const bool self_conj = (p == 0) || (2 * p == a.F.M);
-        const double tot = block_sum<NT>(acc, red) * (self_conj ? 1.0 : 2.0);
-        if (tid == 0) {
-            double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
-            part[blockIdx.x] = tot;
-            if (last_block_ticket(&st->counter, gridDim.x)) {
-                double s = 0.0;
-                for (unsigned bb = 0; bb < gridDim.x; ++bb) s += part[bb];
-                a.energy_out[pair] = 0.5 * s / (double)a.F.N;
-            }
-        }
+        const double vals[1] = {block_sum<NT>(acc, red) * (self_conj ? 1.0 : 2.0)};
+        double tot[1];
+        if (reduce_partials<NT, 1>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot,
+                                      red) &&
+            tid == 0)
+            a.energy_out[pair] = 0.5 * tot[0] / (double)a.F.N;
         return;
     }
     __syncthreads();

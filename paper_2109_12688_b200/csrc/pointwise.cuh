@@ -36,6 +36,29 @@ __device__ __forceinline__ void v_update_voxel(const float wh[3], const float bh
 }
 
 
+// fp32 form of the same update (the point-wise path of the fused x-pass).
+// l2: v = u - g (g.u + d) / (theta + |g|^2), algebraically equal to the reference's
+//     rhs/theta - g (g.rhs) / (theta (theta + |g|^2)), rhs = theta u - d g;
+// l1: identical expression order to admm.cpp:33-39.
+template <int DT>
+__device__ __forceinline__ void v_update_voxel_f32(const float wh[3], const float bh[3], const float g[3], float d,
+                                                   float theta, float inv_theta, float eps, float v[3]) {
+    const float ux = wh[0] - bh[0], uy = wh[1] - bh[1], uz = wh[2] - bh[2];
+    const float gg = fmaf(g[0], g[0], fmaf(g[1], g[1], g[2] * g[2]));
+    const float gu = fmaf(g[0], ux, fmaf(g[1], uy, g[2] * uz));
+    float s;
+    if (DT == 1) {
+        const float zhat = theta * (gu + d) / (gg + eps);
+        const float clip = zhat / fmaxf(fabsf(zhat), 1.0f);
+        s = clip * inv_theta;
+    } else {
+        s = (gu + d) / (theta + gg);
+    }
+    v[0] = fmaf(-g[0], s, ux);
+    v[1] = fmaf(-g[1], s, uy);
+    v[2] = fmaf(-g[2], s, uz);
+}
+
 // volume.cpp:36-41 (axis_sample): clamp to [0, dim-1] BEFORE floor; hi = min(lo+1, dim-1).
 __device__ __forceinline__ void axis_sample(double coord, int dim, int& lo, int& hi, double& frac) {
     const double top = (double)(dim - 1);
