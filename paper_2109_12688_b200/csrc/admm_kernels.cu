@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_ke
     const long long L0 = (long long)blockIdx.x * TL;
     const int nl = (int)min((long long)TL, lines - L0);
     const long long N = a.F.N;
+    const int lt = 31 - __clz(TL);  // TL is a power of two
+    const int tm = TL - 1;
 
     for (int i = tid; i < L; i += nthr) {
         sm.twx[i] = a.twx[i];
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_ke
         for (int c = 0; c < 3; ++c) {
             const float2* Sc = S + (size_t)c * hx * lines;
             for (int idx = tid; idx < hx * TL; idx += nthr) {
-                const int p = idx / TL, l = idx - p * TL;
+                const int p = idx >> lt, l = idx & tm;
                 sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? Sc[(size_t)p * lines + L0 + l] : make_float2(0.f, 0.f);
             }
             __syncthreads();
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_ke
                 // Z'[k] = E + i O with E = X[k] + conj(X[L-k]), O = (X[k] - conj(X[L-k])) W_M^{-k};
                 // imaginary parts of the self-conjugate bins ignored (1-D c2r semantics).
                 for (int idx = tid; idx < L * TL; idx += nthr) {
-                    const int k = idx / TL, l = idx - k * TL;
+                    const int k = idx >> lt, l = idx & tm;
                     float2 A = sm.Xs[k * TL + l];
                     float2 B = sm.Xs[(L - k) * TL + l];
                     if (k == 0) { A.y = 0.f; B.y = 0.f; }
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_ke
                 }
             } else {
                 for (int idx = tid; idx < M * TL; idx += nthr) {
-                    const int k = idx / TL, l = idx - k * TL;
+                    const int k = idx >> lt, l = idx & tm;
                     float2 X;
                     if (k < hx) {
                         X = sm.Xs[k * TL + l];
@@ -419,16 +421,16 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_ke
         }
         __syncthreads();
         if (!(a.dbg_skip & 1)) fft_lines<false>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
-        for (int idx = tid; idx < 3 * hx * TL; idx += nthr) {
-            const int c = idx / (hx * TL);
-            const int rem = idx - c * hx * TL;
-            const int k = rem / TL, l = rem - k * TL;
+        for (int cidx = tid; cidx < 3 * hx * TL; cidx += nthr) {
+            const int c = cidx >= 2 * hx * TL ? 2 : (cidx >= hx * TL ? 1 : 0);
+            const int idx = cidx - c * hx * TL;
+            const int k = idx >> lt, l = idx & tm;
             if (l >= nl) continue;
             const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
             float2 X;
             if (!a.odd) {
-                const float2 zk = bl[sm.xpos[k % L]];
-                const float2 zc = cconj(bl[sm.xpos[(L - k) % L]]);
+                const float2 zk = bl[sm.xpos[k == L ? 0 : k]];
+                const float2 zc = cconj(bl[sm.xpos[k == 0 ? 0 : L - k]]);
                 const float2 e = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
                 const float2 o = make_float2(0.5f * (zk.y - zc.y), -0.5f * (zk.x - zc.x));
                 X = cadd(e, cmul(sm.xtw[k], o));

@@ -7,6 +7,7 @@
 // No compute happens on the host: every numerical step is an sm_100a kernel.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -162,6 +163,11 @@ struct Geometry {
         tma = env_int("DREG_TMA", 0) && (M % 4 == 0) && (lines % 2 == 0);
         TL = tma ? env_int("DREG_TMA_TL", 8) : env_int("DREG_TL", 32);
         xvec = env_int("DREG_XVEC", 2);
+        {
+            int t = 4;  // power of two (the x-pass index math uses shifts)
+            while (t * 2 <= std::max(TL, 4) && t < 64) t *= 2;
+            TL = t;
+        }
         while (TL > 4 && xpass_smem_bytes(L, hx, TL, PM) > 110 * 1024) TL /= 2;
         xsmem = xpass_smem_bytes(L, hx, TL, PM);
         psmem = plane_smem_bytes(Ny, Nz, PY);

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(kTThreads, 1) xpass_tma_kernel(XArgs a, int np
     const long long lines = a.F.lines;
     const long long N = a.F.N;
     const int tileN = TL * M;
+    const int lt = 31 - __clz(TL);
     const int tiles_per_pair = (int)((lines + TL - 1) / TL);
     const int total = tiles_per_pair * npairs;
     const bool accel = a.sp.accelerate != 0;
@@ -151,9 +152,9 @@ __global__ void __launch_bounds__(kTThreads, 1) xpass_tma_kernel(XArgs a, int np
             mbar_wait(&bars[2 * s], ph);
             const float2* X = Xs[s];
             for (int idx = tid; idx < 3 * L * TL; idx += nthr) {
-                const int c = idx / (L * TL);
+                const int c = idx >= 2 * L * TL ? 2 : (idx >= L * TL ? 1 : 0);
                 const int r = idx - c * L * TL;
-                const int k = r / TL, l = r - k * TL;
+                const int k = r >> lt, l = r & (TL - 1);
                 const float2* Xc = X + (size_t)c * hx * TL;
                 float2 A = l < nl ? Xc[k * TL + l] : make_float2(0.f, 0.f);
                 float2 B = l < nl ? Xc[(L - k) * TL + l] : make_float2(0.f, 0.f);
@@ -250,13 +251,13 @@ __global__ void __launch_bounds__(kTThreads, 1) xpass_tma_kernel(XArgs a, int np
             __syncthreads();
             fft_lines<false>(buf, 3 * TL, a.fd_lines, PM, 1, a.px, twx, tid, nthr);
             for (int idx = tid; idx < 3 * hx * TL; idx += nthr) {
-                const int c = idx / (hx * TL);
+                const int c = idx >= 2 * hx * TL ? 2 : (idx >= hx * TL ? 1 : 0);
                 const int rem = idx - c * hx * TL;
-                const int k = rem / TL, l = rem - k * TL;
+                const int k = rem >> lt, l = rem & (TL - 1);
                 if (l >= nl) continue;
                 const float2* bl = buf + (size_t)(c * TL + l) * PM;
-                const float2 zk = bl[xpos[k % L]];
-                const float2 zc = cconj(bl[xpos[(L - k) % L]]);
+                const float2 zk = bl[xpos[k == L ? 0 : k]];
+                const float2 zc = cconj(bl[xpos[k == 0 ? 0 : L - k]]);
                 const float2 e = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
                 const float2 o = make_float2(0.5f * (zk.y - zc.y), -0.5f * (zk.x - zc.x));
                 S[((size_t)c * hx + k) * lines + L0 + l] = cadd(e, cmul(xtw[k], o));
