@@ -208,7 +208,7 @@ def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
 
-    from paper_2109_12688_b200 import dreg, synth
+    from paper_2109_12688_b200 import dreg, shard, synth
 
     dist = world > 1
     if dist:
@@ -219,8 +219,16 @@ def run_ours(args, rank, world, local_rank):
     B = args.pairs_per_gpu
     N = SHAPE[0] * SHAPE[1] * SHAPE[2]
     cfg = reg_cfg(args.order)
-    seeds0 = 1000 + (rank * B) % 256
-    F, M = synth.make_batch(3, seeds0, B, SHAPE)
+    seeds = shard.pair_seeds(rank, world, B)
+    F = np.zeros((B,) + SHAPE, np.float32)
+    M = np.zeros((B,) + SHAPE, np.float32)
+    i = 0
+    while i < B:  # contiguous seed runs (wrap around the 256-pair pool)
+        j = i
+        while j + 1 < B and seeds[j + 1] == seeds[j] + 1:
+            j += 1
+        synth.make_batch(3, seeds[i], j - i + 1, SHAPE, out_fixed=F[i:j + 1], out_moving=M[i:j + 1])
+        i = j + 1
     tgt = torch.from_numpy(F.reshape(B, N)).to(dev)
     src = torch.from_numpy(M.reshape(B, N)).to(dev)
     phi = torch.empty((B, 3, N), dtype=torch.float32, device=dev)
@@ -263,11 +271,7 @@ def run_ours(args, rank, world, local_rank):
         tdist.barrier()
     launches = ctx.kernel_launches() - n0
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = shard.max_over_ranks(e0.elapsed_time(e1), dev)
     value = world * B * args.steps / (ms_max / 1000.0)
 
     # per-pair records (status, velocity_count, solves, folding count, final SAD) -> NCCL all-gather
@@ -277,12 +281,7 @@ def run_ours(args, rank, world, local_rank):
         r = res[p]
         lg = r.per_level[0]
         recs.append([r.status, r.velocity_count, r.solves, js.nonpositive, lg.mean_sad[lg.warps], js.min_det])
-    rec = torch.tensor(recs, dtype=torch.float64, device=dev)
-    if dist:
-        allrec = torch.empty((world * B, rec.shape[1]), dtype=torch.float64, device=dev)
-        tdist.all_gather_into_tensor(allrec, rec)
-        rec = allrec
-    rec = rec.cpu().numpy()
+    rec = shard.gather_records(torch.tensor(recs, dtype=torch.float64, device=dev)).cpu().numpy()
 
     # roofline of the dominant kernel (fused x-pass), CUDA events on the launching stream
     tk = ctx.time_kernels(20)
@@ -323,11 +322,9 @@ def run_ours(args, rank, world, local_rank):
             if i + 1 < args.steps:
                 flush.zero_()
                 torch.cuda.synchronize(dev)
-        et = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if dist:
-            tdist.all_reduce(et, op=tdist.ReduceOp.MAX)
+        et = shard.max_over_ranks(time.perf_counter() - t0, dev)
         e2e = {
-            "value": world * B * args.steps / float(et.item()),
+            "value": world * B * args.steps / et,
             "unit": UNIT,
             "h2d_bytes_per_step": B * 2 * N * 4,
             "d2h_bytes_per_step": B * (3 * N + N) * 4,
@@ -389,15 +386,7 @@ def run_ours(args, rank, world, local_rank):
         },
         "clocks": clk,
         "e2e": e2e,
-        "pairs": {
-            "count": int(rec.shape[0]),
-            "status_ok": int((rec[:, 0] == 0).sum()),
-            "mean_velocity_count": float(rec[:, 1].mean()),
-            "mean_solves": float(solves.mean()),
-            "folding_voxels_total": int(rec[:, 3].sum()),
-            "mean_final_sad": float(rec[:, 4].mean()),
-            "min_det": float(rec[:, 5].min()),
-        },
+        "pairs": shard.summarize(rec),
     }
     if world == 1 and not args.no_cpu:
         from oracle.oracle import available

@@ -1,0 +1,472 @@
+// dreg_b200/dreg.hpp -- header-only C++ drop-in for the reference `dreg` hot path.
+//
+// Same namespace, type names, fields, defaults and function signatures as the
+// reference headers (proj/core/include/dreg/{volume,admm,regularizer,registration,
+// metrics,errors}.hpp); every numerical call is forwarded to the sm_100a library
+// through the C ABI (include/dreg_cuda.h) and its status codes are rethrown as the
+// reference's exceptions (std::invalid_argument, dreg::numeric_error,
+// std::runtime_error).  Switching a reference user over is:
+//     #include "dreg/registration.hpp"   ->  #include "dreg_b200/dreg.hpp"
+//     -ldreg                             ->  -ldreg_cuda
+// Each host thread gets its own device context on dreg::cuda_device() (default 0).
+#pragma once
+
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "dreg_cuda.h"
+
+namespace dreg {
+
+// ---- errors.hpp ------------------------------------------------------------------
+struct io_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct numeric_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// ---- volume.hpp ------------------------------------------------------------------
+struct Dims3 {
+    int x = 0;
+    int y = 0;
+    int z = 0;
+    [[nodiscard]] std::size_t voxels() const {
+        return static_cast<std::size_t>(x) * static_cast<std::size_t>(y) * static_cast<std::size_t>(z);
+    }
+    friend bool operator==(const Dims3& a, const Dims3& b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
+};
+
+struct Spacing3 {
+    double x = 1.0;
+    double y = 1.0;
+    double z = 1.0;
+};
+
+struct Vec3 {
+    double x = 0.0, y = 0.0, z = 0.0;
+};
+
+struct ScalarVolume {
+    Dims3 dims;
+    Spacing3 spacing;
+    std::vector<float> data;
+    ScalarVolume() = default;
+    ScalarVolume(Dims3 d, Spacing3 s, float fill = 0.0f) : dims(d), spacing(s), data(d.voxels(), fill) {
+        if (d.x < 1 || d.y < 1 || d.z < 1) throw std::invalid_argument("volume dims must be positive");
+    }
+    [[nodiscard]] std::size_t index(int x, int y, int z) const {
+        return static_cast<std::size_t>(x) + static_cast<std::size_t>(dims.x) *
+                                                 (static_cast<std::size_t>(y) + static_cast<std::size_t>(dims.y) *
+                                                                                    static_cast<std::size_t>(z));
+    }
+    [[nodiscard]] float at(int x, int y, int z) const { return data[index(x, y, z)]; }
+    float& at(int x, int y, int z) { return data[index(x, y, z)]; }
+};
+
+struct VectorField {
+    Dims3 dims;
+    Spacing3 spacing;
+    std::vector<float> data;  // 3 * voxels, interleaved (vx, vy, vz)
+    VectorField() = default;
+    VectorField(Dims3 d, Spacing3 s) : dims(d), spacing(s), data(3 * d.voxels(), 0.0f) {
+        if (d.x < 1 || d.y < 1 || d.z < 1) throw std::invalid_argument("volume dims must be positive");
+    }
+    [[nodiscard]] Vec3 get(std::size_t v) const { return {data[3 * v], data[3 * v + 1], data[3 * v + 2]}; }
+};
+
+struct DeformationField {
+    VectorField disp;
+    static DeformationField identity(Dims3 d, Spacing3 s) { return {VectorField(d, s)}; }
+};
+
+inline DeformationField make_deformation(VectorField v) { return {std::move(v)}; }
+
+inline bool all_finite(const ScalarVolume& v) {
+    for (float x : v.data)
+        if (!std::isfinite(x)) return false;
+    return true;
+}
+inline bool all_finite(const VectorField& v) {
+    for (float x : v.data)
+        if (!std::isfinite(x)) return false;
+    return true;
+}
+
+// ---- admm.hpp ----------------------------------------------------------------------
+struct SolverConfig {
+    int data_term = 1;
+    int order = 2;
+    double lambda = 0.0;
+    double theta = 0.1;
+    double epsilon = 1e-6;
+    int max_iters = 100;
+    double tol = 0.0;
+    bool accelerate = true;
+    bool log_objective = true;
+};
+
+struct SolverDiagnostics {
+    int iterations = 0;
+    double final_change = 0.0;
+    bool converged = false;
+    std::vector<double> objective;
+    std::vector<double> constraint_residual;
+};
+
+struct SolveResult {
+    VectorField velocity;
+    SolverDiagnostics diagnostics;
+};
+
+// ---- regularizer.hpp ---------------------------------------------------------------
+struct SpectralKernel {
+    int order = 0;
+    Dims3 dims;
+    std::vector<double> values;
+    [[nodiscard]] double at(int p, int q, int r) const {
+        return values[static_cast<std::size_t>(p) +
+                      static_cast<std::size_t>(dims.x) *
+                          (static_cast<std::size_t>(q) + static_cast<std::size_t>(dims.y) * static_cast<std::size_t>(r))];
+    }
+};
+
+// ---- registration.hpp --------------------------------------------------------------
+enum class Profile { capped, converged };
+
+struct RegistrationConfig {
+    SolverConfig solver;
+    int levels = 3;
+    std::vector<int> max_warps_per_level;
+    std::vector<int> max_admm_iters_per_level;
+    double warp_improvement_threshold = 0.02;
+    Profile profile = Profile::capped;
+    bool smooth_levels = true;
+};
+
+struct LevelLog {
+    Dims3 dims;
+    int warps = 0;
+    std::vector<double> mean_sad;
+    std::vector<int> solver_iterations;
+};
+
+struct RegistrationResult {
+    DeformationField phi;
+    ScalarVolume warped;
+    int velocity_count = 0;
+    std::vector<LevelLog> per_level;
+    double elapsed_seconds = 0.0;
+};
+
+// ---- metrics.hpp -------------------------------------------------------------------
+struct JacobianStats {
+    double pct_nonpositive = 0.0;
+    double min_det = 0.0;
+};
+
+// =================================== implementation ==================================
+namespace b200_detail {
+
+struct Ctx {
+    dreg_cuda_ctx* h = nullptr;
+    explicit Ctx(int dev) {
+        const int st = dreg_cuda_ctx_create(dev, &h);
+        if (st != DREG_OK) throw std::runtime_error("dreg_cuda_ctx_create failed (no sm_100 device?)");
+    }
+    ~Ctx() { dreg_cuda_ctx_destroy(h); }
+    Ctx(const Ctx&) = delete;
+    Ctx& operator=(const Ctx&) = delete;
+};
+
+inline int& device_slot() {
+    static int d = 0;
+    return d;
+}
+
+inline dreg_cuda_ctx* ctx() {
+    thread_local std::unique_ptr<Ctx> c;
+    thread_local int dev = -1;
+    if (!c || dev != device_slot()) {
+        c.reset();
+        c = std::make_unique<Ctx>(device_slot());
+        dev = device_slot();
+    }
+    return c->h;
+}
+
+inline void check(int st) {
+    if (st == DREG_OK) return;
+    const std::string msg = dreg_cuda_last_error(ctx());
+    if (st == DREG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    if (st == DREG_NUMERIC) throw numeric_error(msg);
+    throw std::runtime_error(msg);
+}
+
+inline dreg_dims3 D(Dims3 d) { return {d.x, d.y, d.z}; }
+
+inline dreg_solver_cfg S(const SolverConfig& s) {
+    dreg_solver_cfg c;
+    c.data_term = s.data_term;
+    c.order = s.order;
+    c.lambda = s.lambda;
+    c.theta = s.theta;
+    c.epsilon = s.epsilon;
+    c.max_iters = s.max_iters;
+    c.tol = s.tol;
+    c.accelerate = s.accelerate ? 1 : 0;
+    c.log_objective = s.log_objective ? 1 : 0;
+    return c;
+}
+
+inline void same(Dims3 a, Dims3 b, const char* what) {
+    if (!(a == b)) throw std::invalid_argument(std::string(what) + ": dimension mismatch");
+}
+
+}  // namespace b200_detail
+
+/// Device used by this thread's implicit context (default 0).
+inline void set_cuda_device(int device) { b200_detail::device_slot() = device; }
+inline int cuda_device() { return b200_detail::device_slot(); }
+
+inline void validate(const SolverConfig& cfg) {
+    const dreg_solver_cfg c = b200_detail::S(cfg);
+    if (dreg_validate_solver_cfg(&c) != DREG_OK) {
+        if (cfg.data_term != 1 && cfg.data_term != 2) throw std::invalid_argument("solver: data term exponent must be 1 or 2");
+        if (cfg.order < 1 || cfg.order > 6) throw std::invalid_argument("solver: regulariser order must be in [1, 6]");
+        if (!(cfg.lambda >= 0.0)) throw std::invalid_argument("solver: lambda must be >= 0");
+        if (!(cfg.theta > 0.0)) throw std::invalid_argument("solver: theta must be > 0");
+        if (!(cfg.epsilon > 0.0)) throw std::invalid_argument("solver: epsilon must be > 0");
+        if (cfg.max_iters < 1) throw std::invalid_argument("solver: max_iters must be >= 1");
+        throw std::invalid_argument("solver: tol must be >= 0");
+    }
+}
+
+inline double nesterov_next_alpha(double alpha) { return dreg_nesterov_next_alpha(alpha); }
+
+inline SpectralKernel laplacian_symbol(int n, Dims3 dims) {
+    SpectralKernel k{n, dims, std::vector<double>(dims.voxels())};
+    if (dreg_laplacian_symbol(n, b200_detail::D(dims), k.values.data()) != DREG_OK)
+        throw std::invalid_argument("laplacian_symbol: order must be in [1, 6] and every axis >= 2");
+    return k;
+}
+
+inline double regulariser_energy(const VectorField& w, int n) {
+    double e = 0.0;
+    b200_detail::check(dreg_cuda_regulariser_energy(b200_detail::ctx(), w.data.data(), b200_detail::D(w.dims), n, &e));
+    return e;
+}
+
+inline VectorField v_update_l1(const ScalarVolume& target, const ScalarVolume& warped_source, const VectorField& grad,
+                               const VectorField& w_hat, const VectorField& b_hat, const SolverConfig& cfg) {
+    b200_detail::same(target.dims, warped_source.dims, "v_update_l1");
+    b200_detail::same(target.dims, grad.dims, "v_update_l1");
+    b200_detail::same(target.dims, w_hat.dims, "v_update_l1");
+    b200_detail::same(target.dims, b_hat.dims, "v_update_l1");
+    SolverConfig c = cfg;
+    c.data_term = 1;
+    const dreg_solver_cfg s = b200_detail::S(c);
+    VectorField out(target.dims, target.spacing);
+    b200_detail::check(dreg_cuda_v_update(b200_detail::ctx(), target.data.data(), warped_source.data.data(),
+                                          grad.data.data(), w_hat.data.data(), b_hat.data.data(),
+                                          b200_detail::D(target.dims), &s, out.data.data()));
+    return out;
+}
+
+inline VectorField v_update_l2(const ScalarVolume& target, const ScalarVolume& warped_source, const VectorField& grad,
+                               const VectorField& w_hat, const VectorField& b_hat, const SolverConfig& cfg) {
+    b200_detail::same(target.dims, warped_source.dims, "v_update_l2");
+    b200_detail::same(target.dims, grad.dims, "v_update_l2");
+    b200_detail::same(target.dims, w_hat.dims, "v_update_l2");
+    b200_detail::same(target.dims, b_hat.dims, "v_update_l2");
+    SolverConfig c = cfg;
+    c.data_term = 2;
+    const dreg_solver_cfg s = b200_detail::S(c);
+    VectorField out(target.dims, target.spacing);
+    b200_detail::check(dreg_cuda_v_update(b200_detail::ctx(), target.data.data(), warped_source.data.data(),
+                                          grad.data.data(), w_hat.data.data(), b_hat.data.data(),
+                                          b200_detail::D(target.dims), &s, out.data.data()));
+    return out;
+}
+
+inline VectorField w_update(const VectorField& v, const VectorField& b_hat, const SpectralKernel& kernel,
+                            const SolverConfig& cfg) {
+    b200_detail::same(v.dims, b_hat.dims, "w_update");
+    b200_detail::same(v.dims, kernel.dims, "w_update: kernel");
+    SolverConfig c = cfg;
+    c.order = kernel.order;  // the device builds the symbol of this order on the fly
+    const dreg_solver_cfg s = b200_detail::S(c);
+    VectorField out(v.dims, v.spacing);
+    b200_detail::check(dreg_cuda_w_update(b200_detail::ctx(), v.data.data(), b_hat.data.data(), b200_detail::D(v.dims),
+                                          &s, out.data.data()));
+    return out;
+}
+
+inline SolveResult solve_velocity(const ScalarVolume& target, const ScalarVolume& warped_source,
+                                  const SolverConfig& cfg) {
+    validate(cfg);
+    b200_detail::same(target.dims, warped_source.dims, "solve_velocity");
+    const dreg_solver_cfg s = b200_detail::S(cfg);
+    SolveResult r{VectorField(target.dims, target.spacing), {}};
+    std::vector<double> obj(static_cast<std::size_t>(cfg.max_iters)), res(static_cast<std::size_t>(cfg.max_iters));
+    dreg_solver_diag d{0, 0.0, 0, obj.data(), res.data()};
+    b200_detail::check(dreg_cuda_solve_velocity(b200_detail::ctx(), target.data.data(), warped_source.data.data(),
+                                                b200_detail::D(target.dims), &s, r.velocity.data.data(), &d));
+    r.diagnostics.iterations = d.iterations;
+    r.diagnostics.final_change = d.final_change;
+    r.diagnostics.converged = d.converged != 0;
+    if (cfg.log_objective) r.diagnostics.objective.assign(obj.begin(), obj.begin() + d.iterations);
+    r.diagnostics.constraint_residual.assign(res.begin(), res.begin() + d.iterations);
+    return r;
+}
+
+inline RegistrationConfig make_registration_config(Profile profile, SolverConfig solver, int levels = 3) {
+    if (levels < 1) throw std::invalid_argument("registration: levels must be >= 1");
+    dreg_reg_cfg c;
+    const dreg_solver_cfg s = b200_detail::S(solver);
+    if (dreg_make_registration_config(profile == Profile::converged ? DREG_PROFILE_CONVERGED : DREG_PROFILE_CAPPED,
+                                      &s, levels, &c) != DREG_OK)
+        throw std::invalid_argument("registration: levels must be >= 1");
+    RegistrationConfig r;
+    r.solver = solver;
+    r.solver.tol = c.solver.tol;
+    r.levels = levels;
+    r.max_warps_per_level.assign(c.max_warps_per_level, c.max_warps_per_level + levels);
+    r.max_admm_iters_per_level.assign(c.max_admm_iters_per_level, c.max_admm_iters_per_level + levels);
+    r.warp_improvement_threshold = c.warp_improvement_threshold;
+    r.profile = profile;
+    r.smooth_levels = true;
+    return r;
+}
+
+inline dreg_reg_cfg to_c(const RegistrationConfig& cfg) {
+    if (cfg.levels < 1) throw std::invalid_argument("register_pair: levels must be >= 1");
+    if (cfg.max_warps_per_level.size() != static_cast<std::size_t>(cfg.levels) ||
+        cfg.max_admm_iters_per_level.size() != static_cast<std::size_t>(cfg.levels))
+        throw std::invalid_argument("register_pair: per-level caps must list one entry per level");
+    if (cfg.levels > DREG_MAX_LEVELS) throw std::invalid_argument("register_pair: too many levels");
+    dreg_reg_cfg c;
+    std::memset(&c, 0, sizeof c);
+    c.solver = b200_detail::S(cfg.solver);
+    c.levels = cfg.levels;
+    for (int l = 0; l < cfg.levels; ++l) {
+        c.max_warps_per_level[l] = cfg.max_warps_per_level[static_cast<std::size_t>(l)];
+        c.max_admm_iters_per_level[l] = cfg.max_admm_iters_per_level[static_cast<std::size_t>(l)];
+    }
+    c.warp_improvement_threshold = cfg.warp_improvement_threshold;
+    c.profile = cfg.profile == Profile::converged ? DREG_PROFILE_CONVERGED : DREG_PROFILE_CAPPED;
+    c.smooth_levels = cfg.smooth_levels ? 1 : 0;
+    return c;
+}
+
+inline RegistrationResult register_pair(const ScalarVolume& target, const ScalarVolume& source,
+                                        const RegistrationConfig& cfg) {
+    b200_detail::same(target.dims, source.dims, "register_pair");
+    const dreg_reg_cfg c = to_c(cfg);
+    RegistrationResult r;
+    r.phi = DeformationField::identity(target.dims, target.spacing);
+    r.warped = ScalarVolume(target.dims, target.spacing);
+    dreg_pair_result pr;
+    b200_detail::check(dreg_cuda_register_pair(b200_detail::ctx(), target.data.data(), source.data.data(),
+                                               b200_detail::D(target.dims),
+                                               {target.spacing.x, target.spacing.y, target.spacing.z}, &c,
+                                               r.phi.disp.data.data(), r.warped.data.data(), &pr));
+    r.velocity_count = pr.velocity_count;
+    for (int l = 0; l < pr.levels; ++l) {
+        const dreg_level_log& lg = pr.per_level[l];
+        LevelLog o;
+        o.dims = {lg.dims.x, lg.dims.y, lg.dims.z};
+        o.warps = lg.warps;
+        o.mean_sad.assign(lg.mean_sad, lg.mean_sad + lg.warps + 1);
+        o.solver_iterations.assign(lg.solver_iterations, lg.solver_iterations + lg.warps);
+        r.per_level.push_back(std::move(o));
+    }
+    r.elapsed_seconds = pr.elapsed_seconds;
+    return r;
+}
+
+inline ScalarVolume warp_image(const ScalarVolume& img, const DeformationField& phi) {
+    b200_detail::same(img.dims, phi.disp.dims, "warp_image");
+    ScalarVolume out(img.dims, img.spacing);
+    b200_detail::check(dreg_cuda_warp_image(b200_detail::ctx(), img.data.data(), phi.disp.data.data(),
+                                            b200_detail::D(img.dims), out.data.data()));
+    return out;
+}
+
+inline VectorField image_gradient(const ScalarVolume& img) {
+    VectorField out(img.dims, img.spacing);
+    b200_detail::check(dreg_cuda_image_gradient(b200_detail::ctx(), img.data.data(), b200_detail::D(img.dims),
+                                                out.data.data()));
+    return out;
+}
+
+inline DeformationField compose_deformation(const DeformationField& phi, const VectorField& v) {
+    b200_detail::same(phi.disp.dims, v.dims, "compose_deformation");
+    DeformationField out{VectorField(v.dims, phi.disp.spacing)};
+    b200_detail::check(dreg_cuda_compose_deformation(b200_detail::ctx(), phi.disp.data.data(), v.data.data(),
+                                                     b200_detail::D(v.dims), out.disp.data.data()));
+    return out;
+}
+
+inline ScalarVolume jacobian_determinant(const DeformationField& phi) {
+    ScalarVolume out(phi.disp.dims, phi.disp.spacing);
+    b200_detail::check(dreg_cuda_jacobian(b200_detail::ctx(), phi.disp.data.data(), b200_detail::D(phi.disp.dims),
+                                          out.data.data(), nullptr));
+    return out;
+}
+
+inline JacobianStats jacobian_stats(const DeformationField& phi) {
+    dreg_jacobian_stats st;
+    b200_detail::check(dreg_cuda_jacobian(b200_detail::ctx(), phi.disp.data.data(), b200_detail::D(phi.disp.dims),
+                                          nullptr, &st));
+    return {st.pct_nonpositive, st.min_det};
+}
+
+inline std::pair<ScalarVolume, ScalarVolume> normalize_intensity_pair(const ScalarVolume& a, const ScalarVolume& b) {
+    b200_detail::same(a.dims, b.dims, "normalize_intensity_pair");
+    ScalarVolume oa(a.dims, a.spacing), ob(b.dims, b.spacing);
+    b200_detail::check(dreg_cuda_normalize_intensity_pair(b200_detail::ctx(), a.data.data(), b.data.data(),
+                                                          b200_detail::D(a.dims), oa.data.data(), ob.data.data()));
+    return {std::move(oa), std::move(ob)};
+}
+
+inline ScalarVolume binomial_smooth(const ScalarVolume& img) {
+    ScalarVolume out(img.dims, img.spacing);
+    b200_detail::check(dreg_cuda_binomial_smooth(b200_detail::ctx(), img.data.data(), b200_detail::D(img.dims),
+                                                 out.data.data()));
+    return out;
+}
+
+inline double mean_sad(const ScalarVolume& a, const ScalarVolume& b) {
+    b200_detail::same(a.dims, b.dims, "mean_sad");
+    double m = 0.0;
+    b200_detail::check(dreg_cuda_mean_sad(b200_detail::ctx(), a.data.data(), b.data.data(), b200_detail::D(a.dims), &m));
+    return m;
+}
+
+inline ScalarVolume downsample(const ScalarVolume& img) {
+    const Dims3 o{(img.dims.x + 1) / 2, (img.dims.y + 1) / 2, (img.dims.z + 1) / 2};
+    ScalarVolume out(o, {img.spacing.x * 2.0, img.spacing.y * 2.0, img.spacing.z * 2.0});
+    b200_detail::check(dreg_cuda_downsample(b200_detail::ctx(), img.data.data(), b200_detail::D(img.dims),
+                                            out.data.data()));
+    return out;
+}
+
+inline VectorField upsample_velocity(const VectorField& v, Dims3 target_dims) {
+    VectorField out(target_dims, {v.spacing.x / 2.0, v.spacing.y / 2.0, v.spacing.z / 2.0});
+    b200_detail::check(dreg_cuda_upsample_velocity(b200_detail::ctx(), v.data.data(), b200_detail::D(v.dims),
+                                                   b200_detail::D(target_dims), out.data.data()));
+    return out;
+}
+
+inline DeformationField upsample_deformation(const DeformationField& phi, Dims3 target_dims) {
+    return {upsample_velocity(phi.disp, target_dims)};
+}
+
+}  // namespace dreg

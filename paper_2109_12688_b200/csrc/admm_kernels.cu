@@ -628,7 +628,7 @@ static cudaError_t launch_fast(const PArgs& a, int mode, int npairs, cudaStream_
     constexpr int R1Z = NZ == 256 ? 16 : (NZ >= 64 ? 8 : 4);
     constexpr int NT = 256;
     using Lay = PlaneLayout<NY, NY / R1Y>;
-    const size_t smem = sizeof(float2) * NZ * Lay::P + sizeof(double) * 32;
+    const size_t smem = sizeof(float2) * (NZ * Lay::P + NY + NZ) + sizeof(double) * 32 + sizeof(float) * (NY + NZ);
     void (*k)(PArgs) = mode == 0 ? plane_fast_kernel<NY, NZ, R1Y, R1Z, NT, 0> : plane_fast_kernel<NY, NZ, R1Y, R1Z, NT, 1>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

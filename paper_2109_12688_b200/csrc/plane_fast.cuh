@@ -79,15 +79,26 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
     extern __shared__ __align__(16) unsigned char smem[];
     float2* buf = reinterpret_cast<float2*>(smem);
     double* red = reinterpret_cast<double*>(buf + NZ * Lay::P);
+    float2* twy = reinterpret_cast<float2*>(red + 32);  // tables staged once per CTA
+    float2* twz = twy + NY;
+    float* sys = reinterpret_cast<float*>(twz + NZ);
+    float* szs = sys + NY;
     const int tid = threadIdx.x;
     const int hx = a.F.hx;
     const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
     float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)a.F.lines;
-    const float2* __restrict__ twy = a.twy;
-    const float2* __restrict__ twz = a.twz;
+    for (int i = tid; i < NY; i += NT) {
+        twy[i] = __ldg(a.twy + i);
+        sys[i] = __ldg(a.sy_fast + i);
+    }
+    for (int i = tid; i < NZ; i += NT) {
+        twz[i] = __ldg(a.twz + i);
+        szs[i] = __ldg(a.sz_fast + i);
+    }
+    __syncthreads();
 
     // y stage 1 (DIF radix R1Y, n1 = R2Y), straight from global
-#pragma unroll 2
+#pragma unroll
     for (int b = tid; b < NZ * R2Y; b += NT) {
         const int j1 = b % R2Y, z = b / R2Y;
         float2 x[R1Y];
@@ -95,7 +106,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
         for (int t = 0; t < R1Y; ++t) x[t] = __ldg(Sp + z * NY + j1 + R2Y * t);
         rdft<false, R1Y>(x);
 #pragma unroll
-        for (int k = 1; k < R1Y; ++k) x[k] = cmul(x[k], __ldg(twy + j1 * k));
+        for (int k = 1; k < R1Y; ++k) x[k] = cmul(x[k], twy[j1 * k]);
 #pragma unroll
         for (int k = 0; k < R1Y; ++k) buf[Lay::at(j1 + R2Y * k, z)] = x[k];
     }
@@ -119,13 +130,14 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
         for (int t = 0; t < R1Z; ++t) x[t] = buf[Lay::at(y, j1 + R2Z * t)];
         rdft<false, R1Z>(x);
 #pragma unroll
-        for (int k = 1; k < R1Z; ++k) x[k] = cmul(x[k], __ldg(twz + j1 * k));
+        for (int k = 1; k < R1Z; ++k) x[k] = cmul(x[k], twz[j1 * k]);
 #pragma unroll
         for (int k = 0; k < R1Z; ++k) buf[Lay::at(y, j1 + R2Z * k)] = x[k];
     }
     __syncthreads();
     // z stage 2 + multiplier + adjoint z stage 2 (or the energy sum)
     const float sxp = __ldg(a.sx + p);
+    const int order = a.order;
     double acc = 0.0;
     for (int b = tid; b < NY * R1Z; b += NT) {
         const int y = b % NY, blk = b / NY;
@@ -133,14 +145,19 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
 #pragma unroll
         for (int e = 0; e < R2Z; ++e) x[e] = buf[Lay::at(y, blk * R2Z + e)];
         rdft<false, R2Z>(x);
-        const float sy = __ldg(a.sy_fast + y);
+        const float sy = sys[y];
         if (MODE == 0) {
+            const float sxy = sxp + sy;
 #pragma unroll
             for (int e = 0; e < R2Z; ++e) {
-                const float base = 2.0f * (sxp + sy + __ldg(a.sz_fast + blk * R2Z + e));
-                float K = base;
-                for (int q = 1; q < a.order; ++q) K *= base;
-                const float m = a.scale / (a.lambda * K + a.theta);
+                // theta / (lambda (2 s)^n + theta) / N, s = 3 - cos - cos - cos (regularizer.cpp:69-73)
+                const float base = 2.0f * (sxy + szs[blk * R2Z + e]);
+                const float b2 = base * base;
+                float K = (order & 1) ? base : 1.0f;
+                K *= order >= 2 ? b2 : 1.0f;
+                K *= order >= 4 ? b2 : 1.0f;
+                K *= order >= 6 ? b2 : 1.0f;
+                const float m = a.scale * __frcp_rn(fmaf(a.lambda, K, a.theta));
                 x[e] = make_float2(x[e].x * m, x[e].y * m);
             }
             rdft<true, R2Z>(x);
@@ -149,7 +166,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
         } else {
 #pragma unroll
             for (int e = 0; e < R2Z; ++e) {
-                const double base = 2.0 * ((double)sxp + (double)sy + (double)__ldg(a.sz_fast + blk * R2Z + e));
+                const double base = 2.0 * ((double)sxp + (double)sy + (double)szs[blk * R2Z + e]);
                 double K = base;
                 for (int q = 1; q < a.order; ++q) K *= base;
                 acc += K * ((double)x[e].x * x[e].x + (double)x[e].y * x[e].y);
@@ -174,7 +191,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
 #pragma unroll
         for (int k = 0; k < R1Z; ++k) x[k] = buf[Lay::at(y, j1 + R2Z * k)];
 #pragma unroll
-        for (int k = 1; k < R1Z; ++k) x[k] = cmulc(x[k], __ldg(twz + j1 * k));
+        for (int k = 1; k < R1Z; ++k) x[k] = cmulc(x[k], twz[j1 * k]);
         rdft<true, R1Z>(x);
 #pragma unroll
         for (int t = 0; t < R1Z; ++t) buf[Lay::at(y, j1 + R2Z * t)] = x[t];
@@ -199,7 +216,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
 #pragma unroll
         for (int k = 0; k < R1Y; ++k) x[k] = buf[Lay::at(j1 + R2Y * k, z)];
 #pragma unroll
-        for (int k = 1; k < R1Y; ++k) x[k] = cmulc(x[k], __ldg(twy + j1 * k));
+        for (int k = 1; k < R1Y; ++k) x[k] = cmulc(x[k], twy[j1 * k]);
         rdft<true, R1Y>(x);
 #pragma unroll
         for (int t = 0; t < R1Y; ++t) Sp[z * NY + j1 + R2Y * t] = x[t];

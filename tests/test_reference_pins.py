@@ -1,0 +1,344 @@
+"""The reference's own hot-path test pins (proj/tests/test_{admm,volume,regularizer,
+registration}.cpp and acceptance_main.cpp), restated with numpy and run against the
+CPU oracle (always) and the sm_100a path (-m gpu).  Cited per test; parameters and
+tolerances follow the reference unless noted (the GPU spectral solve is fp32, held
+to the reference's own 1e-5 * max|ref| w-update tolerance).
+"""
+import numpy as np
+import pytest
+
+from conftest import Rng, random_field, random_volume, smooth_random_field
+from paper_2109_12688_b200 import abi
+
+
+@pytest.fixture(params=["oracle", pytest.param("gpu", marks=pytest.mark.gpu)])
+def lib(request, oracle):
+    if request.param == "oracle":
+        return oracle
+    return request.getfixturevalue("ctx")
+
+
+def dense_neg_laplacian(shape):
+    """oracles.cpp:111-131: periodic 7-point negative Laplacian, voxels x voxels."""
+    z, y, x = shape
+    n = x * y * z
+    m = np.zeros((n, n))
+    idx = lambda xx, yy, zz: (xx % x) + x * ((yy % y) + y * (zz % z))  # noqa: E731
+    for k in range(z):
+        for j in range(y):
+            for i in range(x):
+                r = idx(i, j, k)
+                m[r, r] += 6.0
+                for d in ((-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)):
+                    m[r, idx(i + d[0], j + d[1], k + d[2])] -= 1.0
+    return m
+
+
+def dense_w_solve(rhs, order, lam, theta):
+    """oracles.cpp:141-164: (lambda K^n + theta I) w = theta rhs per component."""
+    shp = rhs.shape[:3]
+    K = np.linalg.matrix_power(dense_neg_laplacian(shp), order)
+    A = lam * K + theta * np.eye(K.shape[0])
+    out = np.zeros_like(rhs, dtype=np.float64)
+    for c in range(3):
+        out[..., c] = np.linalg.solve(A, theta * rhs[..., c].reshape(-1).astype(np.float64)).reshape(shp)
+    return out
+
+
+# ---- test_admm.cpp ---------------------------------------------------------------
+def test_alpha_sequence(lib):
+    """test_admm.cpp:53-64: alpha_1 = 1.618034, first coefficient 0, increasing."""
+    a = 1.0
+    nxt = lib.nesterov_next_alpha(a)
+    assert abs(nxt - 1.618034) < 1e-6
+    assert (a - 1.0) / nxt == 0.0
+    prev = nxt
+    for _ in range(50):
+        cur = lib.nesterov_next_alpha(prev)
+        assert cur > prev
+        prev = cur
+
+
+def _one_voxel(vals):
+    return np.array(vals, np.float32).reshape(1, 1, 1, 3)
+
+
+def test_l1_zero_residual_returns_u(lib):
+    """test_admm.cpp:66-89: rho(w_hat - b_hat) = 0 -> v = w_hat - b_hat (theta 0.07)."""
+    g = _one_voxel([0.5, -0.25, 1.0])
+    wh, bh = _one_voxel([0.3, 0.1, -0.2]), _one_voxel([0.1, -0.1, 0.05])
+    u = (wh.astype(np.float64) - bh)
+    # choose warped - target so that g.u + d = 0
+    d = -float((g.astype(np.float64) * u).sum())
+    t = np.zeros((1, 1, 1), np.float32)
+    w = np.array(d, np.float32).reshape(1, 1, 1)
+    out = lib.v_update(t, w, g, wh, bh, abi.solver_cfg(data_term=1, theta=0.07))
+    assert np.allclose(out, u, atol=1e-6)
+
+
+@pytest.mark.parametrize("dt", [1, 2])
+def test_zero_gradient_returns_u(lib, dt):
+    """test_admm.cpp:91-109 (l1, theta 0.1) and :136-153 (l2, 2^3, seeds 9/10, theta 0.05)."""
+    shp = (2, 2, 2)
+    wh, bh = random_field(shp, 9, 1.0), random_field(shp, 10, 1.0)
+    g = np.zeros_like(wh)
+    t, w = random_volume(shp, 11), random_volume(shp, 12)
+    out = lib.v_update(t, w, g, wh, bh, abi.solver_cfg(data_term=dt, theta=0.1 if dt == 1 else 0.05))
+    assert np.allclose(out, wh.astype(np.float64) - bh, atol=1e-6)
+
+
+def test_l2_normal_equation(lib):
+    """test_admm.cpp:155-182: (g g^T + theta I) v = theta u - d g; 8^3 seed 900, theta 0.09."""
+    shp = (8, 8, 8)
+    g, wh, bh = random_field(shp, 900, 1.0), random_field(shp, 901, 1.0), random_field(shp, 902, 1.0)
+    t, w = random_volume(shp, 903), random_volume(shp, 904)
+    theta = 0.09
+    v = lib.v_update(t, w, g, wh, bh, abi.solver_cfg(data_term=2, theta=theta)).astype(np.float64)
+    g64 = g.astype(np.float64)
+    u = wh.astype(np.float64) - bh
+    d = (w.astype(np.float64) - t)[..., None]
+    rhs = theta * u - d * g64
+    lhs = g64 * (g64 * v).sum(-1, keepdims=True) + theta * v
+    scale = 1.0 + np.abs(rhs).max()
+    assert np.abs(lhs - rhs).max() <= 1e-5 * scale * 10  # fp32 storage of v
+
+
+def test_l1_matches_line_search(lib):
+    """test_admm.cpp:111-134: closed-form l1 vs a dense sweep of t in u + t g (theta 0.08)."""
+    shp = (4, 4, 4)
+    theta = 0.08
+    for seed in range(500, 503):
+        g, wh, bh = random_field(shp, seed, 1.0), random_field(shp, seed + 10, 1.0), random_field(shp, seed + 20, 1.0)
+        t, w = random_volume(shp, seed + 30), random_volume(shp, seed + 40)
+        v = lib.v_update(t, w, g, wh, bh, abi.solver_cfg(data_term=1, theta=theta)).astype(np.float64)
+        g64 = g.astype(np.float64).reshape(-1, 3)
+        u = (wh.astype(np.float64) - bh).reshape(-1, 3)
+        d = (w.astype(np.float64) - t).reshape(-1)
+        gg = (g64 * g64).sum(1)
+        rho_u = (g64 * u).sum(1) + d
+        # objective along the gradient direction: |rho(u) + t gg| + theta/2 t^2 gg
+        ts = np.linspace(-40, 40, 160001)
+        for i in range(0, u.shape[0], 7):
+            f = np.abs(rho_u[i] + ts * gg[i]) + 0.5 * theta * ts * ts * gg[i]
+            tb = ts[np.argmin(f)]
+            assert np.allclose(v.reshape(-1, 3)[i], u[i] + tb * g64[i], atol=2e-3)
+
+
+@pytest.mark.parametrize("shape", [(4, 4, 4), (4, 6, 4), (4, 4, 5)])
+@pytest.mark.parametrize("order", [1, 2])
+def test_w_update_dense_solve(lib, shape, order):
+    """test_admm.cpp:184-211: w_update == dense periodic solve, lambda 2, theta 0.1."""
+    v, bh = random_field(shape, 40 + order, 1.0), random_field(shape, 50 + order, 1.0)
+    out = lib.w_update(v, bh, abi.solver_cfg(order=order, lambda_=2.0, theta=0.1))
+    ref = dense_w_solve(v.astype(np.float64) + bh, order, 2.0, 0.1)
+    assert np.abs(out - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+def test_w_update_lambda_zero_and_constant(lib):
+    """test_admm.cpp:213-248: lambda 0 -> v + b_hat; constant field passes through."""
+    v, bh = random_field((6, 6, 6), 60, 1.0), random_field((6, 6, 6), 61, 1.0)
+    out = lib.w_update(v, bh, abi.solver_cfg(order=2, lambda_=0.0, theta=0.1))
+    assert np.abs(out - (v.astype(np.float64) + bh)).max() <= 1e-5
+    c = np.full((4, 4, 4, 3), 0.75, np.float32)
+    out = lib.w_update(c, np.zeros_like(c), abi.solver_cfg(order=2, lambda_=3.0, theta=0.1))
+    assert np.abs(out - 0.75).max() <= 1e-6
+
+
+def test_identical_images_give_zero_velocity(lib):
+    """test_admm.cpp:250-266: I0 == I1 -> mean |v| <= 1e-4."""
+    blob = gaussian_blob((12, 12, 12), (5.5, 5.5, 5.5), 3.0)
+    v, d = lib.solve_velocity(blob, blob,
+                              abi.solver_cfg(data_term=1, order=1, lambda_=1.0, theta=0.1, max_iters=50, tol=1e-7))
+    assert np.abs(v).mean() <= 1e-4
+
+
+def test_constraint_residual_shrinks(lib):
+    """test_admm.cpp:268-284: l2, n 1, lambda 2, theta 0.05, tol 1e-4 on 16^3."""
+    zz, yy, xx = np.mgrid[0:16, 0:16, 0:16]
+    a = np.exp(-((xx - 7.5) ** 2 + (yy - 8) ** 2 + (zz - 8) ** 2) / 18.0).astype(np.float32)
+    b = np.exp(-((xx - 8.5) ** 2 + (yy - 8) ** 2 + (zz - 8) ** 2) / 18.0).astype(np.float32)
+    v, d = lib.solve_velocity(a, b, abi.solver_cfg(data_term=2, order=1, lambda_=2.0, theta=0.05, max_iters=400,
+                                                   tol=1e-4, log_objective=False))
+    r = d["constraint_residual"]
+    assert r[-1] < r[0]
+
+
+def gaussian_blob(shape, centre, sigma):
+    """test_admm.cpp:35-47."""
+    z, y, x = shape
+    zz, yy, xx = np.mgrid[0:z, 0:y, 0:x].astype(np.float64)
+    d2 = (xx - centre[0]) ** 2 + (yy - centre[1]) ** 2 + (zz - centre[2]) ** 2
+    return np.exp(-d2 / (2.0 * sigma * sigma)).astype(np.float32)
+
+
+def test_accelerate_on_off_same_objective(lib):
+    """test_admm.cpp:362-382: accelerated and plain both converge to objectives within 1%."""
+    t = gaussian_blob((12, 12, 12), (5.5, 5.5, 5.5), 2.5)
+    s = gaussian_blob((12, 12, 12), (6.3, 5.5, 5.5), 2.5)
+    objs = []
+    for acc in (True, False):
+        v, d = lib.solve_velocity(t, s, abi.solver_cfg(data_term=2, order=2, lambda_=3.0, theta=0.05, max_iters=400,
+                                                       tol=1e-5, accelerate=acc, log_objective=True))
+        assert d["converged"]
+        objs.append(d["objective"][-1])
+    assert abs(objs[0] - objs[1]) <= 0.01 * abs(objs[1])
+
+
+def test_acceptance_acceleration_criterion(lib):
+    """acceptance_main.cpp:164-210 (criterion 3): 32^3 sinusoid shifted by 4 voxels,
+    accelerated needs <= the plain iterations and objectives agree within 1%."""
+    r = Rng(11)
+    ph = r.uniform(3, 0.0, 6.28)
+    zz, yy, xx = np.mgrid[0:32, 0:32, 0:32].astype(np.float64)
+    img = lambda x, y, z: 0.5 + 0.4 * np.sin(2 * 3.14159265358979 * x / 16 + ph[0]) * \
+        np.sin(2 * 3.14159265358979 * y / 16 + ph[1]) * np.sin(2 * 3.14159265358979 * z / 16 + ph[2])  # noqa: E731
+    t = img(xx, yy, zz).astype(np.float32)
+    s = img(xx + 4.0, yy, zz).astype(np.float32)
+    res = []
+    for acc in (True, False):
+        v, d = lib.solve_velocity(t, s, abi.solver_cfg(data_term=2, order=2, lambda_=1.0, theta=0.02, max_iters=2000,
+                                                       tol=0.01, accelerate=acc, log_objective=True))
+        assert d["converged"]
+        res.append((d["iterations"], d["objective"][-1]))
+    assert res[0][0] <= res[1][0]
+    assert abs(res[0][1] - res[1][1]) <= 0.01 * abs(res[1][1])
+
+
+# ---- test_regularizer.cpp ---------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_symbol_identities(oracle, n):
+    """test_regularizer.cpp:66-101: zero at DC, 4^n at pure-x Nyquist, <= 12^n."""
+    k = oracle.laplacian_symbol(n, (8, 6, 4))
+    assert k[0, 0, 0] == 0.0
+    assert abs(k[0, 0, 4] - 4.0 ** n) <= 1e-9 * 4.0 ** n
+    assert k.max() <= 12.0 ** n + 1e-9
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_energy_dense_form_and_homogeneity(lib, n):
+    """test_regularizer.cpp:114-154: energy == 0.5 sum w^T K^n w; quadratic in w."""
+    w = random_field((4, 5, 4), 70 + n, 1.0)
+    K = np.linalg.matrix_power(dense_neg_laplacian(w.shape[:3]), n)
+    ref = 0.5 * sum(w[..., c].reshape(-1).astype(np.float64) @ K @ w[..., c].reshape(-1).astype(np.float64)
+                    for c in range(3))
+    e = lib.regulariser_energy(w, n)
+    assert abs(e - ref) <= (1e-9 if lib.__class__.__name__ == "CpuLib" else 2e-6) * abs(ref)
+    e2 = lib.regulariser_energy(w * np.float32(2.0), n)
+    assert abs(e2 - 4 * e) <= 1e-5 * abs(e2)
+
+
+# ---- test_volume.cpp --------------------------------------------------------------
+def test_trilinear_lattice_and_clamp(lib):
+    """test_volume.cpp:39-70: lattice points exact; clamped outside; affine images exact."""
+    shp = (8, 8, 8)
+    zz, yy, xx = np.mgrid[0:8, 0:8, 0:8].astype(np.float32)
+    affine = (0.5 * xx + 0.25 * yy - 0.125 * zz + 1.0).astype(np.float32)
+    disp = np.zeros(shp + (3,), np.float32)
+    disp[..., 0] = 0.5
+    out = lib.warp_image(affine, disp)
+    expect = 0.5 * np.minimum(xx + 0.5, 7) + 0.25 * yy - 0.125 * zz + 1.0
+    assert np.allclose(out, expect, atol=1e-6)
+    disp[..., 0] = -20.0
+    out = lib.warp_image(affine, disp)
+    assert np.allclose(out, 0.25 * yy - 0.125 * zz + 1.0, atol=1e-6)
+
+
+def test_warp_matches_naive(lib):
+    """test_volume.cpp:79-97: warp == naive trilinear oracle (1e-6), 8^3 seeds 21/22, amplitude 1.5."""
+    img, disp = random_volume((8, 8, 8), 21), random_field((8, 8, 8), 22, 1.5)
+    out = lib.warp_image(img, disp)
+    z, y, x = img.shape
+    ref = np.zeros_like(out, dtype=np.float64)
+    for k in range(z):
+        for j in range(y):
+            for i in range(x):
+                p = np.array([i, j, k], np.float64) + disp[k, j, i].astype(np.float64)
+                c = np.clip(p, 0, np.array([x - 1, y - 1, z - 1], np.float64))
+                lo = np.floor(c).astype(int)
+                hi = np.minimum(lo + 1, [x - 1, y - 1, z - 1])
+                f = c - lo
+                acc = 0.0
+                for dz in (0, 1):
+                    for dy in (0, 1):
+                        for dx in (0, 1):
+                            wgt = (f[0] if dx else 1 - f[0]) * (f[1] if dy else 1 - f[1]) * (f[2] if dz else 1 - f[2])
+                            acc += wgt * img[hi[2] if dz else lo[2], hi[1] if dy else lo[1], hi[0] if dx else lo[0]]
+                ref[k, j, i] = acc
+    assert np.abs(out - ref).max() <= 1e-6
+
+
+def test_gradient_exact_cases(lib):
+    """test_volume.cpp:105-141: ramp, constant and quadratic profiles."""
+    zz, yy, xx = np.mgrid[0:6, 0:7, 0:8].astype(np.float32)
+    g = lib.image_gradient((2 * xx - 3 * yy + 0.5 * zz).astype(np.float32))
+    assert np.allclose(g[..., 0], 2) and np.allclose(g[..., 1], -3) and np.allclose(g[..., 2], 0.5)
+    assert np.array_equal(lib.image_gradient(np.full((4, 4, 4), 3.0, np.float32)), np.zeros((4, 4, 4, 3), np.float32))
+    q = (xx * xx).astype(np.float32)
+    g = lib.image_gradient(q)
+    assert np.allclose(g[:, :, 1:-1, 0], 2 * xx[:, :, 1:-1])  # central difference exact on quadratics
+    assert np.allclose(g[:, :, 0, 0], 1.0) and np.allclose(g[:, :, -1, 0], 49 - 36)
+
+
+def test_compose_translations_add(lib, oracle):
+    """test_volume.cpp:148-190: v = 0 bit-exact; translations add."""
+    a = smooth_random_field((8, 8, 8), 51, 0.4, oracle)
+    assert np.array_equal(lib.compose_deformation(a, np.zeros_like(a)), a)
+    t1 = np.zeros((8, 8, 8, 3), np.float32)
+    t1[..., 0] = 0.5
+    t2 = np.zeros_like(t1)
+    t2[..., 1] = -0.25
+    out = lib.compose_deformation(t1, t2)
+    interior = out[1:-1, 1:-1, 1:-1]
+    assert np.allclose(interior[..., 0], 0.5) and np.allclose(interior[..., 1], -0.25)
+
+
+def test_jacobian_identities(lib):
+    """test_volume.cpp:214-248: det 1 for identity/translation; (1+a)(1+b)(1+c) for linear maps."""
+    u = np.zeros((6, 7, 8, 3), np.float32)
+    assert np.allclose(lib.jacobian_determinant(u), 1.0)
+    u[..., 0] = 1.25
+    assert np.allclose(lib.jacobian_determinant(u), 1.0)
+    zz, yy, xx = np.mgrid[0:6, 0:7, 0:8].astype(np.float32)
+    u = np.stack([0.1 * xx, -0.2 * yy, 0.3 * zz], -1).astype(np.float32)
+    assert np.allclose(lib.jacobian_determinant(u), 1.1 * 0.8 * 1.3, atol=1e-5)
+
+
+# ---- test_registration.cpp -----------------------------------------------------------
+def test_register_identity_pair(lib):
+    """test_registration.cpp:197-210: identity pair -> mean |u| <= 0.05."""
+    from paper_2109_12688_b200 import synth
+
+    f, _ = synth.make_pair(1, 9, (16, 16, 16))
+    s = abi.solver_cfg(data_term=1, order=2, lambda_=5.0, theta=0.05, max_iters=10, log_objective=False)
+    phi, warped, res = lib.register_pair(f, f, abi.reg_cfg(s, 1, (5,), (10,)))
+    assert np.abs(phi).mean() <= 0.05
+
+
+def test_register_translation_recovery(lib):
+    """test_registration.cpp:211-230: a translated blob is recovered (interior mean error)."""
+    zz, yy, xx = np.mgrid[0:24, 0:24, 0:24].astype(np.float64)
+    t = np.exp(-((xx - 12) ** 2 + (yy - 12) ** 2 + (zz - 12) ** 2) / (2 * 16.0)).astype(np.float32)
+    s = np.exp(-((xx - 13) ** 2 + (yy - 12) ** 2 + (zz - 12) ** 2) / (2 * 16.0)).astype(np.float32)
+    cfg = abi.reg_cfg(abi.solver_cfg(data_term=2, order=2, lambda_=0.05, theta=0.5, max_iters=50,
+                                     log_objective=False), 1, (10,), (50,))
+    phi, warped, res = lib.register_pair(t, s, cfg)
+    core = phi[8:16, 8:16, 8:16]
+    assert abs(core[..., 0].mean() - 1.0) <= 0.5
+    assert res.velocity_count >= 1
+    # accepted mean SAD is monotone (test_registration.cpp:263-284)
+    ms = abi.level_logs(res)[0]["mean_sad"]
+    assert all(b <= a for a, b in zip(ms, ms[1:]))
+
+
+def test_register_rejects_bad_input(lib):
+    """test_registration.cpp:304-349: NaN -> numeric_error; invalid configs -> invalid_argument."""
+    f = random_volume((8, 8, 8), 5)
+    m = f.copy()
+    m[1, 2, 3] = np.nan
+    ok = abi.reg_cfg(abi.solver_cfg(max_iters=2), 1, (1,), (2,))
+    with pytest.raises(Exception) as e:
+        lib.register_pair(f, m, ok)
+    assert "non-finite" in str(e.value)
+    bad = abi.reg_cfg(abi.solver_cfg(order=7), 1, (1,), (2,))
+    with pytest.raises(Exception):
+        lib.register_pair(f, f, bad)
