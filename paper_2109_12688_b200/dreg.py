@@ -177,6 +177,12 @@ class Context:
         if st != abi.DREG_OK:
             _raise(st, self.lib.dreg_cuda_last_error(self.h).decode())
 
+    # ---- host helpers (same names as the module functions / reference API) --------
+    nesterov_next_alpha = staticmethod(nesterov_next_alpha)
+    validate = staticmethod(validate)
+    make_registration_config = staticmethod(make_registration_config)
+    laplacian_symbol = staticmethod(laplacian_symbol)
+
     # ---- context knobs ---------------------------------------------------------
     def kernel_launches(self) -> int:
         return int(self.lib.dreg_cuda_kernel_launches(self.h))
