@@ -73,8 +73,8 @@ __device__ __forceinline__ void stv(float* p, const float* in) {
     }
 }
 
-template <int MODE, int DT, int VEC, bool F64 = false>
-__global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : 3) xpass_kernel(XArgs a) {
+template <int MODE, int DT, int VEC, bool F64 = false, int MINB = 3>
+__global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass_kernel(XArgs a) {
     const int pair = blockIdx.y;
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
@@ -581,6 +581,7 @@ static cudaError_t launch_x_mode(const XArgs& a, int npairs, cudaStream_t s) {
     if (vec == 2 && a.F.M % 2) vec = 1;
     void (*k)(XArgs);
     if (a.f64) k = vec == 4 ? xpass_kernel<MODE, DT, 4, true> : (vec == 2 ? xpass_kernel<MODE, DT, 2, true> : xpass_kernel<MODE, DT, 1, true>);
+    else if (a.minb == 4) k = vec == 4 ? xpass_kernel<MODE, DT, 4, false, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2, false, 4> : xpass_kernel<MODE, DT, 1, false, 4>);
     else k = vec == 4 ? xpass_kernel<MODE, DT, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2> : xpass_kernel<MODE, DT, 1>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -596,6 +597,7 @@ static cudaError_t launch_x_dt(const XArgs& a, int npairs, cudaStream_t s) {
 }
 
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s) {
+    if (mode <= X_TAIL && xpass_fast_eligible(a)) return launch_xpass_fast(a, mode, npairs, s);
     if (mode <= X_TAIL && xpass_tma_eligible(a)) return launch_xpass_tma(a, mode, npairs, s);
     switch (mode) {
         case X_FIRST: return launch_x_dt<X_FIRST>(a, npairs, s);

@@ -500,6 +500,8 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag) {
     a.tma_ctas_per_sm = env_int("DREG_TMA_CTAS", 1);
     a.dbg_skip = env_int("DREG_DBG_SKIP", 0);
     a.f64 = env_int("DREG_F64", 0);
+    a.minb = env_int("DREG_XMINB", 3);
+    a.fast_x = env_int("DREG_FAST_X", 1);
     a.fd_lines.init((unsigned)(3 * w.geo.TL));
     return a;
 }

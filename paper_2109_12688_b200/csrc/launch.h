@@ -30,6 +30,8 @@ struct XArgs {
     int tma;            // use the TMA-staged x-pass (xpass_tma.cu) when eligible
     int tma_ctas_per_sm;  // persistent CTAs per SM for the TMA x-pass
     int f64;            // fp64 point-wise arithmetic in the generic x-pass (DREG_F64)
+    int minb;           // x-pass launch-bounds variant: min CTAs per SM (3 or 4)
+    int fast_x;         // use the specialised x-pass (xpass_fast.cu) for M in {64, 128, 256}
     int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
     FastDiv fd_lines;   // divide by 3 * TL
 };
@@ -63,6 +65,8 @@ cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
 bool xpass_tma_eligible(const XArgs& a);
 size_t xpass_tma_smem_bytes(int L, int hx, int TL, int PM, int M);
 cudaError_t launch_xpass_tma(const XArgs& a, int mode, int npairs, cudaStream_t s);
+bool xpass_fast_eligible(const XArgs& a);
+cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s);
 
 // ---- field kernels (field_kernels.cu) ----

@@ -1,0 +1,392 @@
+// Compile-time-specialised fused x-pass for x extents M = 16 R2 (line FFT length
+// L = M/2 = 8 R2, R2 in {4, 8, 16}: M = 64, 128, 256), TL = 32 x-lines per CTA.
+// Same per-voxel semantics as xpass_kernel (admm_kernels.cu; reference
+// admm.cpp:23-63,130-153,155-170 and fft.cpp r2c/c2r along x); the difference is the
+// FFT plumbing:
+//
+//  * one cp.async wave stages all three components' spectrum rows, transposed,
+//    straight into the FFT buffer (no separate staging buffer, no per-component waits);
+//  * the c2r pre-processing (E + iO from X[k], conj X[L-k]) is fused with the first
+//    adjoint stage (radix R2 on contiguous position blocks) in registers;
+//  * the r2c post-processing is fused with the last forward stage: with
+//    L = 8 R2 digit reversal, position block b holds the frequencies k = b (mod 8), so
+//    blocks {j, 8-j} hold every partner pair (k, L-k) and one thread finishes both.
+// Position of frequency k = 8 p1 + b is R2 b + p1 (same scheme as fft_device.cuh).
+#include "fft_device.cuh"
+#include "kernels.cuh"
+#include "launch.h"
+#include "plane_fast.cuh"
+#include "pointwise.cuh"
+
+namespace dregb {
+
+namespace {
+
+constexpr int kFT = 256;  // threads
+constexpr int kFTL = 32;  // x-lines per CTA
+constexpr int kR1 = 8;
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int n = valid ? 8 : 0;  // src-size 0 => zero fill
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void ldvN(const float* p, float* out) {
+    if constexpr (N == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        out[0] = t.x;
+        out[1] = t.y;
+    } else {
+        out[0] = p[0];
+    }
+}
+template <int N>
+__device__ __forceinline__ void stvN(float* p, const float* in) {
+    if constexpr (N == 2) *reinterpret_cast<float2*>(p) = make_float2(in[0], in[1]);
+    else p[0] = in[0];
+}
+
+}  // namespace
+
+template <int MODE, int DT, int R2>
+__global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
+    constexpr int L = kR1 * R2;
+    constexpr int HX = L + 1;
+    constexpr int PM = L + 1;  // odd line pitch (complex)
+    constexpr int M = 2 * L;
+    constexpr int TL = kFTL;
+    constexpr int VEC = 2;
+    const int pair = blockIdx.y;
+    PairState* st = a.F.st + pair;
+    if (!st->active || st->status) return;
+    if (MODE <= X_GENERAL && st->solve_done) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* buf = reinterpret_cast<float2*>(smem);        // [3][TL][PM]
+    float2* twx = buf + 3 * TL * PM;                      // W_L^e
+    float2* xtw = twx + L;                                // W_M^k, k in [0, HX]
+    double* red = reinterpret_cast<double*>(xtw + HX + 1);
+    const int tid = threadIdx.x;
+    const long long lines = a.F.lines;
+    const long long L0 = (long long)blockIdx.x * TL;
+    const int nl = (int)min((long long)TL, lines - L0);
+    const long long N = a.F.N;
+
+    float* V = a.F.V + (size_t)pair * 3 * N;
+    float* BH = a.F.BH + (size_t)pair * 3 * N;
+    float* WP = a.F.WP + (size_t)pair * 3 * N;
+    float* BP = a.F.BP + (size_t)pair * 3 * N;
+    const float* G = a.F.G + (size_t)pair * 3 * N;
+    const float* Dd = a.F.D + (size_t)pair * N;
+    float2* S = a.F.S + (size_t)pair * 3 * HX * lines;
+
+    // ---- stage all three spectra (transposed) + tables ----
+    if (MODE != X_FIRST) {
+        for (int i = tid; i < 3 * HX * TL; i += kFT) {
+            const int l = i & (TL - 1);
+            const int cp = i >> 5;  // c * HX + p
+            const int c = cp / HX, p = cp - c * HX;
+            const bool ok = l < nl;
+            cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
+        }
+    }
+    for (int i = tid; i < L; i += kFT) twx[i] = a.twx[i];
+    for (int i = tid; i <= HX; i += kFT) xtw[i] = a.xtw[i];
+    if (MODE != X_FIRST) cp_async_wait_all();
+    __syncthreads();
+
+    // ---- phase 1: c2r -> w_{k-1} in natural order ----
+    if (MODE != X_FIRST) {
+        // (a) pre-process + adjoint of the last DIF stage, whole lines per round
+        constexpr int TASKS = 3 * TL * (kR1 / 2);  // (line, block pair j)
+#pragma unroll 1
+        for (int r0 = 0; r0 < TASKS; r0 += kFT) {
+            const int t = r0 + tid;
+            const bool act = t < TASKS;
+            const int line = t >> 2, j = t & 3;  // line = c * TL + l
+            const float2* X = buf + line * PM;
+            float2 z[2][R2];
+            if (act) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
+#pragma unroll
+                    for (int p1 = 0; p1 < R2; ++p1) {
+                        const int k = kR1 * p1 + b;
+                        float2 A = X[k];
+                        float2 B = X[L - k];
+                        if (k == 0) {
+                            A.y = 0.f;
+                            B.y = 0.f;
+                        }
+                        B.y = -B.y;
+                        const float2 e = cadd(A, B);
+                        const float2 o = cmulc(csub(A, B), xtw[k]);
+                        z[q][p1] = make_float2(e.x - o.y, e.y + o.x);
+                    }
+                    rdft<true, R2>(z[q]);
+                }
+            }
+            __syncthreads();  // every read of these lines done before any write
+            if (act) {
+                float2* Y = buf + line * PM;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
+#pragma unroll
+                    for (int e = 0; e < R2; ++e) Y[R2 * b + e] = z[q][e];
+                }
+            }
+        }
+        __syncthreads();
+        // (b) adjoint of the first DIF stage: conj twiddle, inverse radix 8 over stride R2
+        for (int t = tid; t < 3 * TL * R2; t += kFT) {
+            const int line = t / R2, j1 = t - line * R2;
+            float2* Y = buf + line * PM;
+            float2 x[kR1];
+#pragma unroll
+            for (int k = 0; k < kR1; ++k) x[k] = Y[j1 + R2 * k];
+#pragma unroll
+            for (int k = 1; k < kR1; ++k) x[k] = cmulc(x[k], twx[j1 * k]);
+            dft8<true>(x);
+#pragma unroll
+            for (int s = 0; s < kR1; ++s) Y[j1 + R2 * s] = x[s];
+        }
+        __syncthreads();
+    }
+
+    // ---- phase 2: point-wise ADMM updates (fp32) ----
+    const float thf = (float)a.sp.theta, ithf = (float)(1.0 / a.sp.theta), epsf = (float)a.sp.epsilon;
+    const float cf = (float)a.coef;
+    const bool accel = a.sp.accelerate != 0;
+    const size_t base = (size_t)L0 * M;
+    const int nvox = nl * M;
+    float fc = 0.f, fr = 0.f, fo = 0.f;
+#pragma unroll 2
+    for (int i0 = tid * VEC; i0 < nvox; i0 += kFT * VEC) {
+        const int l = i0 / M, x0 = i0 - l * M;
+        const size_t gi = base + i0;
+        float w[3][VEC], vp[3][VEC], bo[3][VEC], wp[3][VEC], bp[3][VEC], g[3][VEC], dv[VEC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (MODE != X_FIRST) ldvN<VEC>(V + (size_t)c * N + gi, vp[c]);
+            if (MODE == X_GENERAL) ldvN<VEC>(BH + (size_t)c * N + gi, bo[c]);
+            if (MODE == X_GENERAL && accel) {
+                ldvN<VEC>(WP + (size_t)c * N + gi, wp[c]);
+                ldvN<VEC>(BP + (size_t)c * N + gi, bp[c]);
+            }
+            if (MODE != X_TAIL) ldvN<VEC>(G + (size_t)c * N + gi, g[c]);
+        }
+        if (MODE != X_TAIL) ldvN<VEC>(Dd + gi, dv);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float* wl = reinterpret_cast<const float*>(buf + (c * TL + l) * PM);
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) {
+                w[c][jj] = MODE == X_FIRST ? 0.f : wl[x0 + jj];
+                if (MODE == X_FIRST) vp[c][jj] = 0.f;
+                if (MODE != X_GENERAL) bo[c][jj] = 0.f;
+            }
+        }
+        if (MODE == X_TAIL) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int jj = 0; jj < VEC; ++jj) {
+                    const float dd = vp[c][jj] - w[c][jj];
+                    fr = fmaf(dd, dd, fr);
+                }
+            continue;
+        }
+        float wh[3][VEC], bh[3][VEC], vn[3][VEC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) {
+                if (MODE == X_FIRST) {
+                    wh[c][jj] = 0.f;
+                    bh[c][jj] = 0.f;
+                    continue;
+                }
+                const float dd = vp[c][jj] - w[c][jj];
+                fr = fmaf(dd, dd, fr);
+                const float b = bo[c][jj] + dd;  // dual update (admm.cpp:142-153)
+                if (MODE == X_GENERAL && accel) {
+                    wh[c][jj] = fmaf(cf, w[c][jj] - wp[c][jj], w[c][jj]);  // admm.cpp:130-139
+                    bh[c][jj] = fmaf(cf, b - bp[c][jj], b);
+                } else {
+                    wh[c][jj] = w[c][jj];
+                    bh[c][jj] = b;
+                }
+                bo[c][jj] = b;
+            }
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj) {
+            const float whj[3] = {wh[0][jj], wh[1][jj], wh[2][jj]};
+            const float bhj[3] = {bh[0][jj], bh[1][jj], bh[2][jj]};
+            const float gj[3] = {g[0][jj], g[1][jj], g[2][jj]};
+            float vj[3];
+            v_update_voxel_f32<DT>(whj, bhj, gj, dv[jj], thf, ithf, epsf, vj);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                vn[c][jj] = vj[c];
+                fc += fabsf(vj[c] - vp[c][jj]);
+            }
+            if (a.sp.log_objective) {
+                const float rho = fmaf(gj[0], vj[0], fmaf(gj[1], vj[1], gj[2] * vj[2])) + dv[jj];
+                fo += DT == 1 ? fabsf(rho) : 0.5f * rho * rho;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (MODE != X_FIRST && accel) {
+                stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
+                stvN<VEC>(BP + (size_t)c * N + gi, bo[c]);
+            }
+            stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
+            if (MODE != X_FIRST) stvN<VEC>(BH + (size_t)c * N + gi, bh[c]);
+            float* ul = reinterpret_cast<float*>(buf + (c * TL + l) * PM);
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) ul[x0 + jj] = vn[c][jj] + bh[c][jj];
+        }
+    }
+
+    // ---- phase 3: r2c along x ----
+    if (MODE != X_TAIL) {
+        if (nl < TL) {
+            for (int idx = tid; idx < 3 * TL * PM; idx += kFT) {
+                const int l = (idx / PM) & (TL - 1);
+                if (l >= nl) buf[idx] = make_float2(0.f, 0.f);
+            }
+        }
+        __syncthreads();
+        // (a) first DIF stage: radix 8 over stride R2, twiddle W_L^{j1 k}
+        for (int t = tid; t < 3 * TL * R2; t += kFT) {
+            const int line = t / R2, j1 = t - line * R2;
+            float2* Y = buf + line * PM;
+            float2 x[kR1];
+#pragma unroll
+            for (int s = 0; s < kR1; ++s) x[s] = Y[j1 + R2 * s];
+            dft8<false>(x);
+#pragma unroll
+            for (int k = 1; k < kR1; ++k) x[k] = cmul(x[k], twx[j1 * k]);
+#pragma unroll
+            for (int k = 0; k < kR1; ++k) Y[j1 + R2 * k] = x[k];
+        }
+        __syncthreads();
+        // (b) last DIF stage on block pairs {j, 8-j} + r2c post-processing -> global
+        constexpr int TASKS = 3 * (kR1 / 2) * TL;  // (c, j) outer, line fastest (coalesced stores)
+        for (int t = tid; t < TASKS; t += kFT) {
+            const int l = t & (TL - 1);
+            const int cj = t >> 5;
+            const int c = cj >> 2, j = cj & 3;
+            if (l >= nl) continue;
+            const float2* Y = buf + (c * TL + l) * PM;
+            const int b0 = j, b1 = j == 0 ? kR1 / 2 : kR1 - j;
+            float2 z0[R2], z1[R2];
+#pragma unroll
+            for (int e = 0; e < R2; ++e) {
+                z0[e] = Y[R2 * b0 + e];
+                z1[e] = Y[R2 * b1 + e];
+            }
+            rdft<false, R2>(z0);
+            rdft<false, R2>(z1);
+            float2* Sc = S + (size_t)c * HX * lines + L0 + l;
+            auto emit = [&](int k, float2 zk, float2 zpartner) {
+                const float2 zc = cconj(zpartner);
+                const float2 ee = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
+                const float2 oo = make_float2(0.5f * (zk.y - zc.y), -0.5f * (zk.x - zc.x));
+                Sc[(size_t)k * lines] = cadd(ee, cmul(xtw[k], oo));
+            };
+#pragma unroll
+            for (int p1 = 0; p1 < R2; ++p1) {
+                if (j == 0) {
+                    // block 0: partner of k = 8 p1 is L - k = 8 (R2 - p1) in block 0
+                    emit(kR1 * p1, z0[p1], z0[(R2 - p1) & (R2 - 1)]);
+                    // block 4 is self-paired: partner index R2 - 1 - p1
+                    emit(kR1 * p1 + kR1 / 2, z1[p1], z1[R2 - 1 - p1]);
+                } else {
+                    emit(kR1 * p1 + b0, z0[p1], z1[R2 - 1 - p1]);
+                    emit(kR1 * p1 + b1, z1[p1], z0[R2 - 1 - p1]);
+                }
+            }
+            if (j == 0) emit(L, z0[0], z0[0]);  // Nyquist bin k = L (Z[L] = Z[0])
+        }
+    }
+
+    const double vals[3] = {block_sum<kFT>((double)fc, red), block_sum<kFT>((double)fr, red),
+                            block_sum<kFT>((double)fo, red)};
+    double tot[3];
+    if (reduce_partials<kFT, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
+        tid == 0) {
+        double* dg = a.F.diag ? a.F.diag + (size_t)pair * a.F.diag_stride * 3 : nullptr;
+        if (MODE == X_TAIL) {
+            const int it = st->iterations;
+            if (dg && it >= 1) dg[(it - 1) * 3 + 1] = sqrt(tot[1]);
+        } else {
+            const double change = tot[0] / (3.0 * (double)N);
+            if (dg) {
+                dg[a.k * 3 + 0] = change;
+                if (a.k >= 1) dg[(a.k - 1) * 3 + 1] = sqrt(tot[1]);
+                dg[a.k * 3 + 2] = tot[2];
+            }
+            st->iterations = a.k + 1;
+            st->final_change = change;
+            if (change <= a.sp.tol) {
+                st->solve_done = 1;
+                st->done_iter = a.k;
+            }
+        }
+    }
+}
+
+template <int R2>
+static size_t fast_smem() {
+    constexpr int L = kR1 * R2;
+    return sizeof(float2) * (3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 32;
+}
+
+bool xpass_fast_eligible(const XArgs& a) {
+    if (!a.fast_x || a.odd || a.f64) return false;
+    const int M = a.F.M;
+    return M == 64 || M == 128 || M == 256;
+}
+
+template <int MODE, int DT, int R2>
+static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
+    const dim3 grid((unsigned)((a.F.lines + kFTL - 1) / kFTL), (unsigned)npairs);
+    const size_t smem = fast_smem<R2>();
+    void (*k)(XArgs) = xpass_fast_kernel<MODE, DT, R2>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kFT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int MODE, int DT>
+static cudaError_t launch_fast_r(const XArgs& a, int npairs, cudaStream_t s) {
+    switch (a.F.M) {
+        case 64: return launch_fast_x<MODE, DT, 4>(a, npairs, s);
+        case 128: return launch_fast_x<MODE, DT, 8>(a, npairs, s);
+        default: return launch_fast_x<MODE, DT, 16>(a, npairs, s);
+    }
+}
+
+cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t s) {
+    const bool l1 = a.sp.data_term == 1;
+    switch (mode) {
+        case X_FIRST: return l1 ? launch_fast_r<X_FIRST, 1>(a, npairs, s) : launch_fast_r<X_FIRST, 2>(a, npairs, s);
+        case X_SECOND: return l1 ? launch_fast_r<X_SECOND, 1>(a, npairs, s) : launch_fast_r<X_SECOND, 2>(a, npairs, s);
+        case X_GENERAL: return l1 ? launch_fast_r<X_GENERAL, 1>(a, npairs, s) : launch_fast_r<X_GENERAL, 2>(a, npairs, s);
+        default: return l1 ? launch_fast_r<X_TAIL, 1>(a, npairs, s) : launch_fast_r<X_TAIL, 2>(a, npairs, s);
+    }
+}
+
+}  // namespace dregb
