@@ -32,6 +32,7 @@ struct XArgs {
     int f64;            // fp64 point-wise arithmetic in the generic x-pass (DREG_F64)
     int minb;           // x-pass launch-bounds variant: min CTAs per SM (3 or 4)
     int fast_x;         // use the specialised x-pass (xpass_fast.cu) for M in {64, 128, 256}
+    int fx_variant;     // point-wise loop variant of the specialised x-pass: 10 * VEC + unroll (22 default)
     int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
     FastDiv fd_lines;   // divide by 3 * TL
 };

@@ -37,7 +37,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 template <int N>
 __device__ __forceinline__ void ldvN(const float* p, float* out) {
-    if constexpr (N == 2) {
+    if constexpr (N == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        out[0] = t.x;
+        out[1] = t.y;
+        out[2] = t.z;
+        out[3] = t.w;
+    } else if constexpr (N == 2) {
         const float2 t = *reinterpret_cast<const float2*>(p);
         out[0] = t.x;
         out[1] = t.y;
@@ -47,20 +53,20 @@ __device__ __forceinline__ void ldvN(const float* p, float* out) {
 }
 template <int N>
 __device__ __forceinline__ void stvN(float* p, const float* in) {
-    if constexpr (N == 2) *reinterpret_cast<float2*>(p) = make_float2(in[0], in[1]);
+    if constexpr (N == 4) *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+    else if constexpr (N == 2) *reinterpret_cast<float2*>(p) = make_float2(in[0], in[1]);
     else p[0] = in[0];
 }
 
 }  // namespace
 
-template <int MODE, int DT, int R2>
+template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2>
 __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
     constexpr int L = kR1 * R2;
     constexpr int HX = L + 1;
     constexpr int PM = L + 1;  // odd line pitch (complex)
     constexpr int M = 2 * L;
     constexpr int TL = kFTL;
-    constexpr int VEC = 2;
     const int pair = blockIdx.y;
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
     float fc = 0.f, fr = 0.f, fo = 0.f;
-#pragma unroll 2
+#pragma unroll UNR
     for (int i0 = tid * VEC; i0 < nvox; i0 += kFT * VEC) {
         const int l = i0 / M, x0 = i0 - l * M;
         const size_t gi = base + i0;
@@ -362,6 +368,14 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     const dim3 grid((unsigned)((a.F.lines + kFTL - 1) / kFTL), (unsigned)npairs);
     const size_t smem = fast_smem<R2>();
     void (*k)(XArgs) = xpass_fast_kernel<MODE, DT, R2>;
+    switch (a.fx_variant) {
+        case 41: k = xpass_fast_kernel<MODE, DT, R2, 4, 1>; break;
+        case 21: k = xpass_fast_kernel<MODE, DT, R2, 2, 1>; break;
+        case 24: k = xpass_fast_kernel<MODE, DT, R2, 2, 4>; break;
+        case 11: k = xpass_fast_kernel<MODE, DT, R2, 1, 1>; break;
+        case 14: k = xpass_fast_kernel<MODE, DT, R2, 1, 4>; break;
+        default: break;
+    }
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
