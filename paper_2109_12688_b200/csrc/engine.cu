@@ -261,6 +261,8 @@ struct Workspace {
     }
 
     void alloc(dreg_dims3 d, int pairs) {
+        static unsigned long long next_id = 1;
+        id = next_id++;
         geo.build(d);
         P = pairs;
         const size_t N = (size_t)geo.N;
@@ -305,6 +307,9 @@ struct Workspace {
         }
     }
 
+    PairState* st_shared = nullptr;  // set on coarser pyramid levels: state lives in the finest workspace
+    unsigned long long id = 0;       // allocation generation (graph cache key)
+
     Fields fields(bool with_diag) const {
         Fields F{};
         F.M = geo.M;
@@ -320,7 +325,7 @@ struct Workspace {
         F.G = G.p;
         F.D = D.p;
         F.S = S.p;
-        F.st = st.p;
+        F.st = st_shared ? st_shared : st.p;
         F.part = part.p;
         F.diag = with_diag ? diag.p : nullptr;
         F.diag_stride = diag_iters;
@@ -359,7 +364,8 @@ struct dreg_cuda_ctx {
     int64_t launches = 0;
     int chunk = 0;
     int use_graphs = 1;
-    std::unique_ptr<Workspace> ws;
+    std::map<std::tuple<int, int, int>, std::unique_ptr<Workspace>> wss;  // one per grid size
+    Workspace* last = nullptr;
     // pinned host staging for pointer tables and pair states
     const float** h_tgt = nullptr;
     const float** h_src = nullptr;
@@ -390,15 +396,32 @@ struct dreg_cuda_ctx {
         h_cap = 0;
     }
 
-    Workspace& workspace(dreg_dims3 d, int pairs) {
-        if (!ws || !same_dims(ws->geo, d) || ws->P < pairs) {
-            ws.reset();
+    // Workspace for grid d with capacity >= pairs; keeps at most 6 grids, never
+    // evicting the ones listed in `keep` (the levels of the call in progress).
+    Workspace& workspace(dreg_dims3 d, int pairs, const std::vector<dreg_dims3>& keep = {}) {
+        const auto key = std::make_tuple(d.x, d.y, d.z);
+        auto it = wss.find(key);
+        if (it == wss.end() || it->second->P < pairs) {
             CK(cudaStreamSynchronize(stream));
+            if (it != wss.end()) wss.erase(it);
+            while (wss.size() >= 6) {
+                auto victim = wss.end();
+                for (auto jt = wss.begin(); jt != wss.end(); ++jt) {
+                    bool kept = false;
+                    for (const auto& k : keep)
+                        kept |= std::make_tuple(k.x, k.y, k.z) == jt->first;
+                    if (!kept && jt->second.get() != last) victim = jt;
+                }
+                if (victim == wss.end()) break;
+                wss.erase(victim);
+            }
             auto w = std::make_unique<Workspace>();
             w->alloc(d, pairs);
-            ws = std::move(w);
+            it = wss.emplace(key, std::move(w)).first;
         }
-        return *ws;
+        last = it->second.get();
+        last->st_shared = nullptr;
+        return *last;
     }
 };
 
@@ -589,13 +612,13 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     }
 }
 
-// register_pair for levels == 1 (registration.cpp:180-283), all pairs of the chunk.
-void enqueue_registration(Launcher& L, Workspace& w, int P, const dreg_reg_cfg& cfg, cudaStream_t st) {
+// register_pair (registration.cpp:180-283) for all pairs of the chunk; lv holds the
+// level workspaces coarsest first, the finest (original grid) last.  Per-pair state
+// lives in the finest workspace and is shared by every level.
+void smooth_or_copy(Launcher& L, const Workspace& w, int P, bool smooth, cudaStream_t st) {
     const VolGeom g = w.vg();
     const RegBuffers R = w.regbufs();
-    const Fields F = w.fields(false);
-    L(launch_prep_normalize(g, R, F, P, st), 3);
-    if (cfg.smooth_levels) {
+    if (smooth) {  // binomial_smooth = x, y, z passes (registration.cpp:141-143)
         L(launch_smooth_axis(g, R.tmpA, R.I0, 0, P, st));
         L(launch_smooth_axis(g, R.I0, R.tmpA, 1, P, st));
         L(launch_smooth_axis(g, R.tmpA, R.I0, 2, P, st));
@@ -606,42 +629,69 @@ void enqueue_registration(Launcher& L, Workspace& w, int P, const dreg_reg_cfg& 
         CK(cudaMemcpyAsync(R.I0, R.tmpA, sizeof(float) * g.N * P, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(R.I1, R.tmpB, sizeof(float) * g.N * P, cudaMemcpyDeviceToDevice, st));
     }
-    L(launch_level_init(g, R, F, 0, P, st));
-    dreg_solver_cfg s = cfg.solver;
-    s.max_iters = cfg.max_admm_iters_per_level[0];
-    const int K = cfg.max_warps_per_level[0];
-    for (int wi = 0; wi < K; ++wi) {
-        enqueue_solve(L, w, P, s, false, false, true, st);
-        L(launch_compose_decide(g, R, F, cfg.warp_improvement_threshold, K, P, st));
+}
+
+void enqueue_registration(Launcher& L, const std::vector<Workspace*>& lv, int P, const dreg_reg_cfg& cfg,
+                          cudaStream_t st) {
+    const int Lv = (int)lv.size();
+    Workspace& fine = *lv.back();
+    for (Workspace* w : lv) w->st_shared = (w == &fine) ? nullptr : fine.st.p;
+    const RegBuffers Rf = fine.regbufs();
+    const Fields Ff = fine.fields(false);
+    // normalise with one shared range (registration.cpp:205), pyramid (:208-214), smoothing (:216-221)
+    L(launch_prep_normalize(fine.vg(), Rf, Ff, P, st), 3);
+    for (int l = Lv - 1; l > 0; --l) {
+        const RegBuffers a = lv[l]->regbufs(), b = lv[l - 1]->regbufs();
+        L(launch_pyr_down(lv[l]->vg(), lv[l - 1]->vg(), a.tmpA, a.tmpB, b.tmpA, b.tmpB, P, st));
     }
-    L(launch_finalize(g, R, F, P, st));
+    for (int l = 0; l < Lv; ++l) smooth_or_copy(L, *lv[l], P, cfg.smooth_levels != 0, st);
+    dreg_solver_cfg s = cfg.solver;
+    for (int l = 0; l < Lv; ++l) {
+        Workspace& w = *lv[l];
+        const VolGeom g = w.vg();
+        const RegBuffers R = w.regbufs();
+        const Fields F = w.fields(false);
+        if (l == 0) L(launch_level_init(g, R, F, 0, P, st));
+        else L(launch_level_up(lv[l - 1]->vg(), g, lv[l - 1]->regbufs(), R, F, l, P, st));
+        s.max_iters = cfg.max_admm_iters_per_level[l];
+        const int K = cfg.max_warps_per_level[l];
+        for (int wi = 0; wi < K; ++wi) {
+            enqueue_solve(L, w, P, s, false, false, true, st);
+            L(launch_compose_decide(g, R, F, cfg.warp_improvement_threshold, K, P, st));
+        }
+    }
+    L(launch_finalize(fine.vg(), Rf, Ff, P, st));
 }
 
-std::string graph_key(int P, const dreg_reg_cfg& c) {
+std::string graph_key(int P, const dreg_reg_cfg& c, const std::vector<Workspace*>& lv) {
     char buf[512];
-    std::snprintf(buf, sizeof buf, "%d|%d|%d|%.17g|%.17g|%.17g|%d|%.17g|%d|%d|%d|%d|%.17g|%d", P,
-                  c.solver.data_term, c.solver.order, c.solver.lambda, c.solver.theta, c.solver.epsilon,
-                  c.solver.max_iters, c.solver.tol, c.solver.accelerate, c.levels, c.max_warps_per_level[0],
-                  c.max_admm_iters_per_level[0], c.warp_improvement_threshold, c.smooth_levels);
-    return buf;
+    std::snprintf(buf, sizeof buf, "%d|%d|%d|%.17g|%.17g|%.17g|%.17g|%d|%.17g|%d|%d", P, c.solver.data_term,
+                  c.solver.order, c.solver.lambda, c.solver.theta, c.solver.epsilon, c.solver.tol, c.solver.accelerate,
+                  c.warp_improvement_threshold, c.smooth_levels, c.levels);
+    std::string k = buf;
+    for (int l = 0; l < c.levels; ++l)
+        k += "|" + std::to_string(c.max_warps_per_level[l]) + "x" + std::to_string(c.max_admm_iters_per_level[l]) +
+             "@" + std::to_string(lv[l]->id);
+    return k;
 }
 
-void run_registration(dreg_cuda_ctx* c, Workspace& w, int P, const dreg_reg_cfg& cfg) {
+void run_registration(dreg_cuda_ctx* c, const std::vector<Workspace*>& lv, int P, const dreg_reg_cfg& cfg) {
     cudaStream_t st = c->stream;
+    Workspace& w = *lv.back();
     if (!c->use_graphs) {
         Launcher L{c};
-        enqueue_registration(L, w, P, cfg, st);
+        enqueue_registration(L, lv, P, cfg, st);
         c->launches += L.count;
         return;
     }
-    const std::string key = graph_key(P, cfg);
+    const std::string key = graph_key(P, cfg, lv);
     auto it = w.graphs.find(key);
     if (it == w.graphs.end()) {
         Launcher L{c};
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue_registration(L, w, P, cfg, st);
+            enqueue_registration(L, lv, P, cfg, st);
         } catch (...) {
             cudaStreamEndCapture(st, &graph);
             if (graph) cudaGraphDestroy(graph);
@@ -674,11 +724,10 @@ void validate_reg(const dreg_reg_cfg* cfg, dreg_dims3 d) {
         if (cfg->max_warps_per_level[l] < 0) throw ArgFail("register_pair: negative warp cap");
         if (cfg->max_warps_per_level[l] > DREG_MAX_WARPS) throw ArgFail("register_pair: warp cap above 64");
     }
-    if (cfg->levels != 1)
-        throw ArgFail("register_pair: levels > 1 (pyramid) is not implemented on the B200 path yet");
 }
 
-void fill_results(const PairState* hs, int P, const Workspace& w, dreg_pair_result* out, double elapsed) {
+void fill_results(const PairState* hs, int P, const std::vector<dreg_dims3>& dl, dreg_pair_result* out,
+                  double elapsed) {
     for (int p = 0; p < P; ++p) {
         dreg_pair_result& r = out[p];
         std::memset(&r, 0, sizeof r);
@@ -686,12 +735,14 @@ void fill_results(const PairState* hs, int P, const Workspace& w, dreg_pair_resu
         r.status = s.status;
         r.velocity_count = s.velocity_count;
         r.solves = s.solves;
-        r.levels = 1;
-        dreg_level_log& lg = r.per_level[0];
-        lg.dims = {w.geo.M, w.geo.Ny, w.geo.Nz};
-        lg.warps = s.level_warps[0];
-        for (int i = 0; i <= lg.warps && i <= DREG_MAX_WARPS; ++i) lg.mean_sad[i] = s.mean_sad[0][i];
-        for (int i = 0; i < lg.warps && i < DREG_MAX_WARPS; ++i) lg.solver_iterations[i] = s.solver_iterations[0][i];
+        r.levels = (int)dl.size();
+        for (int l = 0; l < r.levels; ++l) {
+            dreg_level_log& lg = r.per_level[l];
+            lg.dims = dl[l];
+            lg.warps = s.level_warps[l];
+            for (int i = 0; i <= lg.warps && i <= DREG_MAX_WARPS; ++i) lg.mean_sad[i] = s.mean_sad[l][i];
+            for (int i = 0; i < lg.warps && i < DREG_MAX_WARPS; ++i) lg.solver_iterations[i] = s.solver_iterations[l][i];
+        }
         r.elapsed_seconds = elapsed;
     }
 }
@@ -709,7 +760,10 @@ int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs) {
     CK(cudaMemGetInfo(&free_b, &total_b));
     const size_t per = Workspace::bytes_per_pair(tmp);
     size_t fit = (size_t)(0.6 * (double)free_b) / std::max<size_t>(per, 1);
-    if (c->ws && same_dims(c->ws->geo, d)) fit = std::max<size_t>(fit, (size_t)c->ws->P);
+    {
+        auto it = c->wss.find(std::make_tuple(d.x, d.y, d.z));
+        if (it != c->wss.end()) fit = std::max<size_t>(fit, (size_t)it->second->P);
+    }
     int P = (int)std::min<size_t>(fit, 32);
     return std::max(1, std::min(P, n_pairs));
 }
@@ -817,7 +871,8 @@ void dreg_cuda_ctx_destroy(dreg_cuda_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    c->ws.reset();
+    c->wss.clear();
+    c->last = nullptr;
     c->free_host();
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
@@ -855,7 +910,15 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     if (n_pairs == 0) return DREG_OK;
     const bool host = tgt_host != nullptr;
     const int chunk = pick_chunk(c, d, n_pairs);
-    Workspace& w = c->workspace(d, chunk);
+    // level grids, coarsest first (registration.cpp:208-214: dims halved, rounded up)
+    std::vector<dreg_dims3> dl((size_t)cfg->levels);
+    dl.back() = d;
+    for (int l = cfg->levels - 1; l > 0; --l)
+        dl[l - 1] = {(dl[l].x + 1) / 2, (dl[l].y + 1) / 2, (dl[l].z + 1) / 2};
+    std::vector<Workspace*> lv((size_t)cfg->levels);
+    for (int l = 0; l < cfg->levels; ++l) lv[l] = &c->workspace(dl[l], chunk, dl);
+    Workspace& w = c->workspace(d, chunk, dl);
+    lv.back() = &w;
     c->ensure_host(w.P);
     const size_t N = (size_t)w.geo.N;
     cudaStream_t st = c->stream;
@@ -885,7 +948,7 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
         CK(cudaMemcpyAsync(w.src_tab.p, c->h_src, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(w.phi_tab.p, c->h_phi, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(w.warped_tab.p, c->h_warped, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
-        run_registration(c, w, P, *cfg);
+        run_registration(c, lv, P, *cfg);
         if (host) {
             for (int p = 0; p < P; ++p) {
                 const int q = p0 + p;
@@ -907,7 +970,7 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     for (int q = 0; q < n_pairs; ++q) {
         if (states[q].status != DREG_OK && first_bad == DREG_OK) first_bad = states[q].status;
     }
-    if (results) fill_results(states.data(), n_pairs, w, results, el);
+    if (results) fill_results(states.data(), n_pairs, dl, results, el);
     if (first_bad != DREG_OK) {
         c->err = "register_pair: non-finite values (input volumes, velocity or deformation)";
         return first_bad;
@@ -997,9 +1060,9 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
 // ---- measurement ----------------------------------------------------------------
 int dreg_cuda_time_kernels(dreg_cuda_ctx* c, int reps, double* out) {
     return guarded(c, [&] {
-        if (!c->ws) throw ArgFail("time_kernels: no workspace yet (run a registration first)");
+        if (!c->last) throw ArgFail("time_kernels: no workspace yet (run a registration first)");
         if (reps < 1 || !out) throw ArgFail("time_kernels: reps >= 1 and out required");
-        Workspace& w = *c->ws;
+        Workspace& w = *c->last;
         const int P = w.P;
         cudaStream_t st = c->stream;
         dreg_solver_cfg s;

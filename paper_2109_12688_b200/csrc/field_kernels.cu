@@ -552,11 +552,95 @@ cudaError_t launch_downsample(VolGeom src, VolGeom dst, const float* in, float* 
     return cudaGetLastError();
 }
 
-// registration.cpp:114-135: corner-aligned trilinear resample, x2 on every component
 __device__ __forceinline__ double source_coord(int i, int te, int se) {
     if (te <= 1) return 0.0;
     return (double)i * (double)(se - 1) / (double)(te - 1);
 }
+
+// Pyramid construction for a chunk of pairs: level l-1 = downsample(level l) for the
+// normalised target and source (registration.cpp:208-214), [P][N] buffers.
+__global__ void __launch_bounds__(kVT) pyr_down_kernel(VolGeom gs, VolGeom gd, const float* ta, const float* sa,
+                                                       float* tb, float* sb) {
+    const int pair = blockIdx.y;
+    const float* in0 = ta + (size_t)pair * gs.N;
+    const float* in1 = sa + (size_t)pair * gs.N;
+    float* o0 = tb + (size_t)pair * gd.N;
+    float* o1 = sb + (size_t)pair * gd.N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, gd.M, gd.Ny, x, y, z);
+        double s0 = 0.0, s1 = 0.0;
+        for (int dz = 0; dz < 2; ++dz)
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    const size_t j = min(2 * x + dx, gs.M - 1) +
+                                     (size_t)gs.M * (min(2 * y + dy, gs.Ny - 1) + (size_t)gs.Ny * min(2 * z + dz, gs.Nz - 1));
+                    s0 += in0[j];
+                    s1 += in1[j];
+                }
+        o0[i] = (float)(s0 / 8.0);
+        o1[i] = (float)(s1 / 8.0);
+    }
+}
+
+cudaError_t launch_pyr_down(VolGeom src, VolGeom dst, const float* ta, const float* sa, float* tb, float* sb,
+                            int npairs, cudaStream_t s) {
+    pyr_down_kernel<<<dim3(voxel_blocks(dst.N), npairs), kVT, 0, s>>>(src, dst, ta, sa, tb, sb);
+    return cudaGetLastError();
+}
+
+// Level transition (registration.cpp:232-247): phi = upsample_deformation(phi_coarse)
+// (corner-aligned trilinear, x2, stored fp32; :114-139), warped = warp(level source,
+// phi), sad_prev = mean_sad(warped, level target); per-level state reset.
+__global__ void __launch_bounds__(kVT) level_up_kernel(VolGeom gs, VolGeom gd, RegBuffers Rs, RegBuffers Rd, Fields F,
+                                                       int level) {
+    __shared__ double red[32];
+    const int pair = blockIdx.y;
+    PairState* st = F.st + pair;
+    if (st->status) return;
+    const float* phis = Rs.PHI[st->cur] + (size_t)pair * 3 * gs.N;
+    float* phid = Rd.PHI[0] + (size_t)pair * 3 * gd.N;
+    float* W = Rd.WARPED[0] + (size_t)pair * gd.N;
+    const float* I1 = Rd.I1 + (size_t)pair * gd.N;
+    const float* I0 = Rd.I0 + (size_t)pair * gd.N;
+    double sad = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.N;
+         i += (long long)gridDim.x * blockDim.x) {
+        int x, y, z;
+        unflat(i, gd.M, gd.Ny, x, y, z);
+        const double px = source_coord(x, gd.M, gs.M), py = source_coord(y, gd.Ny, gs.Ny),
+                     pz = source_coord(z, gd.Nz, gs.Nz);
+        double u[3];
+        trilinear3(phis, (size_t)gs.N, gs.M, gs.Ny, gs.Nz, px, py, pz, u);
+        const float u0 = (float)(2.0 * u[0]), u1 = (float)(2.0 * u[1]), u2 = (float)(2.0 * u[2]);
+        phid[i] = u0;
+        phid[gd.N + i] = u1;
+        phid[2 * gd.N + i] = u2;
+        const float w = (float)trilinear(I1, gd.M, gd.Ny, gd.Nz, x + (double)u0, y + (double)u1, z + (double)u2);
+        W[i] = w;
+        sad += fabs((double)w - (double)I0[i]);
+    }
+    const double vals[1] = {block_sum<kVT>(sad, red)};
+    double tot[1];
+    if (reduce_partials<kVT, 1>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
+        threadIdx.x == 0) {
+        st->sad_prev = tot[0] / (double)gd.N;
+        st->mean_sad[level][0] = st->sad_prev;
+        st->cur = 0;
+        st->warps = 0;
+        st->level = level;
+        st->active = 1;
+    }
+}
+
+cudaError_t launch_level_up(VolGeom src, VolGeom dst, const RegBuffers& Rs, const RegBuffers& Rd, Fields F, int level,
+                            int npairs, cudaStream_t s) {
+    level_up_kernel<<<dim3(voxel_blocks(dst.N), npairs), kVT, 0, s>>>(src, dst, Rs, Rd, F, level);
+    return cudaGetLastError();
+}
+
+// registration.cpp:114-135: corner-aligned trilinear resample, x2 on every component
 
 __global__ void upsample_kernel(VolGeom gs, VolGeom gd, const float* in, float* out, int ncomp) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < gd.N;

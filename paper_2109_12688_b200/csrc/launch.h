@@ -109,6 +109,11 @@ cudaError_t launch_sad(VolGeom g, const float* a, const float* b, double* part, 
 cudaError_t launch_minmax_normalize(VolGeom g, const float* a, const float* b, float* oa, float* ob,
                                     float* part, unsigned int* counter, cudaStream_t s);
 cudaError_t launch_downsample(VolGeom src, VolGeom dst, const float* in, float* out, cudaStream_t s);
+// pyramid (registration.cpp:208-247): batched downsample of target+source, level transition
+cudaError_t launch_pyr_down(VolGeom src, VolGeom dst, const float* ta, const float* sa, float* tb, float* sb,
+                            int npairs, cudaStream_t s);
+cudaError_t launch_level_up(VolGeom src, VolGeom dst, const RegBuffers& Rs, const RegBuffers& Rd, Fields F, int level,
+                            int npairs, cudaStream_t s);
 cudaError_t launch_upsample(VolGeom src, VolGeom dst, const float* in, float* out, int ncomp,
                             cudaStream_t s);
 cudaError_t launch_aos_to_soa(long long N, const float* aos, float* soa, cudaStream_t s);

@@ -132,11 +132,12 @@ def test_register_pair_levels1(lib, gold):
 
 
 def test_register_pair_two_levels(lib, gold):
-    if not is_oracle(lib):
-        pytest.skip("pyramid (levels > 1) is the next item on the B200 path (SURVEY.md §8(f)1)")
     cfg = lib.make_registration_config(
         abi.DREG_PROFILE_CAPPED,
         abi.solver_cfg(data_term=1, order=2, lambda_=5.0, theta=0.05, log_objective=False), 2)
     phi, warped, res = lib.register_pair(gold["rp_target"], gold["rp_source"], cfg)
-    assert np.array_equal(phi, gold["rp2_phi"]) and np.array_equal(warped, gold["rp2_warped"])
     assert res.velocity_count == int(gold["rp2_velocity_count"])
+    if is_oracle(lib):
+        assert np.array_equal(phi, gold["rp2_phi"]) and np.array_equal(warped, gold["rp2_warped"])
+    else:
+        assert max_abs(phi, gold["rp2_phi"]) <= 1e-3 and rel_l2(phi, gold["rp2_phi"]) <= 1e-4

@@ -231,3 +231,50 @@ def test_identity_pair(ctx):
     s = abi.solver_cfg(data_term=1, order=2, lambda_=5.0, theta=0.05, max_iters=10, log_objective=False)
     phi, warped, res = ctx.register_pair(f, f, abi.reg_cfg(s, 1, (5,), (10,)))
     assert np.abs(phi).mean() <= 0.05  # test_registration.cpp:197-210
+
+
+# ---- pyramid: levels > 1 (registration.cpp:208-247, make_registration_config :62-83) ----
+@pytest.mark.parametrize("levels,data_term", [(2, 2), (3, 1), (3, 2)])
+def test_register_pyramid_capped(ctx, oracle, levels, data_term):
+    f, m = synth.make_pair(1, 21, (32, 64, 64))
+    s = abi.solver_cfg(data_term=data_term, order=2, lambda_=0.1 if data_term == 2 else 5.0,
+                       theta=1.0 if data_term == 2 else 0.05, log_objective=False)
+    cfg = oracle.make_registration_config(abi.DREG_PROFILE_CAPPED, s, levels)
+    phi, warped, res = ctx.register_pair(f, m, cfg)
+    phi_o, warped_o, res_o = oracle.register_pair(f, m, cfg)
+    lg, lo = abi.level_logs(res), abi.level_logs(res_o)
+    assert [l["dims"] for l in lg] == [l["dims"] for l in lo]
+    assert [l["solver_iterations"] for l in lg] == [l["solver_iterations"] for l in lo]
+    assert res.velocity_count == res_o.velocity_count
+    print(f"levels {levels}: phi max-abs {max_abs(phi, phi_o):.3e} rel-L2 {rel_l2(phi, phi_o):.3e}")
+    assert max_abs(phi, phi_o) <= PHI_MAX_ABS and rel_l2(phi, phi_o) <= PHI_REL_L2
+    assert ctx.jacobian_stats(phi).nonpositive == oracle.jacobian_stats(phi_o).nonpositive
+    for a, b in zip(lg, lo):
+        assert np.allclose(a["mean_sad"], b["mean_sad"], rtol=1e-4, atol=1e-9)
+
+
+def test_register_pyramid_converged_odd_dims(ctx, oracle):
+    """converged profile (tol 0.01 early exit per solve) on odd extents (edge-replicated downsample)."""
+    f, m = synth.make_pair(1, 22, (19, 21, 23))
+    s = abi.solver_cfg(data_term=2, order=1, lambda_=0.5, theta=0.5, log_objective=False)
+    cfg = oracle.make_registration_config(abi.DREG_PROFILE_CONVERGED, s, 2)
+    cfg.max_warps_per_level[0] = 4
+    cfg.max_warps_per_level[1] = 3
+    phi, warped, res = ctx.register_pair(f, m, cfg)
+    phi_o, warped_o, res_o = oracle.register_pair(f, m, cfg)
+    lg, lo = abi.level_logs(res), abi.level_logs(res_o)
+    assert res.velocity_count == res_o.velocity_count
+    for a, b in zip(lg, lo):
+        assert a["dims"] == b["dims"]
+        assert all(abs(x - y) <= 1 for x, y in zip(a["solver_iterations"], b["solver_iterations"]))
+    assert max_abs(phi, phi_o) <= PHI_MAX_ABS
+
+
+def test_pyramid_batch_matches_single(ctx):
+    F, M = synth.make_batch(1, 400, 3, (16, 32, 32))
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, log_objective=False)
+    cfg = dreg.make_registration_config(abi.DREG_PROFILE_CAPPED, s, 2)
+    phis, warps, res = ctx.register_batch(list(F), list(M), cfg)
+    for i in range(3):
+        p1, w1, r1 = ctx.register_pair(F[i], M[i], cfg)
+        assert np.array_equal(p1, phis[i]) and r1.velocity_count == res[i].velocity_count
