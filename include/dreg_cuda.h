@@ -138,6 +138,10 @@ int dreg_cuda_set_stream(dreg_cuda_ctx* ctx, void* stream);
 int64_t dreg_cuda_kernel_launches(const dreg_cuda_ctx* ctx);
 /* Pairs processed concurrently per batch chunk (0 = automatic). */
 int dreg_cuda_set_batch_chunk(dreg_cuda_ctx* ctx, int pairs);
+/* Spectral-solve arithmetic: 0 = auto (fp64 butterflies/twiddles/multiplier for solves
+ * of more than 100 iterations, fp32 otherwise), 1 = always fp32, 2 = always fp64.
+ * Field and spectrum storage are fp32 in every mode, like the reference's fields. */
+int dreg_cuda_set_precision(dreg_cuda_ctx* ctx, int mode);
 /* 1 = capture each registration chunk as a CUDA graph (default), 0 = plain launches */
 int dreg_cuda_set_use_graphs(dreg_cuda_ctx* ctx, int enable);
 

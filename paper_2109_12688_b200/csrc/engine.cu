@@ -143,6 +143,8 @@ struct Geometry {
     DevArray<float2> twx, xtw, twy, twz;
     DevArray<int> xpos;
     DevArray<float> sx, sy, sz, sy_fast, sz_fast;
+    DevArray<double2> twx64, xtw64, twy64, twz64;  // precise-mode tables
+    DevArray<double> sx64, sy64, sz64;
     int fast = 0, prefetch = 1;
     size_t xsmem = 0, psmem = 0;
 
@@ -172,9 +174,6 @@ struct Geometry {
         xsmem = xpass_smem_bytes(L, hx, TL, PM);
         psmem = plane_smem_bytes(Ny, Nz, PY);
         if (xsmem > 227 * 1024) throw ArgFail("x extent too large for the shared-memory x-pass");
-        if (psmem > 227 * 1024)
-            throw ArgFail("y*z plane of " + std::to_string(Ny) + "x" + std::to_string(Nz) +
-                          " exceeds the single-CTA plane kernel (227 KB shared memory)");
         if ((lines + TL - 1) / TL > kMaxPartials) throw ArgFail("grid has too many x-lines");
 
         std::vector<float2> h(L);
@@ -201,6 +200,40 @@ struct Geometry {
         s.assign(Nz, 0.f);
         for (int pos = 0; pos < Nz; ++pos) s[pos] = one_minus_cos(freq_of_pos(pz, pos), Nz);
         up(sz, s);
+        {  // fp64 copies of the twiddles / symbol tables for the precise mode
+            auto w64 = [](long num, long den) {
+                long q = num % den;
+                if (q < 0) q += den;
+                const double a = -2.0 * kPi * (double)q / (double)den;
+                return make_double2(std::cos(a), std::sin(a));
+            };
+            auto s64 = [](int k, int n) {
+                if (k == 0) return 0.0;
+                const double t = std::sin(kPi * (double)k / (double)n);
+                return 2.0 * t * t;
+            };
+            std::vector<double2> hd(L);
+            for (int e = 0; e < L; ++e) hd[e] = w64(e, L);
+            up(twx64, hd);
+            hd.assign(hx + 1, {});
+            for (int k = 0; k <= hx; ++k) hd[k] = w64(k, M);
+            up(xtw64, hd);
+            hd.assign(Ny, {});
+            for (int e = 0; e < Ny; ++e) hd[e] = w64(e, Ny);
+            up(twy64, hd);
+            hd.assign(Nz, {});
+            for (int e = 0; e < Nz; ++e) hd[e] = w64(e, Nz);
+            up(twz64, hd);
+            std::vector<double> sd(hx);
+            for (int p = 0; p < hx; ++p) sd[p] = s64(p, M);
+            up(sx64, sd);
+            sd.assign(Ny, 0.0);
+            for (int pos = 0; pos < Ny; ++pos) sd[pos] = s64(freq_of_pos(py, pos), Ny);
+            up(sy64, sd);
+            sd.assign(Nz, 0.0);
+            for (int pos = 0; pos < Nz; ++pos) sd[pos] = s64(freq_of_pos(pz, pos), Nz);
+            up(sz64, sd);
+        }
         fast = plane_fast_supported(Ny, Nz) && env_int("DREG_FAST_PLANE", 1);
         prefetch = env_int("DREG_PREFETCH", 0);
         if (fast) {
@@ -364,6 +397,7 @@ struct dreg_cuda_ctx {
     int64_t launches = 0;
     int chunk = 0;
     int use_graphs = 1;
+    int precision = 0;  // 0 auto (fp64 spectral arithmetic for solves > 100 iterations), 1 fp32, 2 fp64
     std::map<std::tuple<int, int, int>, std::unique_ptr<Workspace>> wss;  // one per grid size
     Workspace* last = nullptr;
     // pinned host staging for pointer tables and pair states
@@ -506,8 +540,11 @@ struct Launcher {
     }
 };
 
-XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag) {
+XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool precise = false) {
     XArgs a{};
+    a.precise = precise ? 1 : 0;
+    a.twx64 = w.geo.twx64.p;
+    a.xtw64 = w.geo.xtw64.p;
     a.F = w.fields(diag);
     a.px = w.geo.px;
     a.twx = w.geo.twx.p;
@@ -530,8 +567,17 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag) {
     return a;
 }
 
-PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag) {
+PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool precise = false) {
     PArgs p{};
+    p.precise = precise ? 1 : 0;
+    p.twy64 = w.geo.twy64.p;
+    p.twz64 = w.geo.twz64.p;
+    p.sx64 = w.geo.sx64.p;
+    p.sy64 = w.geo.sy64.p;
+    p.sz64 = w.geo.sz64.p;
+    p.lambda64 = sp.lambda;
+    p.theta64 = sp.theta;
+    p.scale64 = sp.theta / (double)w.geo.N;
     p.F = w.fields(diag);
     p.py = w.geo.py;
     p.pz = w.geo.pz;
@@ -548,7 +594,7 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag) {
     p.energy_out = w.energy.p;
     p.sy_fast = w.geo.sy_fast.p;
     p.sz_fast = w.geo.sz_fast.p;
-    p.fast = w.geo.fast;
+    p.fast = w.geo.fast && !precise;
     p.fd_ny.init((unsigned)w.geo.Ny);
     p.fd_nz.init((unsigned)w.geo.Nz);
     return p;
@@ -565,8 +611,12 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     const int I = s.max_iters;
     const std::vector<double> coef = nesterov_coefs(I, s.accelerate != 0);
     if (with_setup) L(launch_grad_diff(w.vg(), w.regbufs(), w.fields(diag), P, st));
-    XArgs xa = make_xargs(w, sp, diag);
-    PArgs pa = make_pargs(w, sp, diag);
+    // precision policy: the accelerated iteration amplifies per-iteration
+    // rounding, so long solves get fp64 spectral arithmetic (storage stays fp32)
+    const int pol = L.c->precision;
+    const bool precise = pol == 2 || (pol == 0 && I > 100);
+    XArgs xa = make_xargs(w, sp, diag, precise);
+    PArgs pa = make_pargs(w, sp, diag, precise);
     pa.need_tail = need_tail ? 1 : 0;
     auto energy = [&](int k) {
         // objective_k = data term + lambda * spectral_energy(v_k)   (admm.cpp:288-292)
@@ -684,7 +734,7 @@ void run_registration(dreg_cuda_ctx* c, const std::vector<Workspace*>& lv, int P
         c->launches += L.count;
         return;
     }
-    const std::string key = graph_key(P, cfg, lv);
+    const std::string key = graph_key(P, cfg, lv) + "|prec" + std::to_string(c->precision);
     auto it = w.graphs.find(key);
     if (it == w.graphs.end()) {
         Launcher L{c};
@@ -891,6 +941,12 @@ int64_t dreg_cuda_kernel_launches(const dreg_cuda_ctx* c) { return c ? c->launch
 int dreg_cuda_set_batch_chunk(dreg_cuda_ctx* c, int pairs) {
     if (!c || pairs < 0) return DREG_INVALID_ARGUMENT;
     c->chunk = pairs;
+    return DREG_OK;
+}
+
+int dreg_cuda_set_precision(dreg_cuda_ctx* c, int mode) {
+    if (!c || mode < 0 || mode > 2) return DREG_INVALID_ARGUMENT;
+    c->precision = mode;
     return DREG_OK;
 }
 

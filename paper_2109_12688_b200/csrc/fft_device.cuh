@@ -8,52 +8,86 @@
 // permutation pass from the 3-D FFT (FFTW's plan in the reference does the
 // equivalent internally; fft.cpp:52-55).
 //
-// Layout: element e of line l lives at buf[l*ls + e*es] (complex64).  Threads are
-// mapped line-fastest, which with an odd line pitch makes every stage
-// shared-memory bank-conflict free for both contiguous and strided lines.
+// Everything is templated on the complex type C: float2 (fast path) or double2
+// (precise mode: fp64 butterflies for long solves, storage stays fp32).
+//
+// Layout: element e of line l lives at buf[l*ls + e*es].  Threads are mapped
+// line-fastest, which with an odd line pitch makes every stage shared-memory
+// bank-conflict free for both contiguous and strided lines.
 #pragma once
 
 #include "common.cuh"
 
 namespace dregb {
 
-template <bool INV>
-__device__ __forceinline__ float2 rot_mi(float2 z) {  // multiply by -i (fwd) / +i (inv)
-    return INV ? make_float2(-z.y, z.x) : make_float2(z.y, -z.x);
+template <class C>
+struct CT;
+template <>
+struct CT<float2> {
+    using R = float;
+    __device__ static __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+};
+template <>
+struct CT<double2> {
+    using R = double;
+    __device__ static __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+template <class C>
+__device__ __forceinline__ C cvt_c(float2 v) {
+    return CT<C>::make(v.x, v.y);
+}
+__device__ __forceinline__ float2 to_f2(float2 v) { return v; }
+__device__ __forceinline__ float2 to_f2(double2 v) { return make_float2((float)v.x, (float)v.y); }
+
+template <bool INV, class C>
+__device__ __forceinline__ C rot_mi(C z) {  // multiply by -i (fwd) / +i (inv)
+    return INV ? CT<C>::make(-z.y, z.x) : CT<C>::make(z.y, -z.x);
 }
 
-template <bool INV>
-__device__ __forceinline__ void dft2(float2* x) {
-    const float2 a = x[0], b = x[1];
+template <bool INV, class C>
+__device__ __forceinline__ void dft2(C* x) {
+    const C a = x[0], b = x[1];
     x[0] = cadd(a, b);
     x[1] = csub(a, b);
 }
 
-template <bool INV>
-__device__ __forceinline__ void dft4(float2* x) {
-    const float2 a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
-    const float2 b0 = cadd(x[1], x[3]), b1 = rot_mi<INV>(csub(x[1], x[3]));
+template <bool INV, class C>
+__device__ __forceinline__ void dft4(C* x) {
+    const C a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
+    const C b0 = cadd(x[1], x[3]), b1 = rot_mi<INV>(csub(x[1], x[3]));
     x[0] = cadd(a0, b0);
     x[2] = csub(a0, b0);
     x[1] = cadd(a1, b1);
     x[3] = csub(a1, b1);
 }
 
-template <bool INV>
-__device__ __forceinline__ void dft8(float2* x) {
-    const float h = 0.70710678118654752440f;
-    float2 a[4], b[4];
+template <bool INV, class C>
+__device__ __forceinline__ void dft8(C* x) {
+    using R = typename CT<C>::R;
+    const R h = (R)0.70710678118654752440084436210485;
+    C a[4], b[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         a[j] = cadd(x[j], x[j + 4]);
         b[j] = csub(x[j], x[j + 4]);
     }
     // b_j *= W_8^j (conjugated for the inverse)
-    b[1] = INV ? make_float2(h * (b[1].x - b[1].y), h * (b[1].x + b[1].y))
-               : make_float2(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
+    b[1] = INV ? CT<C>::make(h * (b[1].x - b[1].y), h * (b[1].x + b[1].y))
+               : CT<C>::make(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
     b[2] = rot_mi<INV>(b[2]);
-    b[3] = INV ? make_float2(-h * (b[3].x + b[3].y), h * (b[3].x - b[3].y))
-               : make_float2(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
+    b[3] = INV ? CT<C>::make(-h * (b[3].x + b[3].y), h * (b[3].x - b[3].y))
+               : CT<C>::make(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
     dft4<INV>(a);
     dft4<INV>(b);
 #pragma unroll
@@ -63,29 +97,30 @@ __device__ __forceinline__ void dft8(float2* x) {
     }
 }
 
-template <bool INV>
-__device__ __forceinline__ void dft3(float2* x) {
-    const float c = -0.5f, s = 0.86602540378443864676f;
-    const float2 t1 = cadd(x[1], x[2]);
-    const float2 t2 = make_float2(x[0].x + c * t1.x, x[0].y + c * t1.y);
-    const float2 d = csub(x[1], x[2]);
-    const float2 t3 = rot_mi<INV>(make_float2(s * d.x, s * d.y));
+template <bool INV, class C>
+__device__ __forceinline__ void dft3(C* x) {
+    using R = typename CT<C>::R;
+    const R c = (R)-0.5, s = (R)0.86602540378443864676372317075294;
+    const C t1 = cadd(x[1], x[2]);
+    const C t2 = CT<C>::make(x[0].x + c * t1.x, x[0].y + c * t1.y);
+    const C d = csub(x[1], x[2]);
+    const C t3 = rot_mi<INV>(CT<C>::make(s * d.x, s * d.y));
     x[0] = cadd(x[0], t1);
     x[1] = cadd(t2, t3);
     x[2] = csub(t2, t3);
 }
 
 // Generic radix-R DFT with roots W_R^e = tw[e * (n / R)] (conjugated for INV).
-template <bool INV, int R>
-__device__ __forceinline__ void dft_generic(float2* x, const float2* __restrict__ tw, int n) {
-    float2 y[R];
+template <bool INV, int R, class C>
+__device__ __forceinline__ void dft_generic(C* x, const C* __restrict__ tw, int n) {
+    C y[R];
     const int st = n / R;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-        float2 acc = x[0];
+        C acc = x[0];
 #pragma unroll
         for (int t = 1; t < R; ++t) {
-            const float2 w = tw[((t * k) % R) * st];
+            const C w = tw[((t * k) % R) * st];
             acc = cadd(acc, INV ? cmulc(x[t], w) : cmul(x[t], w));
         }
         y[k] = acc;
@@ -94,8 +129,8 @@ __device__ __forceinline__ void dft_generic(float2* x, const float2* __restrict_
     for (int k = 0; k < R; ++k) x[k] = y[k];
 }
 
-template <bool INV, int R>
-__device__ __forceinline__ void dft_r(float2* x, const float2* __restrict__ tw, int n) {
+template <bool INV, int R, class C>
+__device__ __forceinline__ void dft_r(C* x, const C* __restrict__ tw, int n) {
     if constexpr (R == 2) dft2<INV>(x);
     else if constexpr (R == 3) dft3<INV>(x);
     else if constexpr (R == 4) dft4<INV>(x);
@@ -106,10 +141,9 @@ __device__ __forceinline__ void dft_r(float2* x, const float2* __restrict__ tw, 
 // One butterfly of stage with radix R.  p points at element j1 of its sub-block,
 // step = n1 * es.  DIF: x -> DFT_R -> * W^{j1 k}.  Inverse (adjoint):
 // * conj(W^{j1 k}) -> IDFT_R.
-template <bool INV, int R>
-__device__ __forceinline__ void butterfly(float2* p, int step, int j1, int tws,
-                                          const float2* __restrict__ tw, int n) {
-    float2 x[R];
+template <bool INV, int R, class C>
+__device__ __forceinline__ void butterfly(C* p, int step, int j1, int tws, const C* __restrict__ tw, int n) {
+    C x[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) x[t] = p[t * step];
     if constexpr (INV) {
@@ -130,31 +164,29 @@ __device__ __forceinline__ void butterfly(float2* p, int step, int j1, int tws,
 }
 
 // Slow path for prime radices without a template instance (7 < R <= kMaxRadix).
-template <bool INV>
-__device__ void butterfly_dyn(float2* p, int step, int j1, int tws, const float2* __restrict__ tw,
-                              int n, int R) {
-    float2 x[kMaxRadix];
+template <bool INV, class C>
+__device__ void butterfly_dyn(C* p, int step, int j1, int tws, const C* __restrict__ tw, int n, int R) {
+    C x[kMaxRadix];
     for (int t = 0; t < R; ++t) x[t] = p[t * step];
     const int st = n / R;
     if (INV && j1 != 0)
         for (int k = 1; k < R; ++k) x[k] = cmulc(x[k], tw[j1 * k * tws]);
     for (int k = 0; k < R; ++k) {
-        float2 acc = x[0];
+        C acc = x[0];
         for (int t = 1; t < R; ++t) {
-            const float2 w = tw[((t * k) % R) * st];
+            const C w = tw[((t * k) % R) * st];
             acc = cadd(acc, INV ? cmulc(x[t], w) : cmul(x[t], w));
         }
         if (!INV && j1 != 0 && k != 0) acc = cmul(acc, tw[j1 * k * tws]);
-        p[k * step] = acc;  // safe: no other thread touches this butterfly's slots
+        p[k * step] = acc;  // inputs were copied to x[] first: in place is safe
     }
-    // The loop above wrote outputs while later k still read x[] (registers/local): OK.
 }
 
 // Batched in-place line transform over `nlines` lines.  All threads of the block
 // participate; ends with __syncthreads().
-template <bool INV>
-__device__ void fft_lines(float2* buf, int nlines, const FastDiv& fdl, int ls, int es, const AxisPlan& P,
-                          const float2* __restrict__ tw, int tid, int nthr) {
+template <bool INV, class C>
+__device__ void fft_lines(C* buf, int nlines, const FastDiv& fdl, int ls, int es, const AxisPlan& P,
+                          const C* __restrict__ tw, int tid, int nthr) {
     for (int si = 0; si < P.nst; ++si) {
         const int s = INV ? P.nst - 1 - si : si;
         const int r = P.radix[s], n1 = P.n1[s], tws = P.tws[s];
@@ -168,7 +200,7 @@ __device__ void fft_lines(float2* buf, int nlines, const FastDiv& fdl, int ls, i
             const int line = w - b * nlines;
             const int blk = (int)fd1.div((unsigned)b);
             const int j1 = b - blk * n1;
-            float2* p = buf + line * ls + (blk * ns + j1) * es;
+            C* p = buf + line * ls + (blk * ns + j1) * es;
             switch (r) {
                 case 2: butterfly<INV, 2>(p, step, j1, tws, tw, P.n); break;
                 case 3: butterfly<INV, 3>(p, step, j1, tws, tw, P.n); break;

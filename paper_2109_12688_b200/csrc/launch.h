@@ -33,6 +33,9 @@ struct XArgs {
     int minb;           // x-pass launch-bounds variant: min CTAs per SM (3 or 4)
     int fast_x;         // use the specialised x-pass (xpass_fast.cu) for M in {64, 128, 256}
     int fx_variant;     // point-wise loop variant of the specialised x-pass: 10 * VEC + unroll (22 default)
+    int precise;        // fp64 x-FFT arithmetic (long solves; see plane_split.cu)
+    const double2* twx64;
+    const double2* xtw64;
     int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
     FastDiv fd_lines;   // divide by 3 * TL
 };
@@ -48,6 +51,13 @@ struct PArgs {
     const float* sy_fast;  // [Ny] position table of the specialised plane kernel (radix split R1 x R2)
     const float* sz_fast;  // [Nz]
     int fast;              // use plane_fast_kernel
+    int precise;           // fp64 butterflies/multiplier via the split path
+    const double2* twy64;
+    const double2* twz64;
+    const double* sx64;
+    const double* sy64;
+    const double* sz64;
+    double lambda64, theta64, scale64;
     float lambda, theta, scale;  // scale = theta / voxels
     int order;
     int PY;             // plane row pitch (complex, odd)
@@ -62,6 +72,9 @@ size_t plane_smem_bytes(int Ny, int Nz, int PY);
 // radix split used by the specialised plane kernel for an axis of length n (0 = unsupported)
 int plane_fast_r1(int n);
 bool plane_fast_supported(int Ny, int Nz);
+// three-pass plane for planes above one CTA's shared memory (plane_split.cu)
+bool plane_split_needed(const PArgs& a);
+cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
 bool xpass_tma_eligible(const XArgs& a);
 size_t xpass_tma_smem_bytes(int L, int hx, int TL, int PM, int M);

@@ -19,20 +19,22 @@
 
 namespace dregb {
 
-template <bool INV>
-__device__ __forceinline__ float2 cmul_tw(float2 a, float2 w) {
+template <bool INV, class C>
+__device__ __forceinline__ C cmul_tw(C a, C w) {
     return INV ? cmulc(a, w) : cmul(a, w);
 }
 
 // 16-point DFT in natural order: j = j1 + 4 j2, k = k2 + 4 k1.
-template <bool INV>
-__device__ __forceinline__ void dft16(float2* x) {
-    constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
-    constexpr float h = 0.70710678118654752440f;
+template <bool INV, class C>
+__device__ __forceinline__ void dft16(C* x) {
+    using R = typename CT<C>::R;
+    const R c1 = (R)0.92387953251128675612818318939679, s1 = (R)0.38268343236508977172845998403040;
+    const R h = (R)0.70710678118654752440084436210485;
     // W16^e, e = 0..9 (forward sign)
-    const float2 W[10] = {{1.f, 0.f}, {c1, -s1}, {h, -h}, {s1, -c1}, {0.f, -1.f},
-                          {-s1, -c1}, {-h, -h}, {-c1, -s1}, {-1.f, 0.f}, {-c1, s1}};
-    float2 a[4][4];
+    const C W[10] = {CT<C>::make(1, 0),  CT<C>::make(c1, -s1), CT<C>::make(h, -h),   CT<C>::make(s1, -c1),
+                     CT<C>::make(0, -1), CT<C>::make(-s1, -c1), CT<C>::make(-h, -h), CT<C>::make(-c1, -s1),
+                     CT<C>::make(-1, 0), CT<C>::make(-c1, s1)};
+    C a[4][4];
 #pragma unroll
     for (int j1 = 0; j1 < 4; ++j1) {
 #pragma unroll
@@ -45,15 +47,15 @@ __device__ __forceinline__ void dft16(float2* x) {
         for (int k2 = 1; k2 < 4; ++k2) a[j1][k2] = cmul_tw<INV>(a[j1][k2], W[j1 * k2]);
 #pragma unroll
     for (int k2 = 0; k2 < 4; ++k2) {
-        float2 b[4] = {a[0][k2], a[1][k2], a[2][k2], a[3][k2]};
+        C b[4] = {a[0][k2], a[1][k2], a[2][k2], a[3][k2]};
         dft4<INV>(b);
 #pragma unroll
         for (int k1 = 0; k1 < 4; ++k1) x[k2 + 4 * k1] = b[k1];
     }
 }
 
-template <bool INV, int R>
-__device__ __forceinline__ void rdft(float2* x) {
+template <bool INV, int R, class C>
+__device__ __forceinline__ void rdft(C* x) {
     if constexpr (R == 2) dft2<INV>(x);
     else if constexpr (R == 4) dft4<INV>(x);
     else if constexpr (R == 8) dft8<INV>(x);

@@ -60,8 +60,21 @@ __device__ __forceinline__ void stvN(float* p, const float* in) {
 
 }  // namespace
 
-template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2>
-__global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
+template <class C>
+__device__ __forceinline__ float ld_real(const C* line, int x) {
+    return (float)reinterpret_cast<const decltype(C::x)*>(line)[x];
+}
+
+// u = v + b_hat: formed in the transform's precision (fp64 in precise mode, exactly
+// like the reference's real[i] = double(v) + double(b_hat), admm.cpp:77-80)
+template <class C>
+__device__ __forceinline__ void st_real_sum(C* line, int x, float v, float b) {
+    using R = decltype(C::x);
+    reinterpret_cast<R*>(line)[x] = (R)v + (R)b;
+}
+
+template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2, class C = float2>
+__global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? 3 : 2) xpass_fast_kernel(XArgs a) {
     constexpr int L = kR1 * R2;
     constexpr int HX = L + 1;
     constexpr int PM = L + 1;  // odd line pitch (complex)
@@ -73,10 +86,20 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
     if (MODE <= X_GENERAL && st->solve_done) return;
 
     extern __shared__ __align__(16) unsigned char smem[];
-    float2* buf = reinterpret_cast<float2*>(smem);        // [3][TL][PM]
-    float2* twx = buf + 3 * TL * PM;                      // W_L^e
-    float2* xtw = twx + L;                                // W_M^k, k in [0, HX]
+    constexpr bool F64 = sizeof(C) == 16;
+    C* buf = reinterpret_cast<C*>(smem);                  // [3][TL][PM]
+    C* twx = buf + 3 * TL * PM;                           // W_L^e
+    C* xtw = twx + L;                                     // W_M^k, k in [0, HX]
     double* red = reinterpret_cast<double*>(xtw + HX + 1);
+    const C* twx_g;
+    const C* xtw_g;
+    if constexpr (F64) {
+        twx_g = a.twx64;
+        xtw_g = a.xtw64;
+    } else {
+        twx_g = a.twx;
+        xtw_g = a.xtw;
+    }
     const int tid = threadIdx.x;
     const long long lines = a.F.lines;
     const long long L0 = (long long)blockIdx.x * TL;
@@ -98,12 +121,15 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
             const int cp = i >> 5;  // c * HX + p
             const int c = cp / HX, p = cp - c * HX;
             const bool ok = l < nl;
-            cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
+            if constexpr (F64)
+                buf[(c * TL + l) * PM + p] = ok ? cvt_c<C>(S[(size_t)cp * lines + L0 + l]) : CT<C>::make(0, 0);
+            else
+                cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
         }
     }
-    for (int i = tid; i < L; i += kFT) twx[i] = a.twx[i];
-    for (int i = tid; i <= HX; i += kFT) xtw[i] = a.xtw[i];
-    if (MODE != X_FIRST) cp_async_wait_all();
+    for (int i = tid; i < L; i += kFT) twx[i] = twx_g[i];
+    for (int i = tid; i <= HX; i += kFT) xtw[i] = xtw_g[i];
+    if (!F64 && MODE != X_FIRST) cp_async_wait_all();
     __syncthreads();
 
     // ---- phase 1: c2r -> w_{k-1} in natural order ----
@@ -115,8 +141,8 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
             const int t = r0 + tid;
             const bool act = t < TASKS;
             const int line = t >> 2, j = t & 3;  // line = c * TL + l
-            const float2* X = buf + line * PM;
-            float2 z[2][R2];
+            const C* X = buf + line * PM;
+            C z[2][R2];
             if (act) {
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
@@ -124,23 +150,23 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
 #pragma unroll
                     for (int p1 = 0; p1 < R2; ++p1) {
                         const int k = kR1 * p1 + b;
-                        float2 A = X[k];
-                        float2 B = X[L - k];
+                        C A = X[k];
+                        C B = X[L - k];
                         if (k == 0) {
-                            A.y = 0.f;
-                            B.y = 0.f;
+                            A.y = 0;
+                            B.y = 0;
                         }
                         B.y = -B.y;
-                        const float2 e = cadd(A, B);
-                        const float2 o = cmulc(csub(A, B), xtw[k]);
-                        z[q][p1] = make_float2(e.x - o.y, e.y + o.x);
+                        const C e = cadd(A, B);
+                        const C o = cmulc(csub(A, B), xtw[k]);
+                        z[q][p1] = CT<C>::make(e.x - o.y, e.y + o.x);
                     }
                     rdft<true, R2>(z[q]);
                 }
             }
             __syncthreads();  // every read of these lines done before any write
             if (act) {
-                float2* Y = buf + line * PM;
+                C* Y = buf + line * PM;
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
@@ -153,8 +179,8 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
         // (b) adjoint of the first DIF stage: conj twiddle, inverse radix 8 over stride R2
         for (int t = tid; t < 3 * TL * R2; t += kFT) {
             const int line = t / R2, j1 = t - line * R2;
-            float2* Y = buf + line * PM;
-            float2 x[kR1];
+            C* Y = buf + line * PM;
+            C x[kR1];
 #pragma unroll
             for (int k = 0; k < kR1; ++k) x[k] = Y[j1 + R2 * k];
 #pragma unroll
@@ -191,10 +217,10 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
         if (MODE != X_TAIL) ldvN<VEC>(Dd + gi, dv);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float* wl = reinterpret_cast<const float*>(buf + (c * TL + l) * PM);
+            const C* wl = buf + (c * TL + l) * PM;
 #pragma unroll
             for (int jj = 0; jj < VEC; ++jj) {
-                w[c][jj] = MODE == X_FIRST ? 0.f : wl[x0 + jj];
+                w[c][jj] = MODE == X_FIRST ? 0.f : ld_real(wl, x0 + jj);
                 if (MODE == X_FIRST) vp[c][jj] = 0.f;
                 if (MODE != X_GENERAL) bo[c][jj] = 0.f;
             }
@@ -256,9 +282,9 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
             }
             stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
             if (MODE != X_FIRST) stvN<VEC>(BH + (size_t)c * N + gi, bh[c]);
-            float* ul = reinterpret_cast<float*>(buf + (c * TL + l) * PM);
+            C* ul = buf + (c * TL + l) * PM;
 #pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) ul[x0 + jj] = vn[c][jj] + bh[c][jj];
+            for (int jj = 0; jj < VEC; ++jj) st_real_sum(ul, x0 + jj, vn[c][jj], bh[c][jj]);
         }
     }
 
@@ -267,15 +293,15 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
         if (nl < TL) {
             for (int idx = tid; idx < 3 * TL * PM; idx += kFT) {
                 const int l = (idx / PM) & (TL - 1);
-                if (l >= nl) buf[idx] = make_float2(0.f, 0.f);
+                if (l >= nl) buf[idx] = CT<C>::make(0, 0);
             }
         }
         __syncthreads();
         // (a) first DIF stage: radix 8 over stride R2, twiddle W_L^{j1 k}
         for (int t = tid; t < 3 * TL * R2; t += kFT) {
             const int line = t / R2, j1 = t - line * R2;
-            float2* Y = buf + line * PM;
-            float2 x[kR1];
+            C* Y = buf + line * PM;
+            C x[kR1];
 #pragma unroll
             for (int s = 0; s < kR1; ++s) x[s] = Y[j1 + R2 * s];
             dft8<false>(x);
@@ -292,9 +318,9 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
             const int cj = t >> 5;
             const int c = cj >> 2, j = cj & 3;
             if (l >= nl) continue;
-            const float2* Y = buf + (c * TL + l) * PM;
+            const C* Y = buf + (c * TL + l) * PM;
             const int b0 = j, b1 = j == 0 ? kR1 / 2 : kR1 - j;
-            float2 z0[R2], z1[R2];
+            C z0[R2], z1[R2];
 #pragma unroll
             for (int e = 0; e < R2; ++e) {
                 z0[e] = Y[R2 * b0 + e];
@@ -303,11 +329,11 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
             rdft<false, R2>(z0);
             rdft<false, R2>(z1);
             float2* Sc = S + (size_t)c * HX * lines + L0 + l;
-            auto emit = [&](int k, float2 zk, float2 zpartner) {
-                const float2 zc = cconj(zpartner);
-                const float2 ee = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
-                const float2 oo = make_float2(0.5f * (zk.y - zc.y), -0.5f * (zk.x - zc.x));
-                Sc[(size_t)k * lines] = cadd(ee, cmul(xtw[k], oo));
+            auto emit = [&](int k, C zk, C zpartner) {
+                const C zc = cconj(zpartner);
+                const C ee = CT<C>::make((zk.x + zc.x) * 0.5f, (zk.y + zc.y) * 0.5f);
+                const C oo = CT<C>::make((zk.y - zc.y) * 0.5f, -(zk.x - zc.x) * 0.5f);
+                Sc[(size_t)k * lines] = to_f2(cadd(ee, cmul(xtw[k], oo)));
             };
 #pragma unroll
             for (int p1 = 0; p1 < R2; ++p1) {
@@ -351,10 +377,10 @@ __global__ void __launch_bounds__(kFT, 3) xpass_fast_kernel(XArgs a) {
     }
 }
 
-template <int R2>
+template <int R2, class C = float2>
 static size_t fast_smem() {
     constexpr int L = kR1 * R2;
-    return sizeof(float2) * (3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 32;
+    return sizeof(C) * (3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 32;
 }
 
 bool xpass_fast_eligible(const XArgs& a) {
@@ -366,9 +392,10 @@ bool xpass_fast_eligible(const XArgs& a) {
 template <int MODE, int DT, int R2>
 static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     const dim3 grid((unsigned)((a.F.lines + kFTL - 1) / kFTL), (unsigned)npairs);
-    const size_t smem = fast_smem<R2>();
+    const size_t smem = a.precise ? fast_smem<R2, double2>() : fast_smem<R2>();
     void (*k)(XArgs) = xpass_fast_kernel<MODE, DT, R2>;
-    switch (a.fx_variant) {
+    if (a.precise) k = xpass_fast_kernel<MODE, DT, R2, 2, 2, double2>;
+    else switch (a.fx_variant) {
         case 41: k = xpass_fast_kernel<MODE, DT, R2, 4, 1>; break;
         case 21: k = xpass_fast_kernel<MODE, DT, R2, 2, 1>; break;
         case 24: k = xpass_fast_kernel<MODE, DT, R2, 2, 4>; break;

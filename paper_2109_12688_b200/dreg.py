@@ -67,6 +67,7 @@ def load_library() -> C.CDLL:
     L.dreg_cuda_kernel_launches.restype = C.c_int64
     L.dreg_cuda_set_batch_chunk.argtypes = [P, C.c_int]
     L.dreg_cuda_set_use_graphs.argtypes = [P, C.c_int]
+    L.dreg_cuda_set_precision.argtypes = [P, C.c_int]
     L.dreg_nesterov_next_alpha.argtypes = [C.c_double]
     L.dreg_nesterov_next_alpha.restype = C.c_double
     L.dreg_validate_solver_cfg.argtypes = [C.POINTER(SolverCfg)]
@@ -192,6 +193,10 @@ class Context:
 
     def set_batch_chunk(self, pairs: int) -> None:
         self._check(self.lib.dreg_cuda_set_batch_chunk(self.h, pairs))
+
+    def set_precision(self, mode: int) -> None:
+        """0 auto (fp64 spectral arithmetic for solves > 100 iterations), 1 fp32, 2 fp64."""
+        self._check(self.lib.dreg_cuda_set_precision(self.h, int(mode)))
 
     def set_use_graphs(self, enable: bool) -> None:
         self._check(self.lib.dreg_cuda_set_use_graphs(self.h, int(enable)))

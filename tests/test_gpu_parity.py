@@ -278,3 +278,47 @@ def test_pyramid_batch_matches_single(ctx):
     for i in range(3):
         p1, w1, r1 = ctx.register_pair(F[i], M[i], cfg)
         assert np.array_equal(p1, phis[i]) and r1.velocity_count == res[i].velocity_count
+
+
+# ---- large planes (split three-pass yz kernel, radix-3 z axis) -------------------------
+@pytest.mark.parametrize("shape", [(48, 64, 256), (96, 160, 64), (24, 320, 32)])
+def test_w_update_split_plane(ctx, oracle, shape):
+    """planes whose y*z complex exceeds one CTA's shared memory take the 3-pass path."""
+    v, bh = random_field(shape, 77, 1.0), random_field(shape, 78, 1.0)
+    cfg = abi.solver_cfg(order=2, lambda_=2.0, theta=0.1)
+    out, ref = ctx.w_update(v, bh, cfg), oracle.w_update(v, bh, cfg)
+    assert max_abs(out, ref) <= 1e-5 * np.abs(ref).max()
+    e, r = ctx.regulariser_energy(v, 2), oracle.regulariser_energy(v, 2)
+    assert abs(e - r) <= 2e-6 * abs(r)
+
+
+@pytest.mark.slow
+def test_w_update_config5_grid(ctx, oracle):
+    """config 5 grid (Dims3{256,256,192}): 256 x 192 planes, radix-3 z axis, M = 256 x-pass."""
+    shape = (192, 256, 256)
+    v, bh = random_field(shape, 79, 1.0), random_field(shape, 80, 1.0)
+    cfg = abi.solver_cfg(order=2, lambda_=0.1, theta=1.0)
+    out, ref = ctx.w_update(v, bh, cfg), oracle.w_update(v, bh, cfg)
+    assert max_abs(out, ref) <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.slow
+def test_register_config4_like(ctx, oracle):
+    """config 4 settings (swirl phantom, n=3, lambda 0.05, theta 0.5, 15 fields x 200 iterations)
+    on a 64^3 grid so the single-threaded oracle finishes; zero folding on both sides."""
+    f, m = synth.make_pair(4, 4, (64, 64, 64))
+    c = synth.CONFIGS["config4"]
+    s = abi.solver_cfg(data_term=2, order=c["order"], lambda_=c["lambda_"], theta=c["theta"],
+                       max_iters=c["iters"], log_objective=False)
+    cfg = abi.reg_cfg(s, 1, (c["warps"],), (c["iters"],))
+    phi, res = _reg_parity(ctx, oracle, f, m, cfg)
+    assert ctx.jacobian_stats(phi).nonpositive == 0
+
+
+@pytest.mark.slow
+def test_register_config5_grid_short(ctx, oracle):
+    """config 5 grid and phantom (Dims3{256,256,192}), 2 fields x 10 iterations."""
+    c = synth.CONFIGS["config5"]
+    f, m = synth.make_pair(c["synth"], c["seed"], c["shape"])
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=10, log_objective=False)
+    _reg_parity(ctx, oracle, f, m, abi.reg_cfg(s, 1, (2,), (10,)))
