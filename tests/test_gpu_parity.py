@@ -322,3 +322,38 @@ def test_register_config5_grid_short(ctx, oracle):
     f, m = synth.make_pair(c["synth"], c["seed"], c["shape"])
     s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=10, log_objective=False)
     _reg_parity(ctx, oracle, f, m, abi.reg_cfg(s, 1, (2,), (10,)))
+
+
+@pytest.mark.slow
+def test_config3_all_pairs_against_oracle_records(ctx):
+    """Config 3: all 256 phantom pairs (seeds 1000..1255) registered in batches on the
+    GPU vs the CPU oracle's recorded results (tests/golden/config3_oracle.json, made
+    by tools/run_config3_oracle.py): identical velocity_count, solve count, per-solve
+    iterations and folding counts; SAD logs within 1e-4; | |phi_gpu| - |phi_cpu| |
+    <= 1e-4 |phi_cpu| (a necessary condition of the rel-L2 contract)."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "config3_oracle.json")
+    rec = json.load(open(path))["pairs"]
+    if len(rec) < 256:
+        pytest.skip(f"oracle records incomplete ({len(rec)}/256)")
+    cfg = synth.config_cfg("config3")
+    shape = (64, 128, 128)
+    mismatch = []
+    for s0 in range(1000, 1256, 32):
+        F, M = synth.make_batch(3, s0, 32, shape)
+        phis, _, res = ctx.register_batch(list(F), list(M), cfg, want_warped=False)
+        for i in range(32):
+            r, o = res[i], rec[str(s0 + i)]
+            lg = abi.level_logs(r)[0]
+            js = ctx.jacobian_stats(phis[i])
+            ok = (r.velocity_count == o["velocity_count"] and r.solves == o["solves"]
+                  and lg["solver_iterations"] == o["solver_iterations"] and js.nonpositive == o["folding"]
+                  and np.allclose(lg["mean_sad"], o["mean_sad"], rtol=1e-4))
+            n_g = float(np.sqrt((phis[i].astype(np.float64) ** 2).sum()))
+            n_c = float(np.sqrt(o["phi_sumsq"]))
+            ok = ok and abs(n_g - n_c) <= 1e-4 * n_c
+            if not ok:
+                mismatch.append(s0 + i)
+    assert not mismatch, mismatch
