@@ -73,8 +73,8 @@ __device__ __forceinline__ void st_real_sum(C* line, int x, float v, float b) {
     reinterpret_cast<R*>(line)[x] = (R)v + (R)b;
 }
 
-template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2, class C = float2>
-__global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? 3 : 2) xpass_fast_kernel(XArgs a) {
+template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2, class C = float2, int MINB = 3>
+__global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_kernel(XArgs a) {
     constexpr int L = kR1 * R2;
     constexpr int HX = L + 1;
     constexpr int PM = L + 1;  // odd line pitch (complex)
@@ -401,6 +401,8 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
         case 24: k = xpass_fast_kernel<MODE, DT, R2, 2, 4>; break;
         case 11: k = xpass_fast_kernel<MODE, DT, R2, 1, 1>; break;
         case 14: k = xpass_fast_kernel<MODE, DT, R2, 1, 4>; break;
+        case 224: k = xpass_fast_kernel<MODE, DT, R2, 2, 2, float2, 4>; break;
+        case 214: k = xpass_fast_kernel<MODE, DT, R2, 2, 1, float2, 4>; break;
         default: break;
     }
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -357,3 +357,38 @@ def test_config3_all_pairs_against_oracle_records(ctx):
             if not ok:
                 mismatch.append(s0 + i)
     assert not mismatch, mismatch
+
+
+# ---- robustness: grids through the generic kernels, mixed-validity batches --------------
+@pytest.mark.parametrize("shape", [(8, 12, 20), (10, 16, 48), (12, 20, 96), (16, 16, 160), (4, 4, 4)])
+def test_register_generic_grids(ctx, oracle, shape):
+    """non-power-of-two x extents (generic x-pass), odd y/z (generic plane), tiny grids."""
+    f, m = synth.make_pair(1, 23, shape)
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.2, theta=0.5, max_iters=30, log_objective=False)
+    _reg_parity(ctx, oracle, f, m, abi.reg_cfg(s, 1, (3,), (30,)))
+
+
+def test_batch_isolates_bad_pair(ctx, oracle):
+    """a NaN pair fails alone (status DREG_NUMERIC) and leaves its batch mates intact."""
+    F, M = synth.make_batch(1, 500, 3, (16, 32, 32))
+    M[1, 2, 3, 4] = np.nan
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=20, log_objective=False)
+    cfg = abi.reg_cfg(s, 1, (3,), (20,))
+    with pytest.raises(dreg.NumericError):
+        ctx.register_batch(list(F), list(M), cfg)
+    import ctypes as C
+
+    n = 3
+    res = (abi.PairResult * n)()
+    phis = [np.zeros((16, 32, 32, 3), np.float32) for _ in range(n)]
+    Fp = C.POINTER(C.c_float)
+    T = (Fp * n)(*[np.ascontiguousarray(F[i]).ctypes.data_as(Fp) for i in range(n)])
+    S = (Fp * n)(*[np.ascontiguousarray(M[i]).ctypes.data_as(Fp) for i in range(n)])
+    P = (Fp * n)(*[p.ctypes.data_as(Fp) for p in phis])
+    st = ctx.lib.dreg_cuda_register_batch(ctx.h, n, T, S, abi.Dims3(32, 32, 16), abi.Spacing3(1, 1, 1),
+                                          C.byref(cfg), P, None, res)
+    assert st == abi.DREG_NUMERIC
+    assert [r.status for r in res] == [0, abi.DREG_NUMERIC, 0]
+    for i in (0, 2):
+        po, _, _ = oracle.register_pair(F[i], M[i], cfg)
+        assert max_abs(phis[i], po) <= PHI_MAX_ABS
