@@ -71,72 +71,99 @@ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
-// Deterministic block reduction of doubles (fixed tree order).
-template <int NT>
-__device__ __forceinline__ double block_sum(double v, double* red) {
+// Barrier policies: the whole CTA, or one warp group on a named barrier (bar.sync id, n).
+struct BlockSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+template <int ID, int N>
+struct NamedSync {
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory"); }
+};
+
+// Deterministic reduction of doubles over a group of NT threads (gtid in [0, NT),
+// warp-aligned), fixed tree order.  Result valid in gtid 0.
+template <int NT, class Sync>
+__device__ __forceinline__ double group_sum(double v, double* red, int gtid, Sync sync) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __syncthreads();
+    const int lane = gtid & 31, wid = gtid >> 5;
+    sync();
     if (lane == 0) red[wid] = v;
-    __syncthreads();
+    sync();
     double s = 0.0;
-    if (threadIdx.x == 0) {
+    if (gtid == 0) {
 #pragma unroll
         for (int w = 0; w < NT / 32; ++w) s += red[w];
     }
-    return s;  // valid in thread 0
+    return s;
 }
-
-template <int NT>
-__device__ __forceinline__ double block_min(double v, double* red) {
+template <int NT, class Sync>
+__device__ __forceinline__ double group_min(double v, double* red, int gtid, Sync sync) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_down_sync(0xffffffffu, v, o));
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __syncthreads();
+    const int lane = gtid & 31, wid = gtid >> 5;
+    sync();
     if (lane == 0) red[wid] = v;
-    __syncthreads();
+    sync();
     double s = 1.0e300;
-    if (threadIdx.x == 0) {
+    if (gtid == 0) {
 #pragma unroll
         for (int w = 0; w < NT / 32; ++w) s = fmin(s, red[w]);
     }
     return s;
 }
 
+// Deterministic block reduction of doubles (fixed tree order).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    return group_sum<NT>(v, red, (int)threadIdx.x, BlockSync{});
+}
+template <int NT>
+__device__ __forceinline__ double block_min(double v, double* red) {
+    return group_min<NT>(v, red, (int)threadIdx.x, BlockSync{});
+}
+
 // Deterministic cross-block reduction, K sums per block (fixed per-thread strides +
-// fixed tree => run-to-run bit-identical).  Every thread of the block must call it.
-// Thread 0 writes vals[] as this block's partials into part[k * kMaxPartials + block];
-// the block that arrives last reduces all partials with every thread and returns
-// true (totals valid in thread 0 only).
-template <int NT, int K>
-__device__ __forceinline__ bool reduce_partials(const double (&vals)[K], double* part, unsigned int* counter,
-                                                unsigned int nblocks, double (&tot)[K], double* red,
-                                                unsigned min_mask = 0u, int slot = -1) {
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-        const unsigned sl = slot < 0 ? blockIdx.x : (unsigned)slot;
+// fixed tree => run-to-run bit-identical).  Every thread of the group must call it.
+// gtid 0 writes vals[] as this block's partials into part[k * kMaxPartials + slot];
+// the group that arrives last reduces all partials and returns true (totals valid in
+// gtid 0 only).  s_last: one shared int owned by the group.
+template <int NT, int K, class Sync>
+__device__ __forceinline__ bool group_reduce_partials(const double (&vals)[K], double* part, unsigned int* counter,
+                                                      unsigned int nblocks, double (&tot)[K], double* red,
+                                                      int* s_last, int gtid, Sync sync, unsigned slot,
+                                                      unsigned min_mask = 0u) {
+    if (gtid == 0) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) part[(size_t)k * kMaxPartials + sl] = vals[k];
+        for (int k = 0; k < K; ++k) part[(size_t)k * kMaxPartials + slot] = vals[k];
         __threadfence();
         const unsigned int t = atomicAdd(counter, 1u);
-        s_last = (t == nblocks - 1);
+        *s_last = (t == nblocks - 1);
     }
-    __syncthreads();
-    if (!s_last) return false;
+    sync();
+    if (!*s_last) return false;
     __threadfence();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         const bool is_min = (min_mask >> k) & 1u;
         double acc = is_min ? 1e300 : 0.0;
-        for (unsigned b = threadIdx.x; b < nblocks; b += NT) {
+        for (unsigned b = gtid; b < nblocks; b += NT) {
             const double v = __ldcg(part + (size_t)k * kMaxPartials + b);
             acc = is_min ? fmin(acc, v) : acc + v;
         }
-        tot[k] = is_min ? block_min<NT>(acc, red) : block_sum<NT>(acc, red);
+        tot[k] = is_min ? group_min<NT>(acc, red, gtid, sync) : group_sum<NT>(acc, red, gtid, sync);
     }
-    if (threadIdx.x == 0) *counter = 0u;
+    if (gtid == 0) *counter = 0u;
     return true;
+}
+
+template <int NT, int K>
+__device__ __forceinline__ bool reduce_partials(const double (&vals)[K], double* part, unsigned int* counter,
+                                                unsigned int nblocks, double (&tot)[K], double* red,
+                                                unsigned min_mask = 0u, int slot = -1) {
+    __shared__ int s_last;
+    return group_reduce_partials<NT, K>(vals, part, counter, nblocks, tot, red, &s_last, (int)threadIdx.x,
+                                        BlockSync{}, slot < 0 ? blockIdx.x : (unsigned)slot, min_mask);
 }
 
 // Last-block ticket: returns true in thread 0 of the block that finishes last

@@ -12,6 +12,8 @@
 //    L = 8 R2 digit reversal, position block b holds the frequencies k = b (mod 8), so
 //    blocks {j, 8-j} hold every partner pair (k, L-k) and one thread finishes both.
 // Position of frequency k = 8 p1 + b is R2 b + p1 (same scheme as fft_device.cuh).
+#include <algorithm>
+
 #include "fft_device.cuh"
 #include "kernels.cuh"
 #include "launch.h"
@@ -73,132 +75,108 @@ __device__ __forceinline__ void st_real_sum(C* line, int x, float v, float b) {
     reinterpret_cast<R*>(line)[x] = (R)v + (R)b;
 }
 
-template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2, class C = float2, int MINB = 3>
-__global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_kernel(XArgs a) {
-    constexpr int L = kR1 * R2;
-    constexpr int HX = L + 1;
-    constexpr int PM = L + 1;  // odd line pitch (complex)
-    constexpr int M = 2 * L;
-    constexpr int TL = kFTL;
-    const int pair = blockIdx.y;
-    PairState* st = a.F.st + pair;
-    if (!st->active || st->status) return;
-    if (MODE <= X_GENERAL && st->solve_done) return;
+// ---- tile phases (shared by the one-tile-per-CTA kernel and the pipelined kernel) ----
+// A tile is TL = 32 consecutive x-lines of one pair, all three components; buf holds
+// [3][TL][PM] complex.  `tid` is the thread's index inside the kFT-thread group that
+// runs the phase; `sync` is that group's barrier.
 
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr bool F64 = sizeof(C) == 16;
-    C* buf = reinterpret_cast<C*>(smem);                  // [3][TL][PM]
-    C* twx = buf + 3 * TL * PM;                           // W_L^e
-    C* xtw = twx + L;                                     // W_M^k, k in [0, HX]
-    double* red = reinterpret_cast<double*>(xtw + HX + 1);
-    const C* twx_g;
-    const C* xtw_g;
-    if constexpr (F64) {
-        twx_g = a.twx64;
-        xtw_g = a.xtw64;
-    } else {
-        twx_g = a.twx;
-        xtw_g = a.xtw;
+// cp.async all three components' spectrum rows (transposed) into buf; caller waits.
+template <int R2, class C>
+__device__ __forceinline__ void stage_spectrum(C* buf, const float2* S, long long lines, long long L0, int nl,
+                                               int tid) {
+    constexpr int HX = kR1 * R2 + 1, PM = HX, TL = kFTL;
+    for (int i = tid; i < 3 * HX * TL; i += kFT) {
+        const int l = i & (TL - 1);
+        const int cp = i >> 5;  // c * HX + p
+        const int c = cp / HX, p = cp - c * HX;
+        const bool ok = l < nl;
+        if constexpr (sizeof(C) == 16)
+            buf[(c * TL + l) * PM + p] = ok ? cvt_c<C>(S[(size_t)cp * lines + L0 + l]) : CT<C>::make(0, 0);
+        else
+            cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
     }
-    const int tid = threadIdx.x;
-    const long long lines = a.F.lines;
-    const long long L0 = (long long)blockIdx.x * TL;
-    const int nl = (int)min((long long)TL, lines - L0);
-    const long long N = a.F.N;
+}
 
+// phase 1: c2r of the staged spectrum -> w_{k-1} (real, natural order) in buf.
+template <int R2, class C, class Sync>
+__device__ __forceinline__ void c2r_tile(C* buf, const C* twx, const C* xtw, int tid, Sync sync) {
+    constexpr int L = kR1 * R2, PM = L + 1, TL = kFTL;
+    // (a) pre-process + adjoint of the last DIF stage, whole lines per round
+    constexpr int TASKS = 3 * TL * (kR1 / 2);  // (line, block pair j)
+#pragma unroll 1
+    for (int r0 = 0; r0 < TASKS; r0 += kFT) {
+        const int t = r0 + tid;
+        const bool act = t < TASKS;
+        const int line = t >> 2, j = t & 3;  // line = c * TL + l
+        const C* X = buf + line * PM;
+        C z[2][R2];
+        if (act) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
+#pragma unroll
+                for (int p1 = 0; p1 < R2; ++p1) {
+                    const int k = kR1 * p1 + b;
+                    C A = X[k];
+                    C B = X[L - k];
+                    if (k == 0) {
+                        A.y = 0;
+                        B.y = 0;
+                    }
+                    B.y = -B.y;
+                    const C e = cadd(A, B);
+                    const C o = cmulc(csub(A, B), xtw[k]);
+                    z[q][p1] = CT<C>::make(e.x - o.y, e.y + o.x);
+                }
+                rdft<true, R2>(z[q]);
+            }
+        }
+        sync();  // every read of these lines done before any write
+        if (act) {
+            C* Y = buf + line * PM;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
+#pragma unroll
+                for (int e = 0; e < R2; ++e) Y[R2 * b + e] = z[q][e];
+            }
+        }
+    }
+    sync();
+    // (b) adjoint of the first DIF stage: conj twiddle, inverse radix 8 over stride R2
+    for (int t = tid; t < 3 * TL * R2; t += kFT) {
+        const int line = t / R2, j1 = t - line * R2;
+        C* Y = buf + line * PM;
+        C x[kR1];
+#pragma unroll
+        for (int k = 0; k < kR1; ++k) x[k] = Y[j1 + R2 * k];
+#pragma unroll
+        for (int k = 1; k < kR1; ++k) x[k] = cmulc(x[k], twx[j1 * k]);
+        dft8<true>(x);
+#pragma unroll
+        for (int s = 0; s < kR1; ++s) Y[j1 + R2 * s] = x[s];
+    }
+    sync();
+}
+
+// phase 2: point-wise ADMM updates (fp32) of one tile; accumulates change / residual /
+// data-term partials of this thread.
+template <int MODE, int DT, int R2, int VEC, int UNR, class C>
+__device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid,
+                                               float& fc, float& fr, float& fo) {
+    constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
+    const long long N = a.F.N;
     float* V = a.F.V + (size_t)pair * 3 * N;
     float* BH = a.F.BH + (size_t)pair * 3 * N;
     float* WP = a.F.WP + (size_t)pair * 3 * N;
     float* BP = a.F.BP + (size_t)pair * 3 * N;
     const float* G = a.F.G + (size_t)pair * 3 * N;
     const float* Dd = a.F.D + (size_t)pair * N;
-    float2* S = a.F.S + (size_t)pair * 3 * HX * lines;
-
-    // ---- stage all three spectra (transposed) + tables ----
-    if (MODE != X_FIRST) {
-        for (int i = tid; i < 3 * HX * TL; i += kFT) {
-            const int l = i & (TL - 1);
-            const int cp = i >> 5;  // c * HX + p
-            const int c = cp / HX, p = cp - c * HX;
-            const bool ok = l < nl;
-            if constexpr (F64)
-                buf[(c * TL + l) * PM + p] = ok ? cvt_c<C>(S[(size_t)cp * lines + L0 + l]) : CT<C>::make(0, 0);
-            else
-                cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
-        }
-    }
-    for (int i = tid; i < L; i += kFT) twx[i] = twx_g[i];
-    for (int i = tid; i <= HX; i += kFT) xtw[i] = xtw_g[i];
-    if (!F64 && MODE != X_FIRST) cp_async_wait_all();
-    __syncthreads();
-
-    // ---- phase 1: c2r -> w_{k-1} in natural order ----
-    if (MODE != X_FIRST) {
-        // (a) pre-process + adjoint of the last DIF stage, whole lines per round
-        constexpr int TASKS = 3 * TL * (kR1 / 2);  // (line, block pair j)
-#pragma unroll 1
-        for (int r0 = 0; r0 < TASKS; r0 += kFT) {
-            const int t = r0 + tid;
-            const bool act = t < TASKS;
-            const int line = t >> 2, j = t & 3;  // line = c * TL + l
-            const C* X = buf + line * PM;
-            C z[2][R2];
-            if (act) {
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
-#pragma unroll
-                    for (int p1 = 0; p1 < R2; ++p1) {
-                        const int k = kR1 * p1 + b;
-                        C A = X[k];
-                        C B = X[L - k];
-                        if (k == 0) {
-                            A.y = 0;
-                            B.y = 0;
-                        }
-                        B.y = -B.y;
-                        const C e = cadd(A, B);
-                        const C o = cmulc(csub(A, B), xtw[k]);
-                        z[q][p1] = CT<C>::make(e.x - o.y, e.y + o.x);
-                    }
-                    rdft<true, R2>(z[q]);
-                }
-            }
-            __syncthreads();  // every read of these lines done before any write
-            if (act) {
-                C* Y = buf + line * PM;
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
-#pragma unroll
-                    for (int e = 0; e < R2; ++e) Y[R2 * b + e] = z[q][e];
-                }
-            }
-        }
-        __syncthreads();
-        // (b) adjoint of the first DIF stage: conj twiddle, inverse radix 8 over stride R2
-        for (int t = tid; t < 3 * TL * R2; t += kFT) {
-            const int line = t / R2, j1 = t - line * R2;
-            C* Y = buf + line * PM;
-            C x[kR1];
-#pragma unroll
-            for (int k = 0; k < kR1; ++k) x[k] = Y[j1 + R2 * k];
-#pragma unroll
-            for (int k = 1; k < kR1; ++k) x[k] = cmulc(x[k], twx[j1 * k]);
-            dft8<true>(x);
-#pragma unroll
-            for (int s = 0; s < kR1; ++s) Y[j1 + R2 * s] = x[s];
-        }
-        __syncthreads();
-    }
-
-    // ---- phase 2: point-wise ADMM updates (fp32) ----
     const float thf = (float)a.sp.theta, ithf = (float)(1.0 / a.sp.theta), epsf = (float)a.sp.epsilon;
     const float cf = (float)a.coef;
     const bool accel = a.sp.accelerate != 0;
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
-    float fc = 0.f, fr = 0.f, fo = 0.f;
 #pragma unroll UNR
     for (int i0 = tid * VEC; i0 < nvox; i0 += kFT * VEC) {
         const int l = i0 / M, x0 = i0 - l * M;
@@ -287,75 +265,87 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
             for (int jj = 0; jj < VEC; ++jj) st_real_sum(ul, x0 + jj, vn[c][jj], bh[c][jj]);
         }
     }
+}
 
-    // ---- phase 3: r2c along x ----
-    if (MODE != X_TAIL) {
-        if (nl < TL) {
-            for (int idx = tid; idx < 3 * TL * PM; idx += kFT) {
-                const int l = (idx / PM) & (TL - 1);
-                if (l >= nl) buf[idx] = CT<C>::make(0, 0);
-            }
-        }
-        __syncthreads();
-        // (a) first DIF stage: radix 8 over stride R2, twiddle W_L^{j1 k}
-        for (int t = tid; t < 3 * TL * R2; t += kFT) {
-            const int line = t / R2, j1 = t - line * R2;
-            C* Y = buf + line * PM;
-            C x[kR1];
-#pragma unroll
-            for (int s = 0; s < kR1; ++s) x[s] = Y[j1 + R2 * s];
-            dft8<false>(x);
-#pragma unroll
-            for (int k = 1; k < kR1; ++k) x[k] = cmul(x[k], twx[j1 * k]);
-#pragma unroll
-            for (int k = 0; k < kR1; ++k) Y[j1 + R2 * k] = x[k];
-        }
-        __syncthreads();
-        // (b) last DIF stage on block pairs {j, 8-j} + r2c post-processing -> global
-        constexpr int TASKS = 3 * (kR1 / 2) * TL;  // (c, j) outer, line fastest (coalesced stores)
-        for (int t = tid; t < TASKS; t += kFT) {
-            const int l = t & (TL - 1);
-            const int cj = t >> 5;
-            const int c = cj >> 2, j = cj & 3;
-            if (l >= nl) continue;
-            const C* Y = buf + (c * TL + l) * PM;
-            const int b0 = j, b1 = j == 0 ? kR1 / 2 : kR1 - j;
-            C z0[R2], z1[R2];
-#pragma unroll
-            for (int e = 0; e < R2; ++e) {
-                z0[e] = Y[R2 * b0 + e];
-                z1[e] = Y[R2 * b1 + e];
-            }
-            rdft<false, R2>(z0);
-            rdft<false, R2>(z1);
-            float2* Sc = S + (size_t)c * HX * lines + L0 + l;
-            auto emit = [&](int k, C zk, C zpartner) {
-                const C zc = cconj(zpartner);
-                const C ee = CT<C>::make((zk.x + zc.x) * 0.5f, (zk.y + zc.y) * 0.5f);
-                const C oo = CT<C>::make((zk.y - zc.y) * 0.5f, -(zk.x - zc.x) * 0.5f);
-                Sc[(size_t)k * lines] = to_f2(cadd(ee, cmul(xtw[k], oo)));
-            };
-#pragma unroll
-            for (int p1 = 0; p1 < R2; ++p1) {
-                if (j == 0) {
-                    // block 0: partner of k = 8 p1 is L - k = 8 (R2 - p1) in block 0
-                    emit(kR1 * p1, z0[p1], z0[(R2 - p1) & (R2 - 1)]);
-                    // block 4 is self-paired: partner index R2 - 1 - p1
-                    emit(kR1 * p1 + kR1 / 2, z1[p1], z1[R2 - 1 - p1]);
-                } else {
-                    emit(kR1 * p1 + b0, z0[p1], z1[R2 - 1 - p1]);
-                    emit(kR1 * p1 + b1, z1[p1], z0[R2 - 1 - p1]);
-                }
-            }
-            if (j == 0) emit(L, z0[0], z0[0]);  // Nyquist bin k = L (Z[L] = Z[0])
+// phase 3: r2c of u (real, natural order in buf) -> spectrum rows in global.
+template <int R2, class C, class Sync>
+__device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, float2* S, long long lines,
+                                         long long L0, int nl, int tid, Sync sync) {
+    constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
+    if (nl < TL) {
+        for (int idx = tid; idx < 3 * TL * PM; idx += kFT) {
+            const int l = (idx / PM) & (TL - 1);
+            if (l >= nl) buf[idx] = CT<C>::make(0, 0);
         }
     }
+    sync();
+    // (a) first DIF stage: radix 8 over stride R2, twiddle W_L^{j1 k}
+    for (int t = tid; t < 3 * TL * R2; t += kFT) {
+        const int line = t / R2, j1 = t - line * R2;
+        C* Y = buf + line * PM;
+        C x[kR1];
+#pragma unroll
+        for (int s = 0; s < kR1; ++s) x[s] = Y[j1 + R2 * s];
+        dft8<false>(x);
+#pragma unroll
+        for (int k = 1; k < kR1; ++k) x[k] = cmul(x[k], twx[j1 * k]);
+#pragma unroll
+        for (int k = 0; k < kR1; ++k) Y[j1 + R2 * k] = x[k];
+    }
+    sync();
+    // (b) last DIF stage on block pairs {j, 8-j} + r2c post-processing -> global
+    constexpr int TASKS = 3 * (kR1 / 2) * TL;  // (c, j) outer, line fastest (coalesced stores)
+    for (int t = tid; t < TASKS; t += kFT) {
+        const int l = t & (TL - 1);
+        const int cj = t >> 5;
+        const int c = cj >> 2, j = cj & 3;
+        if (l >= nl) continue;
+        const C* Y = buf + (c * TL + l) * PM;
+        const int b0 = j, b1 = j == 0 ? kR1 / 2 : kR1 - j;
+        C z0[R2], z1[R2];
+#pragma unroll
+        for (int e = 0; e < R2; ++e) {
+            z0[e] = Y[R2 * b0 + e];
+            z1[e] = Y[R2 * b1 + e];
+        }
+        rdft<false, R2>(z0);
+        rdft<false, R2>(z1);
+        float2* Sc = S + (size_t)c * HX * lines + L0 + l;
+        auto emit = [&](int k, C zk, C zpartner) {
+            const C zc = cconj(zpartner);
+            const C ee = CT<C>::make((zk.x + zc.x) * 0.5f, (zk.y + zc.y) * 0.5f);
+            const C oo = CT<C>::make((zk.y - zc.y) * 0.5f, -(zk.x - zc.x) * 0.5f);
+            Sc[(size_t)k * lines] = to_f2(cadd(ee, cmul(xtw[k], oo)));
+        };
+#pragma unroll
+        for (int p1 = 0; p1 < R2; ++p1) {
+            if (j == 0) {
+                // block 0: partner of k = 8 p1 is L - k = 8 (R2 - p1) in block 0
+                emit(kR1 * p1, z0[p1], z0[(R2 - p1) & (R2 - 1)]);
+                // block 4 is self-paired: partner index R2 - 1 - p1
+                emit(kR1 * p1 + kR1 / 2, z1[p1], z1[R2 - 1 - p1]);
+            } else {
+                emit(kR1 * p1 + b0, z0[p1], z1[R2 - 1 - p1]);
+                emit(kR1 * p1 + b1, z1[p1], z0[R2 - 1 - p1]);
+            }
+        }
+        if (j == 0) emit(L, z0[0], z0[0]);  // Nyquist bin k = L (Z[L] = Z[0])
+    }
+}
 
-    const double vals[3] = {block_sum<kFT>((double)fc, red), block_sum<kFT>((double)fr, red),
-                            block_sum<kFT>((double)fo, red)};
+// Per-pair reduction of one tile's partials (slot = tile index within the pair) and
+// the solve-level bookkeeping done by the pair's last tile.
+template <int MODE, class Sync>
+__device__ __forceinline__ void finish_tile(const XArgs& a, int pair, unsigned slot, unsigned ntiles, float fc,
+                                            float fr, float fo, double* red, int* s_last, int tid, Sync sync) {
+    PairState* st = a.F.st + pair;
+    const double vals[3] = {group_sum<kFT>((double)fc, red, tid, sync), group_sum<kFT>((double)fr, red, tid, sync),
+                            group_sum<kFT>((double)fo, red, tid, sync)};
     double tot[3];
-    if (reduce_partials<kFT, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
+    if (group_reduce_partials<kFT, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, ntiles, tot,
+                                      red, s_last, tid, sync, slot) &&
         tid == 0) {
+        const long long N = a.F.N;
         double* dg = a.F.diag ? a.F.diag + (size_t)pair * a.F.diag_stride * 3 : nullptr;
         if (MODE == X_TAIL) {
             const int it = st->iterations;
@@ -373,6 +363,156 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
                 st->solve_done = 1;
                 st->done_iter = a.k;
             }
+        }
+    }
+}
+
+template <int MODE, int DT, int R2, int VEC = 2, int UNR = 2, class C = float2, int MINB = 3>
+__global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_kernel(XArgs a) {
+    constexpr int L = kR1 * R2;
+    constexpr int HX = L + 1;
+    constexpr int PM = L + 1;  // odd line pitch (complex)
+    constexpr int TL = kFTL;
+    const int pair = blockIdx.y;
+    PairState* st = a.F.st + pair;
+    if (!st->active || st->status) return;
+    if (MODE <= X_GENERAL && st->solve_done) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr bool F64 = sizeof(C) == 16;
+    C* buf = reinterpret_cast<C*>(smem);                  // [3][TL][PM]
+    C* twx = buf + 3 * TL * PM;                           // W_L^e
+    C* xtw = twx + L;                                     // W_M^k, k in [0, HX]
+    double* red = reinterpret_cast<double*>(xtw + HX + 1);
+    __shared__ int s_last;
+    const C* twx_g;
+    const C* xtw_g;
+    if constexpr (F64) {
+        twx_g = a.twx64;
+        xtw_g = a.xtw64;
+    } else {
+        twx_g = a.twx;
+        xtw_g = a.xtw;
+    }
+    const int tid = threadIdx.x;
+    const long long lines = a.F.lines;
+    const long long L0 = (long long)blockIdx.x * TL;
+    const int nl = (int)min((long long)TL, lines - L0);
+    const BlockSync sync{};
+
+    if (MODE != X_FIRST) stage_spectrum<R2>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
+    for (int i = tid; i < L; i += kFT) twx[i] = twx_g[i];
+    for (int i = tid; i <= HX; i += kFT) xtw[i] = xtw_g[i];
+    if (!F64 && MODE != X_FIRST) cp_async_wait_all();
+    __syncthreads();
+    if (MODE != X_FIRST) c2r_tile<R2>(buf, twx, xtw, tid, sync);
+    float fc = 0.f, fr = 0.f, fo = 0.f;
+    pointwise_tile<MODE, DT, R2, VEC, UNR>(a, buf, pair, L0, nl, tid, fc, fr, fo);
+    if (MODE != X_TAIL)
+        r2c_tile<R2>(buf, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid, sync);
+    finish_tile<MODE>(a, pair, blockIdx.x, gridDim.x, fc, fr, fo, red, &s_last, tid, sync);
+}
+
+// ---- warp-specialised persistent x-pass (X_GENERAL, fp32) ----------------------------
+// Threads [0, kFT) are the FFT group: stage + c2r tile i into ring buffer i % NB, then
+// r2c of tile i-1.  Threads [kFT, 2 kFT) are the point-wise group: the ADMM update of
+// tile i, streaming the 112 B/voxel of field state.  Hand-off through named barriers:
+//   W_READY(b): FFT arrives after c2r into buffer b; point-wise syncs before reading w.
+//   U_READY(b): point-wise arrives after writing u; FFT syncs before the r2c.
+// With NB >= 2 the x-FFT work of the neighbouring tiles overlaps the HBM stream of
+// tile i instead of serialising with it (the one-tile kernel's critical path).
+// Tiles are assigned round-robin over (pair, tile); per-tile partial sums land in the
+// same slots as the one-tile kernel, so all reductions are bit-identical to it.
+constexpr int kBarFFT = 1, kBarPW = 2, kBarW = 3, kBarU = 6;  // W/U use NB ids each (NB <= 3)
+
+// named barrier base + b with a compile-time id (a run-time id makes ptxas reserve all 16)
+template <int BASE, bool ARRIVE>
+__device__ __forceinline__ void ring_bar(int b) {
+    constexpr int n = 2 * kFT;
+#define DREG_RB(ID)                                                                  \
+    if (ARRIVE) asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(n) : "memory"); \
+    else asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(n) : "memory");
+    switch (b) {
+        case 0: DREG_RB(BASE + 0) break;
+        case 1: DREG_RB(BASE + 1) break;
+        default: DREG_RB(BASE + 2) break;
+    }
+#undef DREG_RB
+}
+
+template <int DT, int R2, int NB, int CPS>
+__global__ void __launch_bounds__(2 * kFT, CPS) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
+    constexpr int MODE = X_GENERAL;
+    constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
+    constexpr int BUF = 3 * TL * PM;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* ring = reinterpret_cast<float2*>(smem);  // [NB][3][TL][PM]
+    float2* twx = ring + NB * BUF;
+    float2* xtw = twx + L;
+    double* red = reinterpret_cast<double*>(xtw + HX + 1);
+    __shared__ int tile_of[NB];
+    __shared__ int s_last;
+    const long long lines = a.F.lines;
+    const int total = tiles_per_pair * npairs;
+    const bool fft_group = threadIdx.x < kFT;
+    const int tid = fft_group ? (int)threadIdx.x : (int)threadIdx.x - kFT;
+
+    if (fft_group) {
+        const NamedSync<kBarFFT, kFT> sync{};
+        for (int i = tid; i < L; i += kFT) twx[i] = a.twx[i];
+        for (int i = tid; i <= HX; i += kFT) xtw[i] = a.xtw[i];
+        // tables are read by this group only; its first barrier below publishes them
+        int prev = -1;  // tile handed to the point-wise group last round
+        int g = blockIdx.x;
+        for (int i = 0;; ++i) {
+            // next runnable tile (pair flags are stable while any of its tiles is pending)
+            while (g < total) {
+                const PairState* st = a.F.st + g / tiles_per_pair;
+                if (st->active && !st->status && !st->solve_done) break;
+                g += gridDim.x;
+            }
+            const int b = i % NB;
+            float2* buf = ring + b * BUF;
+            const int cur = g < total ? g : -1;
+            if (cur >= 0) {
+                const int pair = cur / tiles_per_pair, tile = cur - pair * tiles_per_pair;
+                const long long L0 = (long long)tile * TL;
+                const int nl = (int)min((long long)TL, lines - L0);
+                stage_spectrum<R2>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
+                cp_async_wait_all();
+                sync();
+                c2r_tile<R2>(buf, twx, xtw, tid, sync);
+            }
+            if (tid == 0) tile_of[b] = cur;
+            ring_bar<kBarW, true>(b);
+            if (prev >= 0) {
+                const int pb = (i + NB - 1) % NB;
+                ring_bar<kBarU, false>(pb);
+                const int pair = prev / tiles_per_pair, tile = prev - pair * tiles_per_pair;
+                const long long L0 = (long long)tile * TL;
+                const int nl = (int)min((long long)TL, lines - L0);
+                r2c_tile<R2>(ring + pb * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid,
+                             sync);
+                sync();  // buffer pb is restaged NB - 1 rounds later by this group
+            }
+            if (cur < 0) break;
+            prev = cur;
+            g += gridDim.x;
+        }
+    } else {
+        const NamedSync<kBarPW, kFT> sync{};
+        for (int i = 0;; ++i) {
+            const int b = i % NB;
+            ring_bar<kBarW, false>(b);
+            const int cur = tile_of[b];
+            if (cur < 0) break;
+            const int pair = cur / tiles_per_pair, tile = cur - pair * tiles_per_pair;
+            const long long L0 = (long long)tile * TL;
+            const int nl = (int)min((long long)TL, lines - L0);
+            float fc = 0.f, fr = 0.f, fo = 0.f;
+            pointwise_tile<MODE, DT, R2, 2, 2>(a, ring + b * BUF, pair, L0, nl, tid, fc, fr, fo);
+            ring_bar<kBarU, true>(b);
+            finish_tile<MODE>(a, pair, (unsigned)tile, (unsigned)tiles_per_pair, fc, fr, fo, red, &s_last, tid, sync);
         }
     }
 }
@@ -413,6 +553,32 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int DT, int R2, int NB, int CPS>
+static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
+    constexpr int L = kR1 * R2;
+    const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 32;
+    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, CPS>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = (int)((a.F.lines + kFTL - 1) / kFTL);
+    const int total = tiles * npairs;
+    const int grid = std::min(total, sms * CPS);
+    k<<<grid, 2 * kFT, smem, s>>>(a, tiles, npairs);
+    return cudaGetLastError();
+}
+
+template <int DT, int R2>
+static cudaError_t launch_pipe_r(const XArgs& a, int npairs, cudaStream_t s) {
+    switch (a.pipe) {
+        case 21: return launch_pipe_t<DT, R2, 2, 1>(a, npairs, s);
+        case 22: return launch_pipe_t<DT, R2, 2, 2>(a, npairs, s);
+        default: return launch_pipe_t<DT, R2, 3, 1>(a, npairs, s);
+    }
+}
+
 template <int MODE, int DT>
 static cudaError_t launch_fast_r(const XArgs& a, int npairs, cudaStream_t s) {
     switch (a.F.M) {
@@ -424,6 +590,8 @@ static cudaError_t launch_fast_r(const XArgs& a, int npairs, cudaStream_t s) {
 
 cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t s) {
     const bool l1 = a.sp.data_term == 1;
+    if (mode == X_GENERAL && a.pipe && !a.precise && a.F.M == 128)
+        return l1 ? launch_pipe_r<1, 8>(a, npairs, s) : launch_pipe_r<2, 8>(a, npairs, s);
     switch (mode) {
         case X_FIRST: return l1 ? launch_fast_r<X_FIRST, 1>(a, npairs, s) : launch_fast_r<X_FIRST, 2>(a, npairs, s);
         case X_SECOND: return l1 ? launch_fast_r<X_SECOND, 1>(a, npairs, s) : launch_fast_r<X_SECOND, 2>(a, npairs, s);

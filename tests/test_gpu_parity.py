@@ -7,6 +7,9 @@ relative L2 <= 1e-4; folding counts (det J <= 0) exactly equal.  Point-wise fp64
 building blocks are held to fp32 rounding (a few ulp); the fp32 spectral solve to
 1e-5 * max|ref| like the reference's own w-update pin (test_admm.cpp:184-211).
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -392,3 +395,28 @@ def test_batch_isolates_bad_pair(ctx, oracle):
     for i in (0, 2):
         po, _, _ = oracle.register_pair(F[i], M[i], cfg)
         assert max_abs(phis[i], po) <= PHI_MAX_ABS
+
+
+@pytest.mark.slow
+def test_register_config4_full_against_oracle_record(ctx):
+    """Full config 4 (128^3 swirl, n = 3, 15 fields x 200 iterations; auto precise mode) vs
+    the oracle's record (tests/golden/config4_oracle.json + a [::4]^3 phi subsample, made by
+    tools/run_config4_oracle.py, 23 CPU-minutes): identical velocity / solve / folding
+    counts, SAD log within 1e-4, phi within the contract on the subsample."""
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    rec = json.load(open(os.path.join(gold, "config4_oracle.json")))
+    sub = np.load(os.path.join(gold, "config4_phi_sub4.npz"))["phi"]
+    c = synth.CONFIGS["config4"]
+    f, m = synth.make_pair(c["synth"], c["seed"], c["shape"])
+    phi, warped, res = ctx.register_pair(f, m, synth.config_cfg("config4"))
+    assert res.status == 0
+    assert res.velocity_count == rec["velocity_count"] and res.solves == rec["solves"]
+    assert np.allclose(abi.level_logs(res)[0]["mean_sad"], rec["mean_sad"], rtol=1e-4, atol=1e-9)
+    js = ctx.jacobian_stats(phi)
+    print(f"config4 folding {js.nonpositive} (oracle {rec['folding']}) min det {js.min_det:.4f} "
+          f"(oracle {rec['min_det']:.4f}) sub max-abs {max_abs(phi[::4, ::4, ::4], sub):.2e} "
+          f"rel-L2 {rel_l2(phi[::4, ::4, ::4], sub):.2e}")
+    assert js.nonpositive == rec["folding"]
+    assert abs(js.min_det - rec["min_det"]) <= 1e-3
+    assert max_abs(phi[::4, ::4, ::4], sub) <= PHI_MAX_ABS
+    assert rel_l2(phi[::4, ::4, ::4], sub) <= PHI_REL_L2

@@ -20,6 +20,7 @@ phi, warped, res = o.register_pair(f, m, synth.config_cfg("config4"))
 js = o.jacobian_stats(phi)
 lg = abi.level_logs(res)[0]
 np.save("/tmp/config4_oracle_phi.npy", phi)
+np.savez_compressed(os.path.join(ROOT, "tests", "golden", "config4_phi_sub4.npz"), phi=phi[::4, ::4, ::4].copy())
 json.dump({"config": "config4", "velocity_count": res.velocity_count, "solves": res.solves,
            "mean_sad": lg["mean_sad"], "folding": int(js.nonpositive), "min_det": js.min_det,
            "phi_sum": float(phi.astype(np.float64).sum()), "phi_sumsq": float((phi.astype(np.float64) ** 2).sum()),
