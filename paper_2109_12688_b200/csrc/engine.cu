@@ -563,7 +563,7 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.minb = env_int("DREG_XMINB", 3);
     a.fast_x = env_int("DREG_FAST_X", 1);
     a.fx_variant = env_int("DREG_FX", 22);
-    a.pipe = env_int("DREG_PIPE", 0);
+    a.pipe = env_int("DREG_PIPE", 1);
     a.fd_lines.init((unsigned)(3 * w.geo.TL));
     return a;
 }

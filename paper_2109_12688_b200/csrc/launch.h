@@ -38,7 +38,7 @@ struct XArgs {
     const double2* xtw64;
     int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
     FastDiv fd_lines;   // divide by 3 * TL
-    int pipe;           // warp-specialised persistent x-pass (DREG_PIPE: 0 off, 21/22/31 = NB*10 + CTAs/SM)
+    int pipe;           // warp-specialised persistent x-pass for X_GENERAL, M in {64, 128} (DREG_PIPE: 0 off; default on)
 };
 
 struct PArgs {

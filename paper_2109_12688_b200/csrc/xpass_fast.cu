@@ -37,9 +37,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
-template <int N>
+// HINT 1: streaming loads, no L1 allocation, 256-byte L2 prefetch granule
+template <int N, int HINT = 0>
 __device__ __forceinline__ void ldvN(const float* p, float* out) {
-    if constexpr (N == 4) {
+    if constexpr (N == 4 && HINT == 1) {
+        asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(out[0]), "=f"(out[1]), "=f"(out[2]), "=f"(out[3])
+                     : "l"(p));
+    } else if constexpr (N == 4) {
         const float4 t = *reinterpret_cast<const float4*>(p);
         out[0] = t.x;
         out[1] = t.y;
@@ -75,17 +80,43 @@ __device__ __forceinline__ void st_real_sum(C* line, int x, float v, float b) {
     reinterpret_cast<R*>(line)[x] = (R)v + (R)b;
 }
 
+// VEC consecutive reals of a line starting at even x: 64-bit shared accesses (x even)
+template <int VEC, class C>
+__device__ __forceinline__ void ld_reals(const C* line, int x, float* out) {
+    if constexpr (sizeof(C) == 8 && VEC >= 2) {
+#pragma unroll
+        for (int q = 0; q < VEC; q += 2) {
+            const float2 t = line[(x + q) >> 1];
+            out[q] = t.x;
+            out[q + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) out[q] = ld_real(line, x + q);
+    }
+}
+template <int VEC, class C>
+__device__ __forceinline__ void st_reals_sum(C* line, int x, const float* v, const float* b) {
+    if constexpr (sizeof(C) == 8 && VEC >= 2) {
+#pragma unroll
+        for (int q = 0; q < VEC; q += 2) line[(x + q) >> 1] = make_float2(v[q] + b[q], v[q + 1] + b[q + 1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) st_real_sum(line, x + q, v[q], b[q]);
+    }
+}
+
 // ---- tile phases (shared by the one-tile-per-CTA kernel and the pipelined kernel) ----
 // A tile is TL = 32 consecutive x-lines of one pair, all three components; buf holds
 // [3][TL][PM] complex.  `tid` is the thread's index inside the kFT-thread group that
 // runs the phase; `sync` is that group's barrier.
 
 // cp.async all three components' spectrum rows (transposed) into buf; caller waits.
-template <int R2, class C>
+template <int R2, class C, int NF = kFT>
 __device__ __forceinline__ void stage_spectrum(C* buf, const float2* S, long long lines, long long L0, int nl,
                                                int tid) {
     constexpr int HX = kR1 * R2 + 1, PM = HX, TL = kFTL;
-    for (int i = tid; i < 3 * HX * TL; i += kFT) {
+    for (int i = tid; i < 3 * HX * TL; i += NF) {
         const int l = i & (TL - 1);
         const int cp = i >> 5;  // c * HX + p
         const int c = cp / HX, p = cp - c * HX;
@@ -98,16 +129,19 @@ __device__ __forceinline__ void stage_spectrum(C* buf, const float2* S, long lon
 }
 
 // phase 1: c2r of the staged spectrum -> w_{k-1} (real, natural order) in buf.
-template <int R2, class C, class Sync>
+template <int R2, class C, class Sync, int NF = kFT>
 __device__ __forceinline__ void c2r_tile(C* buf, const C* twx, const C* xtw, int tid, Sync sync) {
     constexpr int L = kR1 * R2, PM = L + 1, TL = kFTL;
-    // (a) pre-process + adjoint of the last DIF stage, whole lines per round
-    constexpr int TASKS = 3 * TL * (kR1 / 2);  // (line, block pair j)
+    // (a) pre-process + adjoint of the last DIF stage.  In place with cross-task reads
+    // inside a line, so each round covers whole lines (LPR lines x 4 block pairs) and
+    // separates all reads from all writes.  Line fastest: a half-warp touches 16 lines
+    // at one block offset; the odd pitch (2 PM = 130 words = 2 mod 32) spreads them
+    // over all 32 banks.
+    constexpr int LPR = NF / (kR1 / 2);
 #pragma unroll 1
-    for (int r0 = 0; r0 < TASKS; r0 += kFT) {
-        const int t = r0 + tid;
-        const bool act = t < TASKS;
-        const int line = t >> 2, j = t & 3;  // line = c * TL + l
+    for (int r0 = 0; r0 < 3 * TL; r0 += LPR) {
+        const int line = r0 + tid % LPR, j = tid / LPR;  // line = c * TL + l
+        const bool act = line < 3 * TL;
         const C* X = buf + line * PM;
         C z[2][R2];
         if (act) {
@@ -144,8 +178,8 @@ __device__ __forceinline__ void c2r_tile(C* buf, const C* twx, const C* xtw, int
     }
     sync();
     // (b) adjoint of the first DIF stage: conj twiddle, inverse radix 8 over stride R2
-    for (int t = tid; t < 3 * TL * R2; t += kFT) {
-        const int line = t / R2, j1 = t - line * R2;
+    for (int t = tid; t < 3 * TL * R2; t += NF) {
+        const int line = t % (3 * TL), j1 = t / (3 * TL);  // line fastest (conflict-free)
         C* Y = buf + line * PM;
         C x[kR1];
 #pragma unroll
@@ -161,7 +195,7 @@ __device__ __forceinline__ void c2r_tile(C* buf, const C* twx, const C* xtw, int
 
 // phase 2: point-wise ADMM updates (fp32) of one tile; accumulates change / residual /
 // data-term partials of this thread.
-template <int MODE, int DT, int R2, int VEC, int UNR, class C>
+template <int MODE, int DT, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0>
 __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid,
                                                float& fc, float& fr, float& fo) {
     constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
@@ -178,28 +212,31 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
 #pragma unroll UNR
-    for (int i0 = tid * VEC; i0 < nvox; i0 += kFT * VEC) {
+    for (int i0 = tid * VEC; i0 < nvox; i0 += NTP * VEC) {
         const int l = i0 / M, x0 = i0 - l * M;
         const size_t gi = base + i0;
         float w[3][VEC], vp[3][VEC], bo[3][VEC], wp[3][VEC], bp[3][VEC], g[3][VEC], dv[VEC];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            if (MODE != X_FIRST) ldvN<VEC>(V + (size_t)c * N + gi, vp[c]);
-            if (MODE == X_GENERAL) ldvN<VEC>(BH + (size_t)c * N + gi, bo[c]);
+            if (MODE != X_FIRST) ldvN<VEC, HINT>(V + (size_t)c * N + gi, vp[c]);
+            if (MODE == X_GENERAL) ldvN<VEC, HINT>(BH + (size_t)c * N + gi, bo[c]);
             if (MODE == X_GENERAL && accel) {
-                ldvN<VEC>(WP + (size_t)c * N + gi, wp[c]);
-                ldvN<VEC>(BP + (size_t)c * N + gi, bp[c]);
+                ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
+                ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);
             }
-            if (MODE != X_TAIL) ldvN<VEC>(G + (size_t)c * N + gi, g[c]);
+            if (MODE != X_TAIL) ldvN<VEC, HINT>(G + (size_t)c * N + gi, g[c]);
         }
-        if (MODE != X_TAIL) ldvN<VEC>(Dd + gi, dv);
+        if (MODE != X_TAIL) ldvN<VEC, HINT>(Dd + gi, dv);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const C* wl = buf + (c * TL + l) * PM;
+            if (MODE != X_FIRST) ld_reals<VEC>(wl, x0, w[c]);
 #pragma unroll
             for (int jj = 0; jj < VEC; ++jj) {
-                w[c][jj] = MODE == X_FIRST ? 0.f : ld_real(wl, x0 + jj);
-                if (MODE == X_FIRST) vp[c][jj] = 0.f;
+                if (MODE == X_FIRST) {
+                    w[c][jj] = 0.f;
+                    vp[c][jj] = 0.f;
+                }
                 if (MODE != X_GENERAL) bo[c][jj] = 0.f;
             }
         }
@@ -260,28 +297,26 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
             }
             stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
             if (MODE != X_FIRST) stvN<VEC>(BH + (size_t)c * N + gi, bh[c]);
-            C* ul = buf + (c * TL + l) * PM;
-#pragma unroll
-            for (int jj = 0; jj < VEC; ++jj) st_real_sum(ul, x0 + jj, vn[c][jj], bh[c][jj]);
+            st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);
         }
     }
 }
 
 // phase 3: r2c of u (real, natural order in buf) -> spectrum rows in global.
-template <int R2, class C, class Sync>
+template <int R2, class C, class Sync, int NF = kFT>
 __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, float2* S, long long lines,
                                          long long L0, int nl, int tid, Sync sync) {
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     if (nl < TL) {
-        for (int idx = tid; idx < 3 * TL * PM; idx += kFT) {
+        for (int idx = tid; idx < 3 * TL * PM; idx += NF) {
             const int l = (idx / PM) & (TL - 1);
             if (l >= nl) buf[idx] = CT<C>::make(0, 0);
         }
     }
     sync();
     // (a) first DIF stage: radix 8 over stride R2, twiddle W_L^{j1 k}
-    for (int t = tid; t < 3 * TL * R2; t += kFT) {
-        const int line = t / R2, j1 = t - line * R2;
+    for (int t = tid; t < 3 * TL * R2; t += NF) {
+        const int line = t % (3 * TL), j1 = t / (3 * TL);  // line fastest (conflict-free)
         C* Y = buf + line * PM;
         C x[kR1];
 #pragma unroll
@@ -295,7 +330,7 @@ __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, flo
     sync();
     // (b) last DIF stage on block pairs {j, 8-j} + r2c post-processing -> global
     constexpr int TASKS = 3 * (kR1 / 2) * TL;  // (c, j) outer, line fastest (coalesced stores)
-    for (int t = tid; t < TASKS; t += kFT) {
+    for (int t = tid; t < TASKS; t += NF) {
         const int l = t & (TL - 1);
         const int cj = t >> 5;
         const int c = cj >> 2, j = cj & 3;
@@ -335,14 +370,14 @@ __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, flo
 
 // Per-pair reduction of one tile's partials (slot = tile index within the pair) and
 // the solve-level bookkeeping done by the pair's last tile.
-template <int MODE, class Sync>
+template <int MODE, class Sync, int NTP = kFT>
 __device__ __forceinline__ void finish_tile(const XArgs& a, int pair, unsigned slot, unsigned ntiles, float fc,
                                             float fr, float fo, double* red, int* s_last, int tid, Sync sync) {
     PairState* st = a.F.st + pair;
-    const double vals[3] = {group_sum<kFT>((double)fc, red, tid, sync), group_sum<kFT>((double)fr, red, tid, sync),
-                            group_sum<kFT>((double)fo, red, tid, sync)};
+    const double vals[3] = {group_sum<NTP>((double)fc, red, tid, sync), group_sum<NTP>((double)fr, red, tid, sync),
+                            group_sum<NTP>((double)fo, red, tid, sync)};
     double tot[3];
-    if (group_reduce_partials<kFT, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, ntiles, tot,
+    if (group_reduce_partials<NTP, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, ntiles, tot,
                                       red, s_last, tid, sync, slot) &&
         tid == 0) {
         const long long N = a.F.N;
@@ -414,24 +449,27 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
 }
 
 // ---- warp-specialised persistent x-pass (X_GENERAL, fp32) ----------------------------
-// Threads [0, kFT) are the FFT group: stage + c2r tile i into ring buffer i % NB, then
-// r2c of tile i-1.  Threads [kFT, 2 kFT) are the point-wise group: the ADMM update of
-// tile i, streaming the 112 B/voxel of field state.  Hand-off through named barriers:
+// Threads [0, kFT) are the FFT group: c2r of tile i in ring buffer i % NB, then the
+// cp.async prefetch of tile i+1's spectrum, then the r2c of tile i-1.  The remaining
+// NPW warps are the point-wise group: the ADMM update of tile i, streaming the
+// 112 B/voxel of field state.  Hand-off through named barriers:
 //   W_READY(b): FFT arrives after c2r into buffer b; point-wise syncs before reading w.
 //   U_READY(b): point-wise arrives after writing u; FFT syncs before the r2c.
-// With NB >= 2 the x-FFT work of the neighbouring tiles overlaps the HBM stream of
-// tile i instead of serialising with it (the one-tile kernel's critical path).
-// Tiles are assigned round-robin over (pair, tile); per-tile partial sums land in the
-// same slots as the one-tile kernel, so all reductions are bit-identical to it.
+// NB = 3: tile i+1 is staged while tile i is updated and tile i-1 transformed back, so
+// the x-FFT work and the spectrum latency overlap the HBM stream instead of
+// serialising with it (the one-tile kernel's critical path).  Each CTA owns a
+// contiguous range of (pair, tile) tiles; the change / residual / data-term partials of
+// a run of consecutive tiles of one pair are reduced once per run (fp64 per-thread sums,
+// fixed tree) and the pair's ticket counts tiles, so the per-pair totals are
+// deterministic for a given SM count.
 constexpr int kBarFFT = 1, kBarPW = 2, kBarW = 3, kBarU = 6;  // W/U use NB ids each (NB <= 3)
 
 // named barrier base + b with a compile-time id (a run-time id makes ptxas reserve all 16)
-template <int BASE, bool ARRIVE>
+template <int BASE, int N, bool ARRIVE>
 __device__ __forceinline__ void ring_bar(int b) {
-    constexpr int n = 2 * kFT;
 #define DREG_RB(ID)                                                                  \
-    if (ARRIVE) asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(n) : "memory"); \
-    else asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(n) : "memory");
+    if (ARRIVE) asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory"); \
+    else asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
     switch (b) {
         case 0: DREG_RB(BASE + 0) break;
         case 1: DREG_RB(BASE + 1) break;
@@ -440,79 +478,162 @@ __device__ __forceinline__ void ring_bar(int b) {
 #undef DREG_RB
 }
 
-template <int DT, int R2, int NB, int CPS>
-__global__ void __launch_bounds__(2 * kFT, CPS) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
+template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0>
+__global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
     constexpr int MODE = X_GENERAL;
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     constexpr int BUF = 3 * TL * PM;
+    constexpr int NF = 32 * FW, NTP = 32 * NPW, NALL = NF + NTP;
+    static_assert(NB == 3, "ring of three tile buffers");
     extern __shared__ __align__(16) unsigned char smem[];
     float2* ring = reinterpret_cast<float2*>(smem);  // [NB][3][TL][PM]
     float2* twx = ring + NB * BUF;
     float2* xtw = twx + L;
-    double* red = reinterpret_cast<double*>(xtw + HX + 1);
+    double* red = reinterpret_cast<double*>(xtw + HX + 1);  // [3][NPW]
+    static_assert(3 * NPW <= 64, "red[] size");
     __shared__ int tile_of[NB];
-    __shared__ int s_last;
     const long long lines = a.F.lines;
-    const int total = tiles_per_pair * npairs;
-    const bool fft_group = threadIdx.x < kFT;
-    const int tid = fft_group ? (int)threadIdx.x : (int)threadIdx.x - kFT;
+    const int T = tiles_per_pair;
+    const int total = T * npairs;
+    const int G = gridDim.x;
+    // contiguous tile range of this CTA (global order: pair-major)
+    auto range_start = [&](int cta) { return (int)(((long long)cta * total) / G); };
+    const int g_end = range_start(blockIdx.x + 1);
+    const bool fft_group = threadIdx.x < NF;
+    const int tid = fft_group ? (int)threadIdx.x : (int)threadIdx.x - NF;
+    auto runnable_from = [&](int g) {  // pair flags are stable while any of its tiles is pending
+        while (g < g_end) {
+            const int pair = g / T;
+            const PairState* st = a.F.st + pair;
+            if (st->active && !st->status && !st->solve_done) return g;
+            g = (pair + 1) * T;
+        }
+        return -1;
+    };
+    auto stage = [&](int g, float2* buf) {
+        const int pair = g / T, tile = g - pair * T;
+        const long long L0 = (long long)tile * TL;
+        const int nl = (int)min((long long)TL, lines - L0);
+        stage_spectrum<R2, float2, NF>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 
     if (fft_group) {
-        const NamedSync<kBarFFT, kFT> sync{};
-        for (int i = tid; i < L; i += kFT) twx[i] = a.twx[i];
-        for (int i = tid; i <= HX; i += kFT) xtw[i] = a.xtw[i];
-        // tables are read by this group only; its first barrier below publishes them
-        int prev = -1;  // tile handed to the point-wise group last round
-        int g = blockIdx.x;
+        const NamedSync<kBarFFT, NF> sync{};
+        for (int i = tid; i < L; i += NF) twx[i] = a.twx[i];
+        for (int i = tid; i <= HX; i += NF) xtw[i] = a.xtw[i];
+        int cur = runnable_from(range_start(blockIdx.x));
+        if (cur >= 0) stage(cur, ring);
+        int prev = -1;
         for (int i = 0;; ++i) {
-            // next runnable tile (pair flags are stable while any of its tiles is pending)
-            while (g < total) {
-                const PairState* st = a.F.st + g / tiles_per_pair;
-                if (st->active && !st->status && !st->solve_done) break;
-                g += gridDim.x;
-            }
             const int b = i % NB;
             float2* buf = ring + b * BUF;
-            const int cur = g < total ? g : -1;
+            const int next = cur >= 0 ? runnable_from(cur + 1) : -1;
             if (cur >= 0) {
-                const int pair = cur / tiles_per_pair, tile = cur - pair * tiles_per_pair;
-                const long long L0 = (long long)tile * TL;
-                const int nl = (int)min((long long)TL, lines - L0);
-                stage_spectrum<R2>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
-                cp_async_wait_all();
-                sync();
-                c2r_tile<R2>(buf, twx, xtw, tid, sync);
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                sync();  // staged spectrum (and, first round, the tables) visible to the group
+                if (!(a.dbg_skip & 1)) c2r_tile<R2, float2, NamedSync<kBarFFT, NF>, NF>(buf, twx, xtw, tid, sync);
             }
             if (tid == 0) tile_of[b] = cur;
-            ring_bar<kBarW, true>(b);
+            ring_bar<kBarW, NALL, true>(b);
+            // prefetch tile i+1 into buffer (i+1) % NB: it held tile i-2, transformed back last round
+            if (next >= 0) stage(next, ring + ((i + 1) % NB) * BUF);
             if (prev >= 0) {
                 const int pb = (i + NB - 1) % NB;
-                ring_bar<kBarU, false>(pb);
-                const int pair = prev / tiles_per_pair, tile = prev - pair * tiles_per_pair;
+                ring_bar<kBarU, NALL, false>(pb);
+                const int pair = prev / T, tile = prev - pair * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
-                r2c_tile<R2>(ring + pb * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid,
-                             sync);
-                sync();  // buffer pb is restaged NB - 1 rounds later by this group
+                if (!(a.dbg_skip & 1))
+                    r2c_tile<R2, float2, NamedSync<kBarFFT, NF>, NF>(ring + pb * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl,
+                                 tid, sync);
+                sync();  // buffer pb is restaged next round by this group
             }
             if (cur < 0) break;
             prev = cur;
-            g += gridDim.x;
+            cur = next;
         }
     } else {
-        const NamedSync<kBarPW, kFT> sync{};
+        const NamedSync<kBarPW, NTP> sync{};
+        // per-thread fp64 sums over the tiles of the current run (consecutive tiles of one pair)
+        double acc[3] = {0.0, 0.0, 0.0};
+        int run_start = -1;
         for (int i = 0;; ++i) {
             const int b = i % NB;
-            ring_bar<kBarW, false>(b);
+            ring_bar<kBarW, NALL, false>(b);
             const int cur = tile_of[b];
             if (cur < 0) break;
-            const int pair = cur / tiles_per_pair, tile = cur - pair * tiles_per_pair;
+            const int pair = cur / T, tile = cur - pair * T;
             const long long L0 = (long long)tile * TL;
             const int nl = (int)min((long long)TL, lines - L0);
             float fc = 0.f, fr = 0.f, fo = 0.f;
-            pointwise_tile<MODE, DT, R2, 2, 2>(a, ring + b * BUF, pair, L0, nl, tid, fc, fr, fo);
-            ring_bar<kBarU, true>(b);
-            finish_tile<MODE>(a, pair, (unsigned)tile, (unsigned)tiles_per_pair, fc, fr, fo, red, &s_last, tid, sync);
+            if (!(a.dbg_skip & 2))
+                pointwise_tile<MODE, DT, R2, VEC, UNR, float2, NTP, HINT>(a, ring + b * BUF, pair, L0, nl, tid,
+                                                                                  fc, fr, fo);
+            ring_bar<kBarU, NALL, true>(b);
+            if (run_start < 0) run_start = tile;
+            acc[0] += (double)fc;
+            acc[1] += (double)fr;
+            acc[2] += (double)fo;
+            // the run ends at the pair's last tile or the end of this CTA's range
+            if (tile != T - 1 && cur + 1 != g_end) continue;
+            if (a.dbg_skip & 8) {
+                acc[0] = acc[1] = acc[2] = 0.0;
+                run_start = -1;
+                continue;
+            }
+            // group sums (fixed tree), then the pair-level ticket weighted by the run length
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], o);
+            sync();  // red[] free (previous run's readers done)
+            if ((tid & 31) == 0)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) red[k * NPW + (tid >> 5)] = acc[k];
+            sync();
+            PairState* st = a.F.st + pair;
+            if (tid == 0) {
+                double* part = a.F.part + (size_t)pair * 3 * kMaxPartials;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    double v = 0.0;
+                    for (int w = 0; w < NPW; ++w) v += red[k * NPW + w];
+                    part[(size_t)k * kMaxPartials + run_start] = v;
+                }
+                const unsigned run_len = (unsigned)(tile + 1 - run_start);
+                __threadfence();
+                const unsigned t = atomicAdd(&st->counter, run_len);
+                if (t + run_len == (unsigned)T) {
+                    __threadfence();
+                    // runs of this pair, in CTA order: deterministic sum
+                    double tot[3] = {0.0, 0.0, 0.0};
+                    const int p0 = pair * T;
+                    for (int c = 0; c < G; ++c) {
+                        const int s0 = max(range_start(c), p0), s1 = min(range_start(c + 1), p0 + T);
+                        if (s0 >= s1) continue;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) tot[k] += __ldcg(part + (size_t)k * kMaxPartials + (s0 - p0));
+                    }
+                    st->counter = 0u;
+                    const long long N = a.F.N;
+                    double* dg = a.F.diag ? a.F.diag + (size_t)pair * a.F.diag_stride * 3 : nullptr;
+                    const double change = tot[0] / (3.0 * (double)N);
+                    if (dg) {
+                        dg[a.k * 3 + 0] = change;
+                        if (a.k >= 1) dg[(a.k - 1) * 3 + 1] = sqrt(tot[1]);
+                        dg[a.k * 3 + 2] = tot[2];
+                    }
+                    st->iterations = a.k + 1;
+                    st->final_change = change;
+                    if (change <= a.sp.tol) {
+                        st->solve_done = 1;
+                        st->done_iter = a.k;
+                    }
+                }
+            }
+            acc[0] = acc[1] = acc[2] = 0.0;
+            run_start = -1;
         }
     }
 }
@@ -553,29 +674,28 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int DT, int R2, int NB, int CPS>
+template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0>
 static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
-    constexpr int L = kR1 * R2;
-    const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 32;
-    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, CPS>;
+    constexpr int L = kR1 * R2, NB = 3;
+    const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 64;
+    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = (int)((a.F.lines + kFTL - 1) / kFTL);
-    const int total = tiles * npairs;
-    const int grid = std::min(total, sms * CPS);
-    k<<<grid, 2 * kFT, smem, s>>>(a, tiles, npairs);
+    const int grid = std::min(tiles * npairs, sms);
+    k<<<grid, 32 * (FW + NPW), smem, s>>>(a, tiles, npairs);
     return cudaGetLastError();
 }
 
 template <int DT, int R2>
 static cudaError_t launch_pipe_r(const XArgs& a, int npairs, cudaStream_t s) {
-    switch (a.pipe) {
-        case 21: return launch_pipe_t<DT, R2, 2, 1>(a, npairs, s);
-        case 22: return launch_pipe_t<DT, R2, 2, 2>(a, npairs, s);
-        default: return launch_pipe_t<DT, R2, 3, 1>(a, npairs, s);
+    switch (a.pipe) {  // FFT warps * 10000 + point-wise warps * 100 + VEC * 10 + unroll
+        case 80841: return launch_pipe_t<DT, R2, 8, 4, 1, 8>(a, npairs, s);
+        case 41221: return launch_pipe_t<DT, R2, 12, 2, 1, 4>(a, npairs, s);
+        default: return launch_pipe_t<DT, R2, 8, 4, 1, 4>(a, npairs, s);  // 40841: measured best at M = 128
     }
 }
 
@@ -592,6 +712,8 @@ cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t
     const bool l1 = a.sp.data_term == 1;
     if (mode == X_GENERAL && a.pipe && !a.precise && a.F.M == 128)
         return l1 ? launch_pipe_r<1, 8>(a, npairs, s) : launch_pipe_r<2, 8>(a, npairs, s);
+    if (mode == X_GENERAL && a.pipe && !a.precise && a.F.M == 64)
+        return l1 ? launch_pipe_r<1, 4>(a, npairs, s) : launch_pipe_r<2, 4>(a, npairs, s);
     switch (mode) {
         case X_FIRST: return l1 ? launch_fast_r<X_FIRST, 1>(a, npairs, s) : launch_fast_r<X_FIRST, 2>(a, npairs, s);
         case X_SECOND: return l1 ? launch_fast_r<X_SECOND, 1>(a, npairs, s) : launch_fast_r<X_SECOND, 2>(a, npairs, s);

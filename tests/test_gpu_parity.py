@@ -420,3 +420,28 @@ def test_register_config4_full_against_oracle_record(ctx):
     assert abs(js.min_det - rec["min_det"]) <= 1e-3
     assert max_abs(phi[::4, ::4, ::4], sub) <= PHI_MAX_ABS
     assert rel_l2(phi[::4, ::4, ::4], sub) <= PHI_REL_L2
+
+
+@pytest.mark.parametrize("shape", [(64, 128, 128), (32, 64, 64)])
+def test_pipelined_xpass_bit_identical_to_one_tile_kernel(shape):
+    """The warp-specialised persistent x-pass (default for M in {64, 128}) and the
+    one-tile-per-CTA kernel (DREG_PIPE=0) produce bit-identical phi."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+            "from paper_2109_12688_b200 import dreg, synth\n"
+            "F, M = synth.make_batch(3, 1000, 3, %r)\n"
+            "cfg = synth.config_cfg('config3')\n"
+            "with dreg.Context(0) as ctx:\n"
+            "    phis, _, res = ctx.register_batch(list(F), list(M), cfg, want_warped=False)\n"
+            "h = hashlib.sha256(b''.join(np.ascontiguousarray(p).tobytes() for p in phis))\n"
+            "print(h.hexdigest(), [r.velocity_count for r in res])\n") % (root, shape)
+    outs = []
+    for pipe in ("0", "1"):
+        env = dict(os.environ, DREG_PIPE=pipe)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs

@@ -21,6 +21,8 @@ cfg = synth.config_cfg("config3")
 cfg.max_warps_per_level[0] = K
 with dreg.Context(0) as ctx:
     phis, warps, res = ctx.register_batch(list(F), list(M), cfg, want_phi=False, want_warped=False)
+    if os.environ.get("DREG_DBG_SKIP_TK"):  # timing-only knob for the kernel loop (not the registration)
+        os.environ["DREG_DBG_SKIP"] = os.environ["DREG_DBG_SKIP_TK"]
     tk = ctx.time_kernels(5)
     print({k: (float(v) if not isinstance(v, int) else v) for k, v in tk.items()})
     print("launches", ctx.kernel_launches(), "velocity_counts", [r.velocity_count for r in res])
