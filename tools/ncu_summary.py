@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/ (tracked evidence).
 
-    python tools/ncu_summary.py <tag> <launches.csv> <full.ncu-rep> <pairs>
+    python tools/ncu_summary.py <tag> <launches.csv> <full.ncu-rep[,more.ncu-rep]> <pairs> [launch-list command]
 
 Writes profiles/<tag>_launches.md (per-kernel share of a registration, cold-cache
 serialised ncu times: compare SHARES, not absolutes), profiles/<tag>_ncu_full.md
@@ -42,19 +42,25 @@ def raw(rep):
 
 def main():
     tag, lcsv, rep, pairs = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+    cmd = sys.argv[5] if len(sys.argv) > 5 else None
     os.makedirs(PROF, exist_ok=True)
     agg = launches(lcsv)
     tot = sum(v[1] for v in agg.values())
     lines = [f"# {tag}: ncu launch list (`--metrics gpu__time_duration.sum --clock-control none`)", "",
-             f"Command: `python tools/profile_step.py {pairs} 1` (one registration chunk of {pairs} config-2 pairs, "
-             "1 velocity field x 50 iterations, then the per-kernel timing loop).  ncu serialises launches and "
-             "runs them cold-cache: use the SHARES.", "",
+             (f"Command: `{cmd}`." if cmd else
+              f"Command: `python tools/profile_step.py {pairs} 1` (one registration chunk of {pairs} config-2 pairs, "
+              "1 velocity field x 50 iterations, then the per-kernel timing loop).") +
+             "  ncu serialises launches and runs them cold-cache: use the SHARES.", "",
              "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"| `{k}` | {n} | {t / 1e3:.1f} | {100 * t / tot:.1f}% |")
     open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
 
-    hdr, units, data = raw(rep)
+    reps = rep.split(",")
+    hdr, units, data = raw(reps[0])
+    for extra in reps[1:]:  # further captures (same metric set) appended
+        h2, _, d2 = raw(extra)
+        data += [[r[h2.index(h)] if h in h2 else "" for h in hdr] for r in d2]
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
