@@ -289,7 +289,7 @@ struct Workspace {
     }
 
     static size_t bytes_per_pair(const Geometry& g) {
-        return sizeof(float) * (size_t)g.N * (15 + 1 + 2 + 6 + 2 + 2 + 3 + 3 + 1) +
+        return sizeof(float) * (size_t)g.N * (15 + 1 + 2 + 6 + 2 + 4 + 6 + 3 + 2) +
                sizeof(float2) * 3 * (size_t)g.hx * g.lines + sizeof(double) * 3 * kMaxPartials;
     }
 
@@ -315,11 +315,12 @@ struct Workspace {
         st.alloc(P);
         part.alloc((size_t)P * 3 * kMaxPartials);
         energy.alloc(P);
-        stage_t.alloc(P * N);
-        stage_s.alloc(P * N);
-        stage3.alloc(P * 3 * N);
+        // host-path staging is double-buffered (two chunks in flight: copies overlap compute)
+        stage_t.alloc(2 * P * N);
+        stage_s.alloc(2 * P * N);
+        stage3.alloc(2 * P * 3 * N);
         phi_soa.alloc(P * 3 * N);
-        warped.alloc(P * N);
+        warped.alloc(2 * P * N);
         tgt_tab.alloc(P);
         src_tab.alloc(P);
         phi_tab.alloc(P);
@@ -407,16 +408,54 @@ struct dreg_cuda_ctx {
     float** h_warped = nullptr;
     PairState* h_st = nullptr;
     int h_cap = 0;
+    PairState* h_states = nullptr;  // per-call pair states (all chunks)
+    int h_states_cap = 0;
+    // host-buffer pipeline: H2D / D2H copy streams and per-slot events
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_graph[2] = {nullptr, nullptr}, ev_h2d[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr},
+                ev_tab[2] = {nullptr, nullptr};
 
-    void ensure_host(int P) {
+    void ensure_host(int P) {  // pointer tables: two slots of P entries
         if (P <= h_cap) return;
         free_host();
-        CK(cudaMallocHost((void**)&h_tgt, sizeof(void*) * P));
-        CK(cudaMallocHost((void**)&h_src, sizeof(void*) * P));
-        CK(cudaMallocHost((void**)&h_phi, sizeof(void*) * P));
-        CK(cudaMallocHost((void**)&h_warped, sizeof(void*) * P));
+        CK(cudaMallocHost((void**)&h_tgt, sizeof(void*) * 2 * P));
+        CK(cudaMallocHost((void**)&h_src, sizeof(void*) * 2 * P));
+        CK(cudaMallocHost((void**)&h_phi, sizeof(void*) * 2 * P));
+        CK(cudaMallocHost((void**)&h_warped, sizeof(void*) * 2 * P));
         CK(cudaMallocHost((void**)&h_st, sizeof(PairState) * P));
         h_cap = P;
+    }
+    void ensure_states(int n) {
+        if (n <= h_states_cap) return;
+        if (h_states) cudaFreeHost(h_states);
+        h_states = nullptr;
+        CK(cudaMallocHost((void**)&h_states, sizeof(PairState) * n));
+        h_states_cap = n;
+    }
+    void ensure_pipeline() {
+        if (h2d) return;
+        CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&ev_graph[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_d2h[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_tab[i], cudaEventDisableTiming));
+        }
+    }
+    void free_pipeline() {
+        for (int i = 0; i < 2; ++i)
+            for (cudaEvent_t* e : {&ev_graph[i], &ev_h2d[i], &ev_d2h[i], &ev_tab[i]})
+                if (*e) {
+                    cudaEventDestroy(*e);
+                    *e = nullptr;
+                }
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
+        h2d = d2h = nullptr;
+        if (h_states) cudaFreeHost(h_states);
+        h_states = nullptr;
+        h_states_cap = 0;
     }
     void free_host() {
         if (h_tgt) cudaFreeHost(h_tgt);
@@ -922,9 +961,12 @@ void dreg_cuda_ctx_destroy(dreg_cuda_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->h2d) cudaStreamSynchronize(c->h2d);
+    if (c->d2h) cudaStreamSynchronize(c->d2h);
     c->wss.clear();
     c->last = nullptr;
     c->free_host();
+    c->free_pipeline();
     if (c->own) cudaStreamDestroy(c->own);
     delete c;
 }
@@ -966,6 +1008,10 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     validate_reg(cfg, d);
     if (n_pairs == 0) return DREG_OK;
     const bool host = tgt_host != nullptr;
+    // Host buffers spanning several chunks: chunk j+1's H2D and chunk j-1's D2H overlap
+    // chunk j's registration (copy streams + double-buffered staging).  A single chunk
+    // is not split for overlap: measured at 32 config-2 pairs, 2 x 16 ran 2% slower
+    // end to end than 1 x 32 (tools/e2e_probe.py).
     const int chunk = pick_chunk(c, d, n_pairs);
     // level grids, coarsest first (registration.cpp:208-214: dims halved, rounded up)
     std::vector<dreg_dims3> dl((size_t)cfg->levels);
@@ -977,52 +1023,99 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     Workspace& w = c->workspace(d, chunk, dl);
     lv.back() = &w;
     c->ensure_host(w.P);
+    c->ensure_states(n_pairs);
     const size_t N = (size_t)w.geo.N;
+    const size_t Pc = (size_t)w.P;
     cudaStream_t st = c->stream;
     int first_bad = DREG_OK;
-    std::vector<PairState> states(n_pairs);
-    for (int p0 = 0; p0 < n_pairs; p0 += chunk) {
+    const int nchunks = (n_pairs + chunk - 1) / chunk;
+    if (host) {
+        c->ensure_pipeline();
+        for (int q = 0; q < n_pairs; ++q)
+            if (!tgt_host[q] || !src_host[q]) throw ArgFail("null input volume");
+        // stage slots are free once the previous chunk's registration on st has consumed them
+        CK(cudaEventRecord(c->ev_graph[0], st));
+        CK(cudaEventRecord(c->ev_graph[1], st));
+        CK(cudaEventRecord(c->ev_d2h[0], st));
+        CK(cudaEventRecord(c->ev_d2h[1], st));
+    }
+    // H2D of chunk j's inputs into stage slot j % 2 (h2d stream)
+    auto issue_h2d = [&](int j) {
+        const int slot = j & 1, p0 = j * chunk, P = std::min(chunk, n_pairs - p0);
+        CK(cudaStreamWaitEvent(c->h2d, c->ev_graph[slot], 0));  // chunk j-2 done with the slot
+        for (int p = 0; p < P; ++p) {
+            CK(cudaMemcpyAsync(w.stage_t.p + (slot * Pc + p) * N, tgt_host[p0 + p], sizeof(float) * N,
+                               cudaMemcpyHostToDevice, c->h2d));
+            CK(cudaMemcpyAsync(w.stage_s.p + (slot * Pc + p) * N, src_host[p0 + p], sizeof(float) * N,
+                               cudaMemcpyHostToDevice, c->h2d));
+        }
+        CK(cudaEventRecord(c->ev_h2d[slot], c->h2d));
+    };
+    if (host) issue_h2d(0);
+    for (int j = 0; j < nchunks; ++j) {
+        const int p0 = j * chunk;
         const int P = std::min(chunk, n_pairs - p0);
-        CK(cudaStreamSynchronize(st));  // host pointer tables are reused
+        const int slot = host ? (j & 1) : 0;
+        if (host && j + 1 < nchunks) issue_h2d(j + 1);  // overlaps this chunk's registration
+        // pinned pointer tables: slot reused two chunks later, once its H2D has executed
+        if (host) CK(cudaEventSynchronize(c->ev_tab[slot]));
+        else CK(cudaStreamSynchronize(st));
+        const float** ht = c->h_tgt + slot * Pc;
+        const float** hs = c->h_src + slot * Pc;
+        float** hp = c->h_phi + slot * Pc;
+        float** hw = c->h_warped + slot * Pc;
         for (int p = 0; p < P; ++p) {
             const int q = p0 + p;
             if (host) {
-                if (!tgt_host[q] || !src_host[q]) throw ArgFail("null input volume");
-                CK(cudaMemcpyAsync(w.stage_t.p + p * N, tgt_host[q], sizeof(float) * N, cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(w.stage_s.p + p * N, src_host[q], sizeof(float) * N, cudaMemcpyHostToDevice, st));
-                c->h_tgt[p] = w.stage_t.p + p * N;
-                c->h_src[p] = w.stage_s.p + p * N;
-                c->h_phi[p] = (phi_host && phi_host[q]) ? w.phi_soa.p + p * 3 * N : nullptr;
-                c->h_warped[p] = (warped_host && warped_host[q]) ? w.warped.p + p * N : nullptr;
+                ht[p] = w.stage_t.p + (slot * Pc + p) * N;
+                hs[p] = w.stage_s.p + (slot * Pc + p) * N;
+                hp[p] = (phi_host && phi_host[q]) ? w.phi_soa.p + p * 3 * N : nullptr;
+                hw[p] = (warped_host && warped_host[q]) ? w.warped.p + (slot * Pc + p) * N : nullptr;
             } else {
-                c->h_tgt[p] = tgt_dev + (size_t)q * N;
-                c->h_src[p] = src_dev + (size_t)q * N;
-                c->h_phi[p] = phi_dev ? phi_dev + (size_t)q * 3 * N : nullptr;
-                c->h_warped[p] = warped_dev ? warped_dev + (size_t)q * N : nullptr;
+                ht[p] = tgt_dev + (size_t)q * N;
+                hs[p] = src_dev + (size_t)q * N;
+                hp[p] = phi_dev ? phi_dev + (size_t)q * 3 * N : nullptr;
+                hw[p] = warped_dev ? warped_dev + (size_t)q * N : nullptr;
             }
         }
-        CK(cudaMemcpyAsync(w.tgt_tab.p, c->h_tgt, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(w.src_tab.p, c->h_src, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(w.phi_tab.p, c->h_phi, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(w.warped_tab.p, c->h_warped, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.tgt_tab.p, ht, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.src_tab.p, hs, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.phi_tab.p, hp, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w.warped_tab.p, hw, sizeof(void*) * P, cudaMemcpyHostToDevice, st));
+        if (host) {
+            CK(cudaEventRecord(c->ev_tab[slot], st));
+            CK(cudaStreamWaitEvent(st, c->ev_h2d[slot], 0));  // inputs landed
+            CK(cudaStreamWaitEvent(st, c->ev_d2h[slot], 0));  // chunk j-2's outputs left the slot
+        }
         run_registration(c, lv, P, *cfg);
         if (host) {
+            for (int p = 0; p < P; ++p)
+                if (phi_host && phi_host[p0 + p]) {
+                    CK(launch_soa_to_aos((long long)N, w.phi_soa.p + p * 3 * N, w.stage3.p + (slot * Pc + p) * 3 * N,
+                                         st));
+                    c->launches += 1;
+                }
+        }
+        // pair states stay on st (tiny): the next chunk's reset cannot overtake them
+        CK(cudaMemcpyAsync(c->h_states + p0, w.st.p, sizeof(PairState) * P, cudaMemcpyDeviceToHost, st));
+        if (host) {
+            CK(cudaEventRecord(c->ev_graph[slot], st));
+            CK(cudaStreamWaitEvent(c->d2h, c->ev_graph[slot], 0));
             for (int p = 0; p < P; ++p) {
                 const int q = p0 + p;
-                if (phi_host && phi_host[q]) {
-                    CK(launch_soa_to_aos((long long)N, w.phi_soa.p + p * 3 * N, w.stage3.p + p * 3 * N, st));
-                    c->launches += 1;
-                    CK(cudaMemcpyAsync(phi_host[q], w.stage3.p + p * 3 * N, sizeof(float) * 3 * N,
-                                       cudaMemcpyDeviceToHost, st));
-                }
+                if (phi_host && phi_host[q])
+                    CK(cudaMemcpyAsync(phi_host[q], w.stage3.p + (slot * Pc + p) * 3 * N, sizeof(float) * 3 * N,
+                                       cudaMemcpyDeviceToHost, c->d2h));
                 if (warped_host && warped_host[q])
-                    CK(cudaMemcpyAsync(warped_host[q], w.warped.p + p * N, sizeof(float) * N, cudaMemcpyDeviceToHost, st));
+                    CK(cudaMemcpyAsync(warped_host[q], w.warped.p + (slot * Pc + p) * N, sizeof(float) * N,
+                                       cudaMemcpyDeviceToHost, c->d2h));
             }
+            CK(cudaEventRecord(c->ev_d2h[slot], c->d2h));
         }
-        CK(cudaMemcpyAsync(c->h_st, w.st.p, sizeof(PairState) * P, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        for (int p = 0; p < P; ++p) states[p0 + p] = c->h_st[p];
     }
+    CK(cudaStreamSynchronize(st));
+    if (host) CK(cudaStreamSynchronize(c->d2h));
+    std::vector<PairState> states(c->h_states, c->h_states + n_pairs);
     const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     for (int q = 0; q < n_pairs; ++q) {
         if (states[q].status != DREG_OK && first_bad == DREG_OK) first_bad = states[q].status;
