@@ -630,7 +630,7 @@ static cudaError_t launch_fast(const PArgs& a, int mode, int npairs, cudaStream_
     constexpr int R1Z = NZ == 256 ? 16 : (NZ >= 64 ? 8 : 4);
     constexpr int NT = 256;
     using Lay = PlaneLayout<NY, NY / R1Y>;
-    const size_t smem = sizeof(float2) * (NZ * Lay::P + NY + NZ) + sizeof(double) * 32 + sizeof(float) * (NY + NZ);
+    const size_t smem = sizeof(float2) * NZ * Lay::P + sizeof(TwEntry) * (NY + NZ) + sizeof(double) * 32 + sizeof(float) * (NY + NZ);
     void (*k)(PArgs) = mode == 0 ? plane_fast_kernel<NY, NZ, R1Y, R1Z, NT, 0> : plane_fast_kernel<NY, NZ, R1Y, R1Z, NT, 1>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -651,7 +651,42 @@ bool plane_fast_supported(int Ny, int Nz) {
     return false;
 }
 
+template <int NY, int NZ, int R1Z>
+static cudaError_t launch_reg(const PArgs& a, int mode, int npairs, cudaStream_t s) {
+    using Lay = PlaneLayout<NY, NY / 8>;
+    const size_t smem = sizeof(float2) * (NZ * Lay::P + NY + NZ) + sizeof(double) * 32 + sizeof(float) * (NY + NZ);
+    void (*k)(PArgs) = plane_reg_kernel<NY, NZ, R1Z, 1, 0>;
+    if (mode == 0) {
+        switch (a.order) {
+            case 1: k = plane_reg_kernel<NY, NZ, R1Z, 0, 1>; break;
+            case 2: k = plane_reg_kernel<NY, NZ, R1Z, 0, 2>; break;
+            case 3: k = plane_reg_kernel<NY, NZ, R1Z, 0, 3>; break;
+            default: k = plane_reg_kernel<NY, NZ, R1Z, 0, 0>; break;
+        }
+    }
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    k<<<dim3((unsigned)(3 * a.F.hx), (unsigned)npairs), (NY / 8) * (NZ / R1Z), smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+#define DREG_REG_CASES(X) X(64, 64) X(64, 128) X(128, 64) X(128, 128)
+
+bool plane_reg_supported(int Ny, int Nz) {
+#define X(a, b) if (Ny == a && Nz == b) return true;
+    DREG_REG_CASES(X)
+#undef X
+    return false;
+}
+
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s) {
+    if (a.fast >= 2) {  // z first stage radix NZ / 16 (second stage radix 16)
+#define X(ny, nz) if (a.F.Ny == ny && a.F.Nz == nz) return launch_reg<ny, nz, nz / 16>(a, mode, npairs, s);
+        DREG_REG_CASES(X)
+#undef X
+    }
     if (a.fast) {
 #define X(ny, nz) if (a.F.Ny == ny && a.F.Nz == nz) return launch_fast<ny, nz>(a, mode, npairs, s);
         DREG_FAST_CASES(X)

@@ -61,14 +61,73 @@ struct PairState {
     int level_warps[DREG_MAX_LEVELS];
 };
 
+// fp32 complex arithmetic.  DREG_PACKED selects the sm_100 packed forms (FADD2 /
+// FMUL2 / FFMA2, one instruction per complex add): 0 = scalar, 1 = packed adds,
+// 2 = packed adds and multiplies.  On B200 a packed op issues at half the scalar
+// rate (tools/pipebench: 4 scalar vs 2 packed warp-instructions/clk/SM, 128 fp32
+// lanes/clk/SM either way), so packing saves issue slots, not FP-pipe time.
+#ifndef DREG_PACKED
+#define DREG_PACKED 0
+#endif
+#if DREG_PACKED >= 1
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// a + s * (b.y, b.x): s = (1, -1) gives a - i b, s = (-1, 1) gives a + i b (exact: |s| = 1)
+__device__ __forceinline__ float2 cadd_swp(float2 a, float2 b, float2 s) {
+    return __ffma2_rn(make_float2(b.y, b.x), s, a);
+}
+#else
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd_swp(float2 a, float2 b, float2 s) {
+    return make_float2(a.x + s.x * b.y, a.y + s.y * b.x);
+}
+#endif
+#if DREG_PACKED >= 2
+// a * b given br = (-b.y, b.x) = i b (precomputed for table twiddles)
+__device__ __forceinline__ float2 cmul_r(float2 a, float2 b, float2 br) {
+    return __ffma2_rn(make_float2(a.y, a.y), br, __fmul2_rn(make_float2(a.x, a.x), b));
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return cmul_r(a, b, make_float2(-b.y, b.x)); }
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), make_float2(b.x, -b.y)));
+}
+// a * w and a * conj(w) for a twiddle-table entry t = (w.x, w.y, -w.y, w.x): two
+// instructions each (the swaps are operand modifiers)
+__device__ __forceinline__ float2 cmul_t(float2 a, float4 t) {
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(t.z, t.w), __fmul2_rn(make_float2(a.x, a.x), make_float2(t.x, t.y)));
+}
+__device__ __forceinline__ float2 cmulc_t(float2 a, float4 t) {
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(t.y, t.x), __fmul2_rn(make_float2(a.x, a.x), make_float2(t.w, t.z)));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+#else
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
     return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+#endif
+// Twiddle-table entry type of the plane kernel: (w, i w) as float4 when multiplies are
+// packed (two instructions per twiddle), plain float2 otherwise (half the LDS width).
+#if DREG_PACKED >= 2
+using TwEntry = float4;
+__device__ __forceinline__ float4 tw_entry(float2 w) { return make_float4(w.x, w.y, -w.y, w.x); }
+#else
+using TwEntry = float2;
+__device__ __forceinline__ float2 tw_entry(float2 w) { return w; }
+#endif
+__device__ __forceinline__ float2 cmul_t(float2 a, float2 t) { return cmul(a, t); }
+__device__ __forceinline__ float2 cmulc_t(float2 a, float2 t) { return cmulc(a, t); }
+// 1/d for normal positive d without the IEEE slow path of __frcp_rn: MUFU.RCP plus
+// one Newton step (<= 1 ulp); used for the regulariser multiplier, d >= theta > 0.
+__device__ __forceinline__ float rcp_nr(float d) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+    return fmaf(r, fmaf(-d, r, 1.0f), r);
+}
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
 // Barrier policies: the whole CTA, or one warp group on a named barrier (bar.sync id, n).

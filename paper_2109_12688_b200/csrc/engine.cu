@@ -234,21 +234,24 @@ struct Geometry {
             for (int pos = 0; pos < Nz; ++pos) sd[pos] = s64(freq_of_pos(pz, pos), Nz);
             up(sz64, sd);
         }
-        fast = plane_fast_supported(Ny, Nz) && env_int("DREG_FAST_PLANE", 1);
+        // 1 = plane_fast_kernel; >= 2 (default 3) = register-blocked plane_reg_kernel where
+        // it applies (first stages radix 8 on y and Nz / 16 on z, second stages in smem)
+        fast = plane_fast_supported(Ny, Nz) ? env_int("DREG_FAST_PLANE", 3) : 0;
+        if (fast >= 2 && !plane_reg_supported(Ny, Nz)) fast = 1;
         prefetch = env_int("DREG_PREFETCH", 0);
         if (fast) {
             // tables for the two-stage split R1 x R2 of the specialised kernel
-            auto split = [](int n) {
+            auto split = [](int n, int r1) {
                 AxisPlan q{};
                 q.n = n;
                 q.nst = 2;
-                q.radix[0] = plane_fast_r1(n);
+                q.radix[0] = r1;
                 q.radix[1] = n / q.radix[0];
                 q.n1[0] = q.radix[1];
                 q.n1[1] = 1;
                 return q;
             };
-            const AxisPlan fy = split(Ny), fz = split(Nz);
+            const AxisPlan fy = split(Ny, plane_fast_r1(Ny)), fz = split(Nz, fast >= 2 ? Nz / 16 : plane_fast_r1(Nz));
             s.assign(Ny, 0.f);
             for (int pos = 0; pos < Ny; ++pos) s[pos] = one_minus_cos(freq_of_pos(fy, pos), Ny);
             up(sy_fast, s);
@@ -629,12 +632,14 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     p.lambda = (float)sp.lambda;
     p.theta = (float)sp.theta;
     p.scale = (float)(sp.theta / (double)w.geo.N);
+    p.lam_n = (float)(sp.lambda * (double)w.geo.N / sp.theta);
+    p.n_f = (float)w.geo.N;
     p.order = sp.order;
     p.PY = w.geo.PY;
     p.energy_out = w.energy.p;
     p.sy_fast = w.geo.sy_fast.p;
     p.sz_fast = w.geo.sz_fast.p;
-    p.fast = w.geo.fast && !precise;
+    p.fast = precise ? 0 : w.geo.fast;
     p.fd_ny.init((unsigned)w.geo.Ny);
     p.fd_nz.init((unsigned)w.geo.Nz);
     return p;

@@ -16,6 +16,8 @@
 // bank-conflict free for both contiguous and strided lines.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dregb {
@@ -64,12 +66,38 @@ __device__ __forceinline__ void dft2(C* x) {
 
 template <bool INV, class C>
 __device__ __forceinline__ void dft4(C* x) {
-    const C a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
-    const C b0 = cadd(x[1], x[3]), b1 = rot_mi<INV>(csub(x[1], x[3]));
+    if constexpr (std::is_same<C, float2>::value) {
+        // packed: the +-i rotation of (x1 - x3) folds into one FFMA2 per output
+        const float2 sp = INV ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f);
+        const float2 sm = make_float2(-sp.x, -sp.y);
+        const C a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
+        const C b0 = cadd(x[1], x[3]), d = csub(x[1], x[3]);
+        x[0] = cadd(a0, b0);
+        x[2] = csub(a0, b0);
+        x[1] = cadd_swp(a1, d, sp);
+        x[3] = cadd_swp(a1, d, sm);
+    } else {
+        const C a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
+        const C b0 = cadd(x[1], x[3]), b1 = rot_mi<INV>(csub(x[1], x[3]));
+        x[0] = cadd(a0, b0);
+        x[2] = csub(a0, b0);
+        x[1] = cadd(a1, b1);
+        x[3] = csub(a1, b1);
+    }
+}
+
+// dft4 of (x0, x1, rot(x2), x3) with rot = multiply by -i (fwd) / +i (inv): the
+// rotation folds into the first butterfly level (packed fp32 only).
+template <bool INV>
+__device__ __forceinline__ void dft4_rot2(float2* x) {
+    const float2 sp = INV ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f);
+    const float2 sm = make_float2(-sp.x, -sp.y);
+    const float2 a0 = cadd_swp(x[0], x[2], sp), a1 = cadd_swp(x[0], x[2], sm);
+    const float2 b0 = cadd(x[1], x[3]), d = csub(x[1], x[3]);
     x[0] = cadd(a0, b0);
     x[2] = csub(a0, b0);
-    x[1] = cadd(a1, b1);
-    x[3] = csub(a1, b1);
+    x[1] = cadd_swp(a1, d, sp);
+    x[3] = cadd_swp(a1, d, sm);
 }
 
 template <bool INV, class C>
@@ -83,13 +111,22 @@ __device__ __forceinline__ void dft8(C* x) {
         b[j] = csub(x[j], x[j + 4]);
     }
     // b_j *= W_8^j (conjugated for the inverse)
-    b[1] = INV ? CT<C>::make(h * (b[1].x - b[1].y), h * (b[1].x + b[1].y))
-               : CT<C>::make(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
-    b[2] = rot_mi<INV>(b[2]);
-    b[3] = INV ? CT<C>::make(-h * (b[3].x + b[3].y), h * (b[3].x - b[3].y))
-               : CT<C>::make(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
-    dft4<INV>(a);
-    dft4<INV>(b);
+    if constexpr (std::is_same<C, float2>::value) {
+        const float2 sp = INV ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f);
+        const float2 sm = make_float2(-sp.x, -sp.y);
+        b[1] = cscale(cadd_swp(b[1], b[1], sp), h);
+        b[3] = cscale(cadd_swp(b[3], b[3], sm), -h);
+        dft4<INV>(a);
+        dft4_rot2<INV>(b);
+    } else {
+        b[1] = INV ? CT<C>::make(h * (b[1].x - b[1].y), h * (b[1].x + b[1].y))
+                   : CT<C>::make(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
+        b[2] = rot_mi<INV>(b[2]);
+        b[3] = INV ? CT<C>::make(-h * (b[3].x + b[3].y), h * (b[3].x - b[3].y))
+                   : CT<C>::make(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
+        dft4<INV>(a);
+        dft4<INV>(b);
+    }
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         x[2 * m] = a[m];

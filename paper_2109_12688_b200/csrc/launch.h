@@ -51,7 +51,7 @@ struct PArgs {
     const float* sz;    // [Nz]
     const float* sy_fast;  // [Ny] position table of the specialised plane kernel (radix split R1 x R2)
     const float* sz_fast;  // [Nz]
-    int fast;              // use plane_fast_kernel
+    int fast;              // 1: plane_fast_kernel, 2: plane_reg_kernel
     int precise;           // fp64 butterflies/multiplier via the split path
     const double2* twy64;
     const double2* twz64;
@@ -60,6 +60,7 @@ struct PArgs {
     const double* sz64;
     double lambda64, theta64, scale64;
     float lambda, theta, scale;  // scale = theta / voxels
+    float lam_n, n_f;            // lambda N / theta and N: multiplier 1 / (lam_n K + n_f)
     int order;
     int PY;             // plane row pitch (complex, odd)
     int k;
@@ -73,6 +74,8 @@ size_t plane_smem_bytes(int Ny, int Nz, int PY);
 // radix split used by the specialised plane kernel for an axis of length n (0 = unsupported)
 int plane_fast_r1(int n);
 bool plane_fast_supported(int Ny, int Nz);
+// register-blocked plane kernel (radix-8 first stages on both axes held in registers)
+bool plane_reg_supported(int Ny, int Nz);
 // three-pass plane for planes above one CTA's shared memory (plane_split.cu)
 bool plane_split_needed(const PArgs& a);
 cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);

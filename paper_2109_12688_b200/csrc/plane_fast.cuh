@@ -44,7 +44,8 @@ __device__ __forceinline__ void dft16(C* x) {
 #pragma unroll
     for (int j1 = 1; j1 < 4; ++j1)
 #pragma unroll
-        for (int k2 = 1; k2 < 4; ++k2) a[j1][k2] = cmul_tw<INV>(a[j1][k2], W[j1 * k2]);
+        for (int k2 = 1; k2 < 4; ++k2)
+            a[j1][k2] = (j1 * k2 == 4) ? rot_mi<INV>(a[j1][k2]) : cmul_tw<INV>(a[j1][k2], W[j1 * k2]);
 #pragma unroll
     for (int k2 = 0; k2 < 4; ++k2) {
         C b[4] = {a[0][k2], a[1][k2], a[2][k2], a[3][k2]};
@@ -56,6 +57,7 @@ __device__ __forceinline__ void dft16(C* x) {
 
 template <bool INV, int R, class C>
 __device__ __forceinline__ void rdft(C* x) {
+    static_assert(R == 2 || R == 4 || R == 8 || R == 16, "rdft: radix 2, 4, 8 or 16");
     if constexpr (R == 2) dft2<INV>(x);
     else if constexpr (R == 4) dft4<INV>(x);
     else if constexpr (R == 8) dft8<INV>(x);
@@ -81,8 +83,8 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
     extern __shared__ __align__(16) unsigned char smem[];
     float2* buf = reinterpret_cast<float2*>(smem);
     double* red = reinterpret_cast<double*>(buf + NZ * Lay::P);
-    float2* twy = reinterpret_cast<float2*>(red + 32);  // tables staged once per CTA
-    float2* twz = twy + NY;
+    TwEntry* twy = reinterpret_cast<TwEntry*>(red + 32);  // tables staged once per CTA
+    TwEntry* twz = twy + NY;
     float* sys = reinterpret_cast<float*>(twz + NZ);
     float* szs = sys + NY;
     const int tid = threadIdx.x;
@@ -90,11 +92,11 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
     const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
     float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)a.F.lines;
     for (int i = tid; i < NY; i += NT) {
-        twy[i] = __ldg(a.twy + i);
+        twy[i] = tw_entry(__ldg(a.twy + i));
         sys[i] = __ldg(a.sy_fast + i);
     }
     for (int i = tid; i < NZ; i += NT) {
-        twz[i] = __ldg(a.twz + i);
+        twz[i] = tw_entry(__ldg(a.twz + i));
         szs[i] = __ldg(a.sz_fast + i);
     }
     __syncthreads();
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
         for (int t = 0; t < R1Y; ++t) x[t] = __ldg(Sp + z * NY + j1 + R2Y * t);
         rdft<false, R1Y>(x);
 #pragma unroll
-        for (int k = 1; k < R1Y; ++k) x[k] = cmul(x[k], twy[j1 * k]);
+        for (int k = 1; k < R1Y; ++k) x[k] = cmul_t(x[k], twy[j1 * k]);
 #pragma unroll
         for (int k = 0; k < R1Y; ++k) buf[Lay::at(j1 + R2Y * k, z)] = x[k];
     }
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
         for (int t = 0; t < R1Z; ++t) x[t] = buf[Lay::at(y, j1 + R2Z * t)];
         rdft<false, R1Z>(x);
 #pragma unroll
-        for (int k = 1; k < R1Z; ++k) x[k] = cmul(x[k], twz[j1 * k]);
+        for (int k = 1; k < R1Z; ++k) x[k] = cmul_t(x[k], twz[j1 * k]);
 #pragma unroll
         for (int k = 0; k < R1Z; ++k) buf[Lay::at(y, j1 + R2Z * k)] = x[k];
     }
@@ -159,8 +161,8 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
                 K *= order >= 2 ? b2 : 1.0f;
                 K *= order >= 4 ? b2 : 1.0f;
                 K *= order >= 6 ? b2 : 1.0f;
-                const float m = a.scale * __frcp_rn(fmaf(a.lambda, K, a.theta));
-                x[e] = make_float2(x[e].x * m, x[e].y * m);
+                const float m = a.scale * rcp_nr(fmaf(a.lambda, K, a.theta));
+                x[e] = cscale(x[e], m);
             }
             rdft<true, R2Z>(x);
 #pragma unroll
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
 #pragma unroll
         for (int k = 0; k < R1Z; ++k) x[k] = buf[Lay::at(y, j1 + R2Z * k)];
 #pragma unroll
-        for (int k = 1; k < R1Z; ++k) x[k] = cmulc(x[k], twz[j1 * k]);
+        for (int k = 1; k < R1Z; ++k) x[k] = cmulc_t(x[k], twz[j1 * k]);
         rdft<true, R1Z>(x);
 #pragma unroll
         for (int t = 0; t < R1Z; ++t) buf[Lay::at(y, j1 + R2Z * t)] = x[t];
@@ -218,10 +220,209 @@ __global__ void __launch_bounds__(NT, (NY * NZ <= 8192) ? 3 : 1) plane_fast_kern
 #pragma unroll
         for (int k = 0; k < R1Y; ++k) x[k] = buf[Lay::at(j1 + R2Y * k, z)];
 #pragma unroll
-        for (int k = 1; k < R1Y; ++k) x[k] = cmulc(x[k], twy[j1 * k]);
+        for (int k = 1; k < R1Y; ++k) x[k] = cmulc_t(x[k], twy[j1 * k]);
         rdft<true, R1Y>(x);
 #pragma unroll
         for (int t = 0; t < R1Y; ++t) Sp[z * NY + j1 + R2Y * t] = x[t];
+    }
+}
+
+// Register-blocked yz-plane kernel (radix-8 / radix-R1Z first stages).  Thread
+// (y1, z1) holds the 8 x R1Z sub-grid {(y1 + R2Y*t, z1 + R2Z*u)} in registers, so the
+// first DIF stage of BOTH axes runs straight out of the global load and the last
+// adjoint stage of both axes straight into the global store:
+//   global -> [y1, z1] -> smem -> [y2] -> smem -> [z2 * m z2^-1] -> smem
+//          -> [y2^-1] -> smem -> [z1^-1, y1^-1] -> global
+// i.e. 4 shared-memory round trips instead of plane_fast_kernel's 6, and each
+// thread loads its first-stage twiddles once per plane instead of once per
+// butterfly.  Positions and multiplier tables are those of plane_fast_kernel with
+// R1Y = 8 and the same R1Z (same digit-reversed placement), so results agree to
+// rounding.
+//
+// The multiplier theta / (lambda K_n + theta) / N is evaluated as
+// 1 / ((lambda N / theta) K_n + N) with K_n = (2 s)^n, the doubled position tables
+// staged in shared memory and n a compile-time constant (ORD 1..3; 0 = run-time n).
+template <int ORD>
+__device__ __forceinline__ float kn_pow(float base, int order) {
+    if constexpr (ORD == 1) return base;
+    else if constexpr (ORD == 2) return base * base;
+    else if constexpr (ORD == 3) return base * (base * base);
+    else {
+        const float b2 = base * base;
+        float K = (order & 1) ? base : 1.0f;
+        K *= order >= 2 ? b2 : 1.0f;
+        K *= order >= 4 ? b2 : 1.0f;
+        K *= order >= 6 ? b2 : 1.0f;
+        return K;
+    }
+}
+
+template <int NY, int NZ, int R1Z, int MODE, int ORD>
+__global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), (NY * NZ <= 8192) ? 3 : 1) plane_reg_kernel(PArgs a) {
+    constexpr int R2Y = NY / 8, R2Z = NZ / R1Z, NT = R2Y * R2Z;
+    static_assert(R2Y <= 16 && R2Z <= 16 && (R1Z == 4 || R1Z == 8), "radix split outside rdft<>");
+    using Lay = PlaneLayout<NY, R2Y>;
+    const int pair = blockIdx.y;
+    PairState* st = a.F.st + pair;
+    if (!st->active || st->status) return;
+    if (st->solve_done && (!a.need_tail || a.k > st->done_iter)) return;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2* buf = reinterpret_cast<float2*>(smem);
+    double* red = reinterpret_cast<double*>(buf + NZ * Lay::P);
+    float2* twy = reinterpret_cast<float2*>(red + 32);
+    float2* twz = twy + NY;
+    float* sys = reinterpret_cast<float*>(twz + NZ);
+    float* szs = sys + NY;
+    const int tid = threadIdx.x;
+    const int hx = a.F.hx;
+    const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
+    float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)a.F.lines;
+    const int y1 = tid % R2Y, z1 = tid / R2Y;
+
+    // stage A: global -> registers (all loads in flight at once)
+    float2 x[R1Z][8];  // [z sub-index][y sub-index]
+#pragma unroll
+    for (int u = 0; u < R1Z; ++u)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[u][t] = __ldg(Sp + (z1 + R2Z * u) * NY + y1 + R2Y * t);
+    // position tables doubled (exact) for the multiplier base 2 (sx + sy + sz)
+    const float dbl = MODE == 0 ? 2.0f : 1.0f;
+    for (int i = tid; i < NY; i += NT) {
+        twy[i] = __ldg(a.twy + i);
+        sys[i] = dbl * __ldg(a.sy_fast + i);
+    }
+    for (int i = tid; i < NZ; i += NT) {
+        twz[i] = __ldg(a.twz + i);
+        szs[i] = dbl * __ldg(a.sz_fast + i);
+    }
+    // y stage 1: radix 8 over t, twiddle W_NY^(y1 k)
+#pragma unroll
+    for (int u = 0; u < R1Z; ++u) dft8<false>(x[u]);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        const float2 w = __ldg(a.twy + y1 * k);
+#pragma unroll
+        for (int u = 0; u < R1Z; ++u) x[u][k] = cmul(x[u][k], w);
+    }
+    // z stage 1: radix R1Z over u, twiddle W_NZ^(z1 k)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        float2 col[R1Z];
+#pragma unroll
+        for (int u = 0; u < R1Z; ++u) col[u] = x[u][t];
+        rdft<false, R1Z>(col);
+#pragma unroll
+        for (int u = 0; u < R1Z; ++u) x[u][t] = col[u];
+    }
+#pragma unroll
+    for (int k = 1; k < R1Z; ++k) {
+        const float2 w = __ldg(a.twz + z1 * k);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[k][t] = cmul(x[k][t], w);
+    }
+#pragma unroll
+    for (int u = 0; u < R1Z; ++u)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) buf[Lay::at(y1 + R2Y * t, z1 + R2Z * u)] = x[u][t];
+    __syncthreads();
+    // y stage 2 (radix R2Y on contiguous blocks)
+    for (int b = tid; b < NZ * 8; b += NT) {
+        const int blk = b % 8, z = b / 8;
+        float2 v[R2Y];
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) v[e] = buf[Lay::at(blk * R2Y + e, z)];
+        rdft<false, R2Y>(v);
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) buf[Lay::at(blk * R2Y + e, z)] = v[e];
+    }
+    __syncthreads();
+    // z stage 2 + multiplier + adjoint z stage 2 (or the energy sum)
+    const float sxp = dbl * __ldg(a.sx + p);
+    const int order = a.order;
+    const float lam_n = a.lam_n, n_f = a.n_f;
+    double acc = 0.0;
+    for (int b = tid; b < NY * R1Z; b += NT) {
+        const int y = b % NY, blk = b / NY;
+        float2 v[R2Z];
+#pragma unroll
+        for (int e = 0; e < R2Z; ++e) v[e] = buf[Lay::at(y, blk * R2Z + e)];
+        rdft<false, R2Z>(v);
+        const float sy = sys[y];
+        if (MODE == 0) {
+            const float sxy = sxp + sy;  // doubled
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) {
+                // theta / (lambda (2 s)^n + theta) / N, s = 3 - cos - cos - cos (regularizer.cpp:69-73)
+                const float K = kn_pow<ORD>(sxy + szs[blk * R2Z + e], order);
+                v[e] = cscale(v[e], rcp_nr(fmaf(lam_n, K, n_f)));
+            }
+            rdft<true, R2Z>(v);
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) buf[Lay::at(y, blk * R2Z + e)] = v[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) {
+                const double base = 2.0 * ((double)sxp + (double)sy + (double)szs[blk * R2Z + e]);
+                double K = base;
+                for (int q = 1; q < a.order; ++q) K *= base;
+                acc += K * ((double)v[e].x * v[e].x + (double)v[e].y * v[e].y);
+            }
+        }
+    }
+    if (MODE == 1) {
+        const bool self_conj = (p == 0) || (2 * p == a.F.M);
+        const double vals[1] = {block_sum<NT>(acc, red) * (self_conj ? 1.0 : 2.0)};
+        double tot[1];
+        if (reduce_partials<NT, 1>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot,
+                                      red) &&
+            tid == 0)
+            a.energy_out[pair] = 0.5 * tot[0] / (double)a.F.N;
+        return;
+    }
+    __syncthreads();
+    // adjoint y stage 2
+    for (int b = tid; b < NZ * 8; b += NT) {
+        const int blk = b % 8, z = b / 8;
+        float2 v[R2Y];
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) v[e] = buf[Lay::at(blk * R2Y + e, z)];
+        rdft<true, R2Y>(v);
+#pragma unroll
+        for (int e = 0; e < R2Y; ++e) buf[Lay::at(blk * R2Y + e, z)] = v[e];
+    }
+    __syncthreads();
+    // stage E: adjoint z stage 1 and y stage 1 in registers, straight to global
+#pragma unroll
+    for (int u = 0; u < R1Z; ++u)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[u][t] = buf[Lay::at(y1 + R2Y * t, z1 + R2Z * u)];
+#pragma unroll
+    for (int k = 1; k < R1Z; ++k) {
+        const float2 w = twz[z1 * k];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[k][t] = cmulc(x[k][t], w);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        float2 col[R1Z];
+#pragma unroll
+        for (int u = 0; u < R1Z; ++u) col[u] = x[u][t];
+        rdft<true, R1Z>(col);
+#pragma unroll
+        for (int u = 0; u < R1Z; ++u) x[u][t] = col[u];
+    }
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        const float2 w = twy[y1 * k];
+#pragma unroll
+        for (int u = 0; u < R1Z; ++u) x[u][k] = cmulc(x[u][k], w);
+    }
+#pragma unroll
+    for (int u = 0; u < R1Z; ++u) {
+        dft8<true>(x[u]);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) Sp[(z1 + R2Z * u) * NY + y1 + R2Y * t] = x[u][t];
     }
 }
 

@@ -34,7 +34,7 @@ from .abi import (  # noqa: F401  (re-exported config helpers)
     solver_cfg,
 )
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdreg_cuda.so")
+_LIB_PATH = os.environ.get("DREG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdreg_cuda.so")
 _F = C.POINTER(C.c_float)
 _D = C.POINTER(C.c_double)
 _lib = None

@@ -98,7 +98,9 @@ def test_downsample_upsample(ctx, oracle):
 
 # ---- spectral w-update (admm.cpp:66-101) -------------------------------------------
 W_SHAPES = [(4, 4, 4), (4, 6, 4), (4, 4, 5), (6, 5, 7), (8, 8, 8), (12, 10, 9), (16, 16, 16),
-            (32, 64, 64), (64, 128, 128), (30, 36, 42), (16, 20, 96)]
+            (32, 64, 64), (64, 128, 128), (30, 36, 42), (16, 20, 96),
+            # every (Nz, Ny) of the register-blocked plane kernel (plane_fast.cuh)
+            (64, 64, 16), (128, 64, 8), (128, 128, 8)]
 
 
 @pytest.mark.parametrize("shape", W_SHAPES)
@@ -111,13 +113,23 @@ def test_w_update(ctx, oracle, shape, order):
     assert max_abs(out, ref) <= 1e-5 * np.abs(ref).max(), max_abs(out, ref)
 
 
+@pytest.mark.parametrize("order", [4, 5, 6])
+def test_w_update_high_order(ctx, oracle, order):
+    """Orders above 3 take the run-time-order multiplier of the plane kernels."""
+    shape = (64, 128, 16)
+    v, bh = random_field(shape, 70 + order, 1.0), random_field(shape, 80 + order, 1.0)
+    cfg = abi.solver_cfg(order=order, lambda_=0.5, theta=0.1)
+    out, ref = ctx.w_update(v, bh, cfg), oracle.w_update(v, bh, cfg)
+    assert max_abs(out, ref) <= 1e-5 * np.abs(ref).max(), max_abs(out, ref)
+
+
 def test_w_update_lambda0_passthrough(ctx):
     v, bh = random_field((6, 6, 6), 60, 1.0), random_field((6, 6, 6), 61, 1.0)
     out = ctx.w_update(v, bh, abi.solver_cfg(order=2, lambda_=0.0, theta=0.1))
     assert max_abs(out, v.astype(np.float64) + bh) <= 1e-5  # test_admm.cpp:213-227
 
 
-@pytest.mark.parametrize("shape", [(4, 4, 4), (6, 5, 7), (32, 64, 64)])
+@pytest.mark.parametrize("shape", [(4, 4, 4), (6, 5, 7), (32, 64, 64), (64, 128, 16), (128, 128, 8)])
 @pytest.mark.parametrize("order", [1, 2, 3])
 def test_regulariser_energy(ctx, oracle, shape, order):
     w = random_field(shape, 90 + order, 1.0)
