@@ -668,7 +668,15 @@ static cudaError_t launch_reg(const PArgs& a, int mode, int npairs, cudaStream_t
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    k<<<dim3((unsigned)(3 * a.F.hx), (unsigned)npairs), (NY / 8) * (NZ / R1Z), smem, s>>>(a);
+    PArgs b = a;
+    if (b.pf_ahead) {  // one wave of resident CTAs ahead
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, (NY / 8) * (NZ / R1Z), smem);
+        b.pf_ahead = b.pf_ahead * sms * per_sm;
+    }
+    k<<<dim3((unsigned)(3 * a.F.hx), (unsigned)npairs), (NY / 8) * (NZ / R1Z), smem, s>>>(b);
     return cudaGetLastError();
 }
 

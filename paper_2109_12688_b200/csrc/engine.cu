@@ -634,6 +634,9 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     p.scale = (float)(sp.theta / (double)w.geo.N);
     p.lam_n = (float)(sp.lambda * (double)w.geo.N / sp.theta);
     p.n_f = (float)w.geo.N;
+    // plane_reg_kernel L2-prefetches the plane one wave of resident CTAs ahead (-2% time;
+    // an L2 prefetch of the x-pass state instead thrashed L2: +38%)
+    p.pf_ahead = env_int("DREG_PLANE_PF", 1);
     p.order = sp.order;
     p.PY = w.geo.PY;
     p.energy_out = w.energy.p;

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kVT) grad_diff_kernel(VolGeom g, RegBuffers R,
         st->done_iter = -1;
     }
     const long long N = g.N;
-    const float* W = R.WARPED[st->cur] + (size_t)pair * N;
+    const float* W = (st->cur ? R.WARPED[1] : R.WARPED[0]) + (size_t)pair * N;  // no param-array indexing
     const float* T = R.I0 + (size_t)pair * N;
     float* G = F.G + (size_t)pair * 3 * N;
     float* D = F.D + (size_t)pair * N;
@@ -60,41 +60,55 @@ cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, int npair
 }
 
 // ---- compose + warp + SAD + decide -------------------------------------------
-__global__ void __launch_bounds__(kVT) compose_decide_kernel(VolGeom g, RegBuffers R, Fields F, double thr,
-                                                             int max_warps) {
+__device__ __forceinline__ void compose_warp_voxel(const VolGeom& g, const float* __restrict__ phi,
+                                                   const float* __restrict__ V, const float* __restrict__ I1,
+                                                   const float* __restrict__ I0, float* __restrict__ phin,
+                                                   float* __restrict__ wn, long long i, double& sad, double& bad) {
+    const long long N = g.N;
+    int x, y, z;
+    unflat(i, g.M, g.Ny, x, y, z);
+    const float v0 = V[i], v1 = V[N + i], v2 = V[2 * N + i];
+    if (!(isfinite(v0) && isfinite(v1) && isfinite(v2))) bad += 1.0;
+    // compose_deformation: disp'(x) = v(x) + disp(x + v(x))   (volume.cpp:161-181)
+    double s[3];
+    trilinear3(phi, (size_t)N, g.M, g.Ny, g.Nz, x + (double)v0, y + (double)v1, z + (double)v2, s);
+    const float p0 = (float)((double)v0 + s[0]);
+    const float p1 = (float)((double)v1 + s[1]);
+    const float p2 = (float)((double)v2 + s[2]);
+    phin[i] = p0;
+    phin[N + i] = p1;
+    phin[2 * N + i] = p2;
+    // warp_image(level_source, phi_candidate)   (registration.cpp:253)
+    const float w = (float)trilinear(I1, g.M, g.Ny, g.Nz, x + (double)p0, y + (double)p1, z + (double)p2);
+    wn[i] = w;
+    sad += fabs((double)w - (double)I0[i]);  // mean_sad (registration.cpp:145-152)
+}
+
+// Two voxels per loop trip (restrict pointers let their gather chains interleave:
+// the kernel is gather-latency bound).
+__global__ void __launch_bounds__(kVT, 3) compose_decide_kernel(VolGeom g, RegBuffers R, Fields F, double thr,
+                                                                int max_warps) {
     __shared__ double red[32];
     const int pair = blockIdx.y;
     PairState* st = F.st + pair;
     if (!st->active || st->status) return;
     const long long N = g.N;
     const int cur = st->cur;
-    const float* phi = R.PHI[cur] + (size_t)pair * 3 * N;
-    float* phin = R.PHI[cur ^ 1] + (size_t)pair * 3 * N;
-    float* wn = R.WARPED[cur ^ 1] + (size_t)pair * N;
-    const float* I1 = R.I1 + (size_t)pair * N;
-    const float* I0 = R.I0 + (size_t)pair * N;
-    const float* V = F.V + (size_t)pair * 3 * N;
+    // select, not index: a run-time index into the parameter arrays copies them to local memory
+    const float* __restrict__ phi = (cur ? R.PHI[1] : R.PHI[0]) + (size_t)pair * 3 * N;
+    float* __restrict__ phin = (cur ? R.PHI[0] : R.PHI[1]) + (size_t)pair * 3 * N;
+    float* __restrict__ wn = (cur ? R.WARPED[0] : R.WARPED[1]) + (size_t)pair * N;
+    const float* __restrict__ I1 = R.I1 + (size_t)pair * N;
+    const float* __restrict__ I0 = R.I0 + (size_t)pair * N;
+    const float* __restrict__ V = F.V + (size_t)pair * 3 * N;
     double sad = 0.0, bad = 0.0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
-         i += (long long)gridDim.x * blockDim.x) {
-        int x, y, z;
-        unflat(i, g.M, g.Ny, x, y, z);
-        const float v0 = V[i], v1 = V[N + i], v2 = V[2 * N + i];
-        if (!(isfinite(v0) && isfinite(v1) && isfinite(v2))) bad += 1.0;
-        // compose_deformation: disp'(x) = v(x) + disp(x + v(x))   (volume.cpp:161-181)
-        double s[3];
-        trilinear3(phi, (size_t)N, g.M, g.Ny, g.Nz, x + (double)v0, y + (double)v1, z + (double)v2, s);
-        const float p0 = (float)((double)v0 + s[0]);
-        const float p1 = (float)((double)v1 + s[1]);
-        const float p2 = (float)((double)v2 + s[2]);
-        phin[i] = p0;
-        phin[N + i] = p1;
-        phin[2 * N + i] = p2;
-        // warp_image(level_source, phi_candidate)   (registration.cpp:253)
-        const float w = (float)trilinear(I1, g.M, g.Ny, g.Nz, x + (double)p0, y + (double)p1, z + (double)p2);
-        wn[i] = w;
-        sad += fabs((double)w - (double)I0[i]);  // mean_sad (registration.cpp:145-152)
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; i + stride < N; i += 2 * stride) {
+        compose_warp_voxel(g, phi, V, I1, I0, phin, wn, i, sad, bad);
+        compose_warp_voxel(g, phi, V, I1, I0, phin, wn, i + stride, sad, bad);
     }
+    if (i < N) compose_warp_voxel(g, phi, V, I1, I0, phin, wn, i, sad, bad);
     const double vals[2] = {block_sum<kVT>(sad, red), block_sum<kVT>(bad, red)};
     double tot[2];
     if (reduce_partials<kVT, 2>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
@@ -307,7 +321,7 @@ __global__ void __launch_bounds__(kVT) finalize_kernel(VolGeom g, RegBuffers R, 
     PairState* st = F.st + pair;
     if (st->status) return;
     const long long N = g.N;
-    const float* phi = R.PHI[st->cur] + (size_t)pair * 3 * N;
+    const float* phi = (st->cur ? R.PHI[1] : R.PHI[0]) + (size_t)pair * 3 * N;
     const float* src = R.src_in[pair];
     float* po = R.phi_out ? R.phi_out[pair] : nullptr;
     float* wo = R.warped_out ? R.warped_out[pair] : nullptr;

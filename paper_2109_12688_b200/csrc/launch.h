@@ -61,6 +61,7 @@ struct PArgs {
     double lambda64, theta64, scale64;
     float lambda, theta, scale;  // scale = theta / voxels
     float lam_n, n_f;            // lambda N / theta and N: multiplier 1 / (lam_n K + n_f)
+    int pf_ahead;                // plane_reg_kernel: L2-prefetch the plane this many blocks ahead (0 = off)
     int order;
     int PY;             // plane row pitch (complex, odd)
     int k;

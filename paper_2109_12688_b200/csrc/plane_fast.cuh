@@ -263,6 +263,15 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), (NY * NZ <= 8192) ? 3 :
     static_assert(R2Y <= 16 && R2Z <= 16 && (R1Z == 4 || R1Z == 8), "radix split outside rdft<>");
     using Lay = PlaneLayout<NY, R2Y>;
     const int pair = blockIdx.y;
+    if (a.pf_ahead && threadIdx.x == 0) {
+        // L2 prefetch of the plane the CTA starting about one wave later will load
+        // (blocks are dispatched in linear order as resident slots free up)
+        const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x + (unsigned)a.pf_ahead;
+        if (lin < gridDim.x * gridDim.y) {
+            const float2* nxt = a.F.S + (size_t)lin * (size_t)a.F.lines;  // plane index pair*3*hx + c*hx + p
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"((unsigned)(NY * NZ * 8)) : "memory");
+        }
+    }
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
     if (st->solve_done && (!a.need_tail || a.k > st->done_iter)) return;

@@ -16,7 +16,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PROF = os.path.join(ROOT, "profiles")
+PROF = os.environ.get("DREG_PROF_DIR") or os.path.join(ROOT, "profiles")
 
 
 def launches(path):
@@ -57,10 +57,13 @@ def main():
     open(os.path.join(PROF, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
 
     reps = rep.split(",")
-    hdr, units, data = raw(reps[0])
-    for extra in reps[1:]:  # further captures (same metric set) appended
-        h2, _, d2 = raw(extra)
-        data += [[r[h2.index(h)] if h in h2 else "" for h in hdr] for r in d2]
+    hdr, _, _ = raw(reps[0])
+    data, units_of = [], []
+    for r_ in reps:  # every capture keeps its own units row
+        h2, u2, d2 = raw(r_)
+        for row in d2:
+            data.append([row[h2.index(h)] if h in h2 else "" for h in hdr])
+            units_of.append([u2[h2.index(h)] if h in h2 else "" for h in hdr])
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
@@ -68,9 +71,10 @@ def main():
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
     out = [f"# {tag}: ncu --set full (`--clock-control none`) of the per-iteration kernels", "",
-           f"Captured from `python tools/profile_step.py {pairs} 1`; {pairs} config-2 pairs per launch.", ""]
+           f"Captured from `python tools/profile_step.py {pairs} 1`; {pairs} config-2 pairs per launch "
+           "(dram bytes are per launch).", ""]
     dram = {}
-    for r in data:
+    for r, units in zip(data, units_of):
         name = r[hdr.index("Kernel Name")]
         out.append(f"## `{name}`")
         out.append("")
@@ -96,7 +100,7 @@ def main():
                 i = hdr.index(w)
                 v = float(r[i].replace(",", ""))
                 u = units[i]
-                return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
             dram = {"kernel": name, "dram_bytes_per_launch": b("dram__bytes_read.sum") + b("dram__bytes_write.sum"),
                     "pairs": pairs, "source": f"profiles/{tag}_ncu_full.md"}
     open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w").write("\n".join(out) + "\n")

@@ -5,9 +5,12 @@ import csv
 import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
+cut = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+if len(cut) > 1:
+    rows = rows[: cut[1]]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = [r for r in rows[2:] if len(r) == len(hdr) and r[0].startswith("0x")]  # first kernel section
 ix = {h: i for i, h in enumerate(hdr)}
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 tot = {s: 0 for s in stalls}
