@@ -467,8 +467,9 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             st->iterations = a.k + 1;
             st->final_change = change;
             if (change <= a.sp.tol) {
-                st->solve_done = 1;
                 st->done_iter = a.k;
+                __threadfence();
+                st->solve_done = 1;
             }
         }
     }

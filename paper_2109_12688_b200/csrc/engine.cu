@@ -606,6 +606,7 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.fast_x = env_int("DREG_FAST_X", 1);
     a.fx_variant = env_int("DREG_FX", 22);
     a.pipe = env_int("DREG_PIPE", 1);
+    a.pipe_all = env_int("DREG_PIPE_ALL", 0);
     a.fd_lines.init((unsigned)(3 * w.geo.TL));
     return a;
 }
@@ -862,7 +863,7 @@ int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs) {
         auto it = c->wss.find(std::make_tuple(d.x, d.y, d.z));
         if (it != c->wss.end()) fit = std::max<size_t>(fit, (size_t)it->second->P);
     }
-    int P = (int)std::min<size_t>(fit, 32);
+    int P = (int)std::min<size_t>(fit, 64);  // 64 pairs/launch: long persistent x-pass tile ranges
     return std::max(1, std::min(P, n_pairs));
 }
 

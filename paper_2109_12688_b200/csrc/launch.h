@@ -39,6 +39,7 @@ struct XArgs {
     int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
     FastDiv fd_lines;   // divide by 3 * TL
     int pipe;           // warp-specialised persistent x-pass for X_GENERAL, M in {64, 128} (DREG_PIPE: 0 off; default on)
+    int pipe_all;       // A/B knob (DREG_PIPE_ALL): split all pairs' tiles statically, not just the iterating ones
 };
 
 struct PArgs {

@@ -395,8 +395,9 @@ __device__ __forceinline__ void finish_tile(const XArgs& a, int pair, unsigned s
             st->iterations = a.k + 1;
             st->final_change = change;
             if (change <= a.sp.tol) {
-                st->solve_done = 1;
                 st->done_iter = a.k;
+                __threadfence();
+                st->solve_done = 1;
             }
         }
     }
@@ -491,27 +492,54 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
     float2* xtw = twx + L;
     double* red = reinterpret_cast<double*>(xtw + HX + 1);  // [3][NPW]
     static_assert(3 * NPW <= 64, "red[] size");
+    int* plist = reinterpret_cast<int*>(red + 64);  // [npairs] schedulable pairs, ascending
     __shared__ int tile_of[NB];
+    __shared__ int s_np;
+    // Only the pairs still iterating are spread over the grid (pairs stop at different
+    // warps; a static split over all pairs would leave the CTAs of finished pairs idle
+    // while the rest do full work).  The predicate uses flags that cannot change during
+    // this launch: a solve_done raised by this launch carries done_iter == k (written
+    // first, fenced), so every CTA derives the same list.
+    if (threadIdx.x < 32) {
+        int n = 0;
+        for (int p0 = 0; p0 < npairs; p0 += 32) {
+            const int p = p0 + (int)threadIdx.x;
+            bool ok = false;
+            if (p < npairs) {
+                const volatile PairState* st = a.F.st + p;
+                ok = a.pipe_all || (st->active && !st->status);  // pipe_all: A/B knob, static split
+                if (ok && !a.pipe_all && st->solve_done) {
+                    __threadfence();
+                    ok = st->done_iter >= a.k;
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (ok) plist[n + __popc(m & ((1u << threadIdx.x) - 1u))] = p;
+            n += __popc(m);
+        }
+        if (threadIdx.x == 0) s_np = n;
+    }
+    __syncthreads();
     const long long lines = a.F.lines;
     const int T = tiles_per_pair;
-    const int total = T * npairs;
+    const int total = T * s_np;  // tiles in schedulable-slot order: slot-major
     const int G = gridDim.x;
-    // contiguous tile range of this CTA (global order: pair-major)
+    // contiguous tile range of this CTA
     auto range_start = [&](int cta) { return (int)(((long long)cta * total) / G); };
     const int g_end = range_start(blockIdx.x + 1);
     const bool fft_group = threadIdx.x < NF;
     const int tid = fft_group ? (int)threadIdx.x : (int)threadIdx.x - NF;
     auto runnable_from = [&](int g) {  // pair flags are stable while any of its tiles is pending
         while (g < g_end) {
-            const int pair = g / T;
-            const PairState* st = a.F.st + pair;
+            const int slot = g / T;
+            const PairState* st = a.F.st + plist[slot];
             if (st->active && !st->status && !st->solve_done) return g;
-            g = (pair + 1) * T;
+            g = (slot + 1) * T;
         }
         return -1;
     };
     auto stage = [&](int g, float2* buf) {
-        const int pair = g / T, tile = g - pair * T;
+        const int pair = plist[g / T], tile = g - (g / T) * T;
         const long long L0 = (long long)tile * TL;
         const int nl = (int)min((long long)TL, lines - L0);
         stage_spectrum<R2, float2, NF>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
@@ -541,7 +569,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             if (prev >= 0) {
                 const int pb = (i + NB - 1) % NB;
                 ring_bar<kBarU, NALL, false>(pb);
-                const int pair = prev / T, tile = prev - pair * T;
+                const int pair = plist[prev / T], tile = prev - (prev / T) * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
                 if (!(a.dbg_skip & 1))
@@ -563,7 +591,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             ring_bar<kBarW, NALL, false>(b);
             const int cur = tile_of[b];
             if (cur < 0) break;
-            const int pair = cur / T, tile = cur - pair * T;
+            const int slot = cur / T, pair = plist[slot], tile = cur - slot * T;
             const long long L0 = (long long)tile * TL;
             const int nl = (int)min((long long)TL, lines - L0);
             float fc = 0.f, fr = 0.f, fo = 0.f;
@@ -608,7 +636,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
                     __threadfence();
                     // runs of this pair, in CTA order: deterministic sum
                     double tot[3] = {0.0, 0.0, 0.0};
-                    const int p0 = pair * T;
+                    const int p0 = slot * T;
                     for (int c = 0; c < G; ++c) {
                         const int s0 = max(range_start(c), p0), s1 = min(range_start(c + 1), p0 + T);
                         if (s0 >= s1) continue;
@@ -627,8 +655,9 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
                     st->iterations = a.k + 1;
                     st->final_change = change;
                     if (change <= a.sp.tol) {
+                        st->done_iter = a.k;  // before the flag: see the schedulable-pair scan
+                        __threadfence();
                         st->solve_done = 1;
-                        st->done_iter = a.k;
                     }
                 }
             }
@@ -677,7 +706,8 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
 template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0>
 static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
     constexpr int L = kR1 * R2, NB = 3;
-    const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 64;
+    const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 64 +
+                        sizeof(int) * (size_t)npairs;
     void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

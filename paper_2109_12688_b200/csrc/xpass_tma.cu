@@ -285,8 +285,9 @@ __global__ void __launch_bounds__(kTThreads, 1) xpass_tma_kernel(XArgs a, int np
                 st->iterations = a.k + 1;
                 st->final_change = change;
                 if (change <= a.sp.tol) {
-                    st->solve_done = 1;
                     st->done_iter = a.k;
+                    __threadfence();
+                    st->solve_done = 1;
                 }
             }
         }

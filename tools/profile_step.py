@@ -20,6 +20,8 @@ F, M = synth.make_batch(3, 1000, B, shape)
 cfg = synth.config_cfg("config3")
 cfg.max_warps_per_level[0] = K
 with dreg.Context(0) as ctx:
+    if os.environ.get("DREG_CHUNK"):  # pairs per device launch (default: auto)
+        ctx.set_batch_chunk(int(os.environ["DREG_CHUNK"]))
     phis, warps, res = ctx.register_batch(list(F), list(M), cfg, want_phi=False, want_warped=False)
     if os.environ.get("DREG_DBG_SKIP_TK"):  # timing-only knob for the kernel loop (not the registration)
         os.environ["DREG_DBG_SKIP"] = os.environ["DREG_DBG_SKIP_TK"]
