@@ -234,6 +234,34 @@ class CpuLib:
         self._check(self._g("upsample_velocity")(_fp(v), abi.dims3(v), dd, _fp(out)))
         return out
 
+    # ---- reference-only helpers (oracle/_ref): the reference's synthetic cases ----
+    def make_case(self, kind: str, shape, shift=(0.0, 0.0, 0.0), seed: int = 0):
+        """synth.hpp make_translate_case / make_sphere_ellipsoid_case / make_random_smooth_case
+        -> (target, source, target_labels, source_labels), arrays (z, y, x)."""
+        if self.kind != "reference":
+            raise RuntimeError("make_case needs the reference library")
+        k = {"translate": 0, "sphere_ellipsoid": 1, "random_smooth": 2}[kind]
+        t, s = np.zeros(shape, np.float32), np.zeros(shape, np.float32)
+        tl, sl = np.zeros(shape, np.uint16), np.zeros(shape, np.uint16)
+        sh = (C.c_double * 3)(*shift)
+        u16 = C.POINTER(C.c_ushort)
+        f = self.lib.ref_make_case
+        f.argtypes = [C.c_int, abi.Dims3, C.POINTER(C.c_double), C.c_uint, _F, _F, u16, u16]
+        self._check(f(k, abi.dims3(t), sh, seed, _fp(t), _fp(s), tl.ctypes.data_as(u16), sl.ctypes.data_as(u16)))
+        return t, s, tl, sl
+
+    def warped_label_dice(self, moving_labels, disp, fixed_labels, label: int = 1) -> float:
+        """metrics.hpp:31,39: dice(warp_labels(moving, phi), fixed, label)."""
+        u16 = C.POINTER(C.c_ushort)
+        m = np.ascontiguousarray(moving_labels, np.uint16)
+        fx = np.ascontiguousarray(fixed_labels, np.uint16)
+        disp = _f32(disp)
+        out = C.c_double()
+        f = self.lib.ref_warped_label_dice
+        f.argtypes = [u16, _F, u16, abi.Dims3, C.c_int, C.POINTER(C.c_double)]
+        self._check(f(m.ctypes.data_as(u16), _fp(disp), fx.ctypes.data_as(u16), abi.dims3(m), label, C.byref(out)))
+        return out.value
+
     def register_pair(self, target, source, cfg: abi.RegCfg, spacing=(1.0, 1.0, 1.0)):
         target, source = _f32(target), _f32(source)
         phi = np.zeros(target.shape + (3,), np.float32)

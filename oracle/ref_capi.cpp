@@ -20,6 +20,7 @@
 #include "dreg/parallel.hpp"
 #include "dreg/registration.hpp"
 #include "dreg/regularizer.hpp"
+#include "dreg/synth.hpp"
 #include "dreg/volume.hpp"
 #include "dreg_cuda.h"
 
@@ -285,6 +286,37 @@ int ref_register_pair(const float* target, const float* source, dreg_dims3 d,
             }
             res->elapsed_seconds = r.elapsed_seconds;
         }
+    });
+}
+
+// The reference's own synthetic cases (synth.hpp), for restating its registration and
+// acceptance tests on identical inputs: kind 0 translate (shift), 1 sphere->ellipsoid,
+// 2 random smooth (seed).  Labels are uint16 as in LabelVolume (nullable).
+int ref_make_case(int kind, dreg_dims3 d, const double* shift, unsigned seed, float* target, float* source,
+                  unsigned short* target_labels, unsigned short* source_labels) {
+    return guard([&] {
+        dreg::SynthPair p;
+        if (kind == 0) p = dreg::make_translate_case(D(d), dreg::Vec3{shift[0], shift[1], shift[2]});
+        else if (kind == 1) p = dreg::make_sphere_ellipsoid_case(D(d));
+        else p = dreg::make_random_smooth_case(D(d), seed);
+        std::memcpy(target, p.target.data.data(), sizeof(float) * p.target.data.size());
+        std::memcpy(source, p.source.data.data(), sizeof(float) * p.source.data.size());
+        if (target_labels)
+            std::memcpy(target_labels, p.target_labels.labels.data(), 2 * p.target_labels.labels.size());
+        if (source_labels)
+            std::memcpy(source_labels, p.source_labels.labels.data(), 2 * p.source_labels.labels.size());
+    });
+}
+
+// dice(warp_labels(moving, phi), fixed, label)   (metrics.hpp:31,39)
+int ref_warped_label_dice(const unsigned short* moving, const float* disp, const unsigned short* fixed, dreg_dims3 d,
+                          int label, double* out) {
+    return guard([&] {
+        dreg::LabelVolume mv(D(d), {1.0, 1.0, 1.0}), fx(D(d), {1.0, 1.0, 1.0});
+        std::memcpy(mv.labels.data(), moving, 2 * mv.labels.size());
+        std::memcpy(fx.labels.data(), fixed, 2 * fx.labels.size());
+        const auto w = dreg::warp_labels(mv, dreg::make_deformation(vec(disp, d)));
+        *out = dreg::dice(w, fx, label);
     });
 }
 

