@@ -13,11 +13,15 @@
 
 #include <cmath>
 #include <cstddef>
+#include <cstdint>
 #include <cstring>
+#include <filesystem>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "dreg_cuda.h"
@@ -170,6 +174,66 @@ struct JacobianStats {
     double pct_nonpositive = 0.0;
     double min_det = 0.0;
 };
+
+/// Integer segmentation labels, x-fastest, 0 = background (metrics.hpp:12-29).
+struct LabelVolume {
+    Dims3 dims;
+    Spacing3 spacing;
+    std::vector<std::uint16_t> labels;
+    LabelVolume() = default;
+    LabelVolume(Dims3 d, Spacing3 s, std::uint16_t fill = 0) : dims(d), spacing(s) {
+        if (d.x < 1 || d.y < 1 || d.z < 1) throw std::invalid_argument("label volume dims must be positive");
+        if (!(s.x > 0.0) || !(s.y > 0.0) || !(s.z > 0.0))
+            throw std::invalid_argument("label volume spacing must be positive");
+        labels.assign(d.voxels(), fill);
+    }
+    [[nodiscard]] std::size_t index(int x, int y, int z) const {
+        return static_cast<std::size_t>(x) + static_cast<std::size_t>(dims.x) *
+                                                 (static_cast<std::size_t>(y) + static_cast<std::size_t>(dims.y) *
+                                                                                    static_cast<std::size_t>(z));
+    }
+    [[nodiscard]] std::uint16_t at(int x, int y, int z) const { return labels[index(x, y, z)]; }
+    std::uint16_t& at(int x, int y, int z) { return labels[index(x, y, z)]; }
+};
+
+// ---- io.hpp --------------------------------------------------------------------------
+enum class VolumeKind : std::uint8_t { scalar = 0, vector = 1, label = 2 };
+using AnyVolume = std::variant<ScalarVolume, VectorField, LabelVolume>;
+
+struct ReportConfig {
+    std::string data_term;
+    int order = 0;
+    double lambda = 0.0;
+    double theta = 0.0;
+    int levels = 0;
+    std::string profile;
+    double tol = 0.0;
+    double warp_improvement_threshold = 0.0;
+    double epsilon = 0.0;
+    int threads = 1;
+};
+
+struct RunReport {
+    std::map<int, double> dice;
+    std::map<int, double> hausdorff_mm;
+    double jacobian_pct_nonpositive = 0.0;
+    double runtime_seconds = 0.0;
+    int velocity_count = 0;
+    ReportConfig config;
+};
+
+// ---- parallel.hpp ---------------------------------------------------------------------
+// The reference's CPU worker count.  The GPU path's results never depend on it; it is
+// kept so callers (and the run report's config echo) see the value they set.
+inline int& b200_thread_slot() {
+    static int n = 1;
+    return n;
+}
+inline void set_thread_count(int n) {
+    if (n < 1) throw std::invalid_argument("thread count must be >= 1");
+    b200_thread_slot() = n;
+}
+inline int thread_count() { return b200_thread_slot(); }
 
 // =================================== implementation ==================================
 namespace b200_detail {
@@ -467,6 +531,109 @@ inline VectorField upsample_velocity(const VectorField& v, Dims3 target_dims) {
 
 inline DeformationField upsample_deformation(const DeformationField& phi, Dims3 target_dims) {
     return {upsample_velocity(phi.disp, target_dims)};
+}
+
+// ---- io.hpp (host file I/O through the C ABI; byte-compatible) -------------------------
+namespace b200_detail {
+inline void io_check(int st, const char* err) {
+    if (st == DREG_OK) return;
+    if (st == DREG_IO_ERROR) throw io_error(err);
+    if (st == DREG_INVALID_ARGUMENT) throw std::invalid_argument(err);
+    throw std::runtime_error(err);
+}
+inline AnyVolume read_any(const std::filesystem::path& path, int expected_kind) {
+    char err[1024];
+    dreg_volume_info info;
+    const std::string p = path.string();
+    io_check(dreg_volume_read(p.c_str(), expected_kind, &info, nullptr, 0, err, sizeof err), err);
+    const Dims3 d{info.dims.x, info.dims.y, info.dims.z};
+    const Spacing3 sp{info.spacing.x, info.spacing.y, info.spacing.z};
+    if (info.kind == DREG_KIND_LABEL) {
+        LabelVolume v(d, sp);
+        io_check(dreg_volume_read(p.c_str(), expected_kind, &info, v.labels.data(), 2 * v.labels.size(), err,
+                                  sizeof err), err);
+        return v;
+    }
+    if (info.kind == DREG_KIND_VECTOR) {
+        VectorField v(d, sp);
+        io_check(dreg_volume_read(p.c_str(), expected_kind, &info, v.data.data(), 4 * v.data.size(), err, sizeof err),
+                 err);
+        return v;
+    }
+    ScalarVolume v(d, sp);
+    io_check(dreg_volume_read(p.c_str(), expected_kind, &info, v.data.data(), 4 * v.data.size(), err, sizeof err),
+             err);
+    return v;
+}
+inline void write_any(const std::filesystem::path& path, int kind, Dims3 d, Spacing3 s, const void* payload) {
+    char err[1024];
+    io_check(dreg_volume_write(path.string().c_str(), kind, D(d), {s.x, s.y, s.z}, payload, err, sizeof err), err);
+}
+}  // namespace b200_detail
+
+inline AnyVolume read_volume(const std::filesystem::path& path) { return b200_detail::read_any(path, -1); }
+inline ScalarVolume read_scalar(const std::filesystem::path& path) {
+    return std::get<ScalarVolume>(b200_detail::read_any(path, DREG_KIND_SCALAR));
+}
+inline VectorField read_vector(const std::filesystem::path& path) {
+    return std::get<VectorField>(b200_detail::read_any(path, DREG_KIND_VECTOR));
+}
+inline LabelVolume read_label(const std::filesystem::path& path) {
+    return std::get<LabelVolume>(b200_detail::read_any(path, DREG_KIND_LABEL));
+}
+inline DeformationField read_deformation(const std::filesystem::path& path) { return {read_vector(path)}; }
+
+inline void write_volume(const std::filesystem::path& path, const ScalarVolume& v) {
+    b200_detail::write_any(path, DREG_KIND_SCALAR, v.dims, v.spacing, v.data.data());
+}
+inline void write_volume(const std::filesystem::path& path, const VectorField& v) {
+    b200_detail::write_any(path, DREG_KIND_VECTOR, v.dims, v.spacing, v.data.data());
+}
+inline void write_volume(const std::filesystem::path& path, const LabelVolume& v) {
+    b200_detail::write_any(path, DREG_KIND_LABEL, v.dims, v.spacing, v.labels.data());
+}
+inline void write_volume(const std::filesystem::path& path, const DeformationField& phi) {
+    write_volume(path, phi.disp);
+}
+
+inline void write_report(const std::filesystem::path& path, const RunReport& r) {
+    std::vector<int> dl, hl;
+    std::vector<double> dv, hv;
+    for (const auto& [k, v] : r.dice) dl.push_back(k), dv.push_back(v);
+    for (const auto& [k, v] : r.hausdorff_mm) hl.push_back(k), hv.push_back(v);
+    const ReportConfig& c = r.config;
+    dreg_run_report rep{static_cast<int>(dl.size()), dl.data(), dv.data(), static_cast<int>(hl.size()), hl.data(),
+                        hv.data(), r.jacobian_pct_nonpositive, r.runtime_seconds, r.velocity_count,
+                        {c.data_term.c_str(), c.order, c.lambda, c.theta, c.levels, c.profile.c_str(), c.tol,
+                         c.warp_improvement_threshold, c.epsilon, c.threads}};
+    char err[1024];
+    b200_detail::io_check(dreg_report_write(path.string().c_str(), &rep, err, sizeof err), err);
+}
+
+// ---- metrics.hpp label metrics (GPU) --------------------------------------------------
+inline double dice(const LabelVolume& a, const LabelVolume& b, int label) {
+    b200_detail::same(a.dims, b.dims, "dice");
+    double out = 0.0;
+    b200_detail::check(dreg_cuda_dice(b200_detail::ctx(), a.labels.data(), b.labels.data(), b200_detail::D(a.dims),
+                                      label, &out));
+    return out;
+}
+
+inline double hausdorff_slice_avg(const LabelVolume& a, const LabelVolume& b, int label) {
+    b200_detail::same(a.dims, b.dims, "hausdorff_slice_avg");
+    double out = 0.0;
+    b200_detail::check(dreg_cuda_hausdorff_slice_avg(b200_detail::ctx(), a.labels.data(), b.labels.data(),
+                                                     b200_detail::D(a.dims),
+                                                     {a.spacing.x, a.spacing.y, a.spacing.z}, label, &out));
+    return out;
+}
+
+inline LabelVolume warp_labels(const LabelVolume& lbl, const DeformationField& phi) {
+    b200_detail::same(lbl.dims, phi.disp.dims, "warp_labels");
+    LabelVolume out(lbl.dims, lbl.spacing);
+    b200_detail::check(dreg_cuda_warp_labels(b200_detail::ctx(), lbl.labels.data(), phi.disp.data.data(),
+                                             b200_detail::D(lbl.dims), out.labels.data()));
+    return out;
 }
 
 }  // namespace dreg

@@ -15,6 +15,7 @@
  *
  * Status codes (no exceptions cross the ABI; the C++ mirror rethrows):
  *   DREG_OK 0, DREG_INVALID_ARGUMENT 2  -> std::invalid_argument
+ *             DREG_IO_ERROR 3           -> dreg::io_error        (errors.hpp; file I/O only)
  *             DREG_NUMERIC 4            -> dreg::numeric_error   (errors.hpp:15-17)
  *             DREG_RUNTIME 5            -> std::runtime_error (CUDA / allocation)
  *
@@ -35,6 +36,7 @@ extern "C" {
 
 #define DREG_OK 0
 #define DREG_INVALID_ARGUMENT 2
+#define DREG_IO_ERROR 3
 #define DREG_NUMERIC 4
 #define DREG_RUNTIME 5
 
@@ -181,6 +183,77 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* ctx, const float* target,
  * events on the context stream.  out[0] = x-pass ms/launch, out[1] = plane ms/launch,
  * out[2] / out[3] = their algorithmic HBM bytes per launch, out[4] = pairs per launch. */
 int dreg_cuda_time_kernels(dreg_cuda_ctx* ctx, int reps, double* out);
+
+/* ---- DREG volume container (io.hpp:15-41; README.md:99-114) ---------------------
+ * Host-only file I/O, byte-compatible with the reference.  Status DREG_IO_ERROR with
+ * the reference's message in `err` (nullable, err_len bytes incl. NUL) on failure. */
+#define DREG_KIND_SCALAR 0
+#define DREG_KIND_VECTOR 1
+#define DREG_KIND_LABEL 2
+typedef struct {
+    int kind;               /* DREG_KIND_* */
+    dreg_dims3 dims;
+    dreg_spacing3 spacing;
+} dreg_volume_info;
+/* Header of `path` (validated like read_volume, io.cpp:88-130). */
+int dreg_volume_info_read(const char* path, dreg_volume_info* out, char* err, size_t err_len);
+/* read_volume / read_scalar / read_vector / read_label (io.hpp:27-35): the whole file
+ * is validated (length, finiteness); expected_kind -1 accepts any kind.  payload gets
+ * f32 (scalar voxels / vector 3*voxels interleaved) or u16 (label) words; capacity in
+ * bytes.  payload may be NULL to validate only. */
+int dreg_volume_read(const char* path, int expected_kind, dreg_volume_info* info, void* payload,
+                     size_t capacity, char* err, size_t err_len);
+/* write_volume (io.hpp:37-40) */
+int dreg_volume_write(const char* path, int kind, dreg_dims3 dims, dreg_spacing3 spacing,
+                      const void* payload, char* err, size_t err_len);
+
+/* dreg::ReportConfig / RunReport (io.hpp:43-62); label maps as parallel arrays. */
+typedef struct {
+    const char* data_term;  /* "l1" | "l2" */
+    int order;
+    double lambda;
+    double theta;
+    int levels;
+    const char* profile;    /* "capped" | "converged" */
+    double tol;
+    double warp_improvement_threshold;
+    double epsilon;
+    int threads;
+} dreg_report_config;
+typedef struct {
+    int n_dice;
+    const int* dice_labels;
+    const double* dice;
+    int n_hausdorff;
+    const int* hausdorff_labels;
+    const double* hausdorff_mm;
+    double jacobian_pct_nonpositive;
+    double runtime_seconds;
+    int velocity_count;
+    dreg_report_config config;
+} dreg_run_report;
+/* write_report (io.hpp:64-66): same keys, order, 6 significant digits, 2-space JSON. */
+int dreg_report_write(const char* path, const dreg_run_report* report, char* err, size_t err_len);
+
+/* ---- label metrics (metrics.hpp:31-42), GPU ---------------------------------------
+ * Label volumes are u16, x-fastest.  warp_labels: nearest-neighbour (lround, clamp)
+ * lookup at x + disp(x), disp AoS.  dice: 2|A∩B|/(|A|+|B|), 1 when both are empty.
+ * hausdorff: per z-slice exact anisotropic EDT (in-plane spacing) symmetric
+ * Hausdorff, averaged over slices where both masks are non-empty;
+ * DREG_INVALID_ARGUMENT when no slice contributes. */
+int dreg_cuda_warp_labels(dreg_cuda_ctx* ctx, const uint16_t* labels, const float* disp,
+                          dreg_dims3 dims, uint16_t* out);
+int dreg_cuda_dice(dreg_cuda_ctx* ctx, const uint16_t* a, const uint16_t* b, dreg_dims3 dims,
+                   int label, double* out);
+int dreg_cuda_hausdorff_slice_avg(dreg_cuda_ctx* ctx, const uint16_t* a, const uint16_t* b,
+                                  dreg_dims3 dims, dreg_spacing3 spacing, int label, double* out);
+/* All labels in one upload: dice_out[i], hausdorff_out[i] for labels[i];
+ * hausdorff_valid[i] = 0 where no slice carries labels[i] in both volumes
+ * (hausdorff_out[i] is then NaN).  Any output may be NULL. */
+int dreg_cuda_label_metrics(dreg_cuda_ctx* ctx, const uint16_t* a, const uint16_t* b,
+                            dreg_dims3 dims, dreg_spacing3 spacing, int n_labels,
+                            const int* labels, double* dice_out, double* hausdorff_out,
+                            int* hausdorff_valid);
 
 /* ---- building blocks (host AoS buffers; each a GPU launch) ---------------------- */
 /* v_update_l1 / v_update_l2 (admm.hpp:49-58); data_term selects which */

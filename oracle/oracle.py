@@ -262,6 +262,73 @@ class CpuLib:
         self._check(f(m.ctypes.data_as(u16), _fp(disp), fx.ctypes.data_as(u16), abi.dims3(m), label, C.byref(out)))
         return out.value
 
+    # ---- reference-only: label metrics, DREG files, reports, salt-and-pepper ------
+    def _ref(self):
+        if self.kind != "reference":
+            raise RuntimeError("needs the reference library (oracle/_ref)")
+        return self.lib
+
+    def add_salt_pepper(self, vol, fraction: float, seed: int) -> np.ndarray:
+        """synth.hpp add_salt_pepper on a copy of vol."""
+        v = _f32(vol).copy()
+        f = self._ref().ref_add_salt_pepper
+        f.argtypes = [_F, abi.Dims3, C.c_double, C.c_uint]
+        self._check(f(_fp(v), abi.dims3(v), fraction, seed))
+        return v
+
+    def dice(self, a, b, label: int) -> float:
+        a, b = np.ascontiguousarray(a, np.uint16), np.ascontiguousarray(b, np.uint16)
+        f = self._ref().ref_dice
+        f.argtypes = [C.c_void_p, C.c_void_p, abi.Dims3, C.c_int, _D]
+        out = C.c_double()
+        self._check(f(a.ctypes.data, b.ctypes.data, abi.dims3(a), label, C.byref(out)))
+        return out.value
+
+    def hausdorff_slice_avg(self, a, b, label: int, spacing=(1.0, 1.0, 1.0)) -> float:
+        a, b = np.ascontiguousarray(a, np.uint16), np.ascontiguousarray(b, np.uint16)
+        f = self._ref().ref_hausdorff_slice_avg
+        f.argtypes = [C.c_void_p, C.c_void_p, abi.Dims3, abi.Spacing3, C.c_int, _D]
+        out = C.c_double()
+        self._check(f(a.ctypes.data, b.ctypes.data, abi.dims3(a), abi.Spacing3(*spacing), label, C.byref(out)))
+        return out.value
+
+    def warp_labels(self, labels, disp) -> np.ndarray:
+        lbl = np.ascontiguousarray(labels, np.uint16)
+        disp = _f32(disp)
+        out = np.empty_like(lbl)
+        f = self._ref().ref_warp_labels
+        f.argtypes = [C.c_void_p, _F, abi.Dims3, C.c_void_p]
+        self._check(f(lbl.ctypes.data, _fp(disp), abi.dims3(lbl), out.ctypes.data))
+        return out
+
+    def write_volume(self, path, data, spacing=(1.0, 1.0, 1.0), kind: str | None = None) -> None:
+        a = np.asarray(data)
+        if kind is None:
+            kind = "label" if a.dtype == np.uint16 else ("vector" if a.ndim == 4 else "scalar")
+        k = {"scalar": 0, "vector": 1, "label": 2}[kind]
+        a = np.ascontiguousarray(a, np.uint16 if k == 2 else np.float32)
+        f = self._ref().ref_write_volume
+        f.argtypes = [C.c_char_p, C.c_int, abi.Dims3, abi.Spacing3, C.c_void_p]
+        self._check(f(os.fsencode(str(path)), k, abi.dims3(a), abi.Spacing3(*spacing), a.ctypes.data))
+
+    def read_volume(self, path, expected_kind: int = -1):
+        """(kind, array, spacing) like paper_2109_12688_b200.dreg.read_volume."""
+        L = self._ref()
+        f = L.ref_read_volume
+        f.argtypes = [C.c_char_p, C.c_int, C.POINTER(abi.VolumeInfo), C.c_void_p, C.c_size_t]
+        info = abi.VolumeInfo()
+        p = os.fsencode(str(path))
+        self._check(f(p, expected_kind, C.byref(info), None, 0))
+        shape = info.dims.shape() + ((3,) if info.kind == 1 else ())
+        out = np.empty(shape, np.uint16 if info.kind == 2 else np.float32)
+        self._check(f(p, expected_kind, C.byref(info), out.ctypes.data, out.nbytes))
+        return info.kind, out, (info.spacing.x, info.spacing.y, info.spacing.z)
+
+    def write_report(self, path, report: abi.RunReport) -> None:
+        f = self._ref().ref_write_report
+        f.argtypes = [C.c_char_p, C.POINTER(abi.RunReport)]
+        self._check(f(os.fsencode(str(path)), C.byref(report)))
+
     def register_pair(self, target, source, cfg: abi.RegCfg, spacing=(1.0, 1.0, 1.0)):
         target, source = _f32(target), _f32(source)
         phi = np.zeros(target.shape + (3,), np.float32)

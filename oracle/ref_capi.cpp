@@ -12,10 +12,13 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
+#include <variant>
 #include <vector>
 
 #include "dreg/admm.hpp"
 #include "dreg/errors.hpp"
+#include "dreg/io.hpp"
 #include "dreg/metrics.hpp"
 #include "dreg/parallel.hpp"
 #include "dreg/registration.hpp"
@@ -67,6 +70,9 @@ int guard(F&& f) {
     } catch (const dreg::numeric_error& e) {
         g_err = e.what();
         return DREG_NUMERIC;
+    } catch (const dreg::io_error& e) {
+        g_err = e.what();
+        return DREG_IO_ERROR;
     } catch (const std::exception& e) {
         g_err = e.what();
         return DREG_RUNTIME;
@@ -317,6 +323,95 @@ int ref_warped_label_dice(const unsigned short* moving, const float* disp, const
         std::memcpy(fx.labels.data(), fixed, 2 * fx.labels.size());
         const auto w = dreg::warp_labels(mv, dreg::make_deformation(vec(disp, d)));
         *out = dreg::dice(w, fx, label);
+    });
+}
+
+// add_salt_pepper (synth.hpp) on a scalar volume, in place.
+int ref_add_salt_pepper(float* vol, dreg_dims3 d, double fraction, unsigned seed) {
+    return guard([&] {
+        auto v = scalar(vol, d);
+        dreg::add_salt_pepper(v, fraction, seed);
+        std::memcpy(vol, v.data.data(), sizeof(float) * v.data.size());
+    });
+}
+
+dreg::LabelVolume labels_of(const unsigned short* p, dreg_dims3 d, dreg_spacing3 s) {
+    dreg::LabelVolume v(D(d), {s.x, s.y, s.z});
+    std::memcpy(v.labels.data(), p, 2 * v.labels.size());
+    return v;
+}
+
+// dice / hausdorff_slice_avg / warp_labels (metrics.hpp:31-42)
+int ref_dice(const unsigned short* a, const unsigned short* b, dreg_dims3 d, int label, double* out) {
+    return guard([&] { *out = dreg::dice(labels_of(a, d, {1, 1, 1}), labels_of(b, d, {1, 1, 1}), label); });
+}
+int ref_hausdorff_slice_avg(const unsigned short* a, const unsigned short* b, dreg_dims3 d, dreg_spacing3 s,
+                            int label, double* out) {
+    return guard([&] { *out = dreg::hausdorff_slice_avg(labels_of(a, d, s), labels_of(b, d, s), label); });
+}
+int ref_warp_labels(const unsigned short* lbl, const float* disp, dreg_dims3 d, unsigned short* out) {
+    return guard([&] {
+        const auto w = dreg::warp_labels(labels_of(lbl, d, {1, 1, 1}), dreg::make_deformation(vec(disp, d)));
+        std::memcpy(out, w.labels.data(), 2 * w.labels.size());
+    });
+}
+
+// write_volume / read_volume (io.hpp:27-40) on raw payloads
+int ref_write_volume(const char* path, int kind, dreg_dims3 d, dreg_spacing3 s, const void* payload) {
+    return guard([&] {
+        const dreg::Spacing3 sp{s.x, s.y, s.z};
+        if (kind == 0) {
+            dreg::ScalarVolume v(D(d), sp);
+            std::memcpy(v.data.data(), payload, 4 * v.data.size());
+            dreg::write_volume(path, v);
+        } else if (kind == 1) {
+            dreg::VectorField v(D(d), sp);
+            std::memcpy(v.data.data(), payload, 4 * v.data.size());
+            dreg::write_volume(path, v);
+        } else {
+            dreg::LabelVolume v(D(d), sp);
+            std::memcpy(v.labels.data(), payload, 2 * v.labels.size());
+            dreg::write_volume(path, v);
+        }
+    });
+}
+// expected_kind: -1 read_volume, 0 read_scalar, 1 read_vector, 2 read_label
+int ref_read_volume(const char* path, int expected_kind, dreg_volume_info* info, void* payload, size_t cap) {
+    return guard([&] {
+        dreg::AnyVolume any;
+        if (expected_kind == 0) any = dreg::read_scalar(path);
+        else if (expected_kind == 1) any = dreg::read_vector(path);
+        else if (expected_kind == 2) any = dreg::read_label(path);
+        else any = dreg::read_volume(path);
+        std::visit(
+            [&](const auto& v) {
+                using T = std::decay_t<decltype(v)>;
+                info->dims = {v.dims.x, v.dims.y, v.dims.z};
+                info->spacing = {v.spacing.x, v.spacing.y, v.spacing.z};
+                if constexpr (std::is_same_v<T, dreg::LabelVolume>) {
+                    info->kind = 2;
+                    if (payload && cap >= 2 * v.labels.size()) std::memcpy(payload, v.labels.data(), 2 * v.labels.size());
+                } else {
+                    info->kind = std::is_same_v<T, dreg::ScalarVolume> ? 0 : 1;
+                    if (payload && cap >= 4 * v.data.size()) std::memcpy(payload, v.data.data(), 4 * v.data.size());
+                }
+            },
+            any);
+    });
+}
+// write_report (io.hpp:64-66)
+int ref_write_report(const char* path, const dreg_run_report* r) {
+    return guard([&] {
+        dreg::RunReport rep;
+        for (int i = 0; i < r->n_dice; ++i) rep.dice[r->dice_labels[i]] = r->dice[i];
+        for (int i = 0; i < r->n_hausdorff; ++i) rep.hausdorff_mm[r->hausdorff_labels[i]] = r->hausdorff_mm[i];
+        rep.jacobian_pct_nonpositive = r->jacobian_pct_nonpositive;
+        rep.runtime_seconds = r->runtime_seconds;
+        rep.velocity_count = r->velocity_count;
+        const dreg_report_config& c = r->config;
+        rep.config = {c.data_term, c.order, c.lambda, c.theta, c.levels, c.profile,
+                      c.tol, c.warp_improvement_threshold, c.epsilon, c.threads};
+        dreg::write_report(path, rep);
     });
 }
 

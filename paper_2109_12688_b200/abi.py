@@ -9,11 +9,16 @@ import ctypes as C
 
 DREG_OK = 0
 DREG_INVALID_ARGUMENT = 2
+DREG_IO_ERROR = 3
 DREG_NUMERIC = 4
 DREG_RUNTIME = 5
 
 DREG_MAX_LEVELS = 8
 DREG_MAX_WARPS = 64
+
+DREG_KIND_SCALAR = 0
+DREG_KIND_VECTOR = 1
+DREG_KIND_LABEL = 2
 
 DREG_PROFILE_CAPPED = 0
 DREG_PROFILE_CONVERGED = 1
@@ -113,6 +118,46 @@ class JacobianStats(C.Structure):
         ("min_det", C.c_double),
         ("nonpositive", C.c_int64),
         ("interior", C.c_int64),
+    ]
+
+
+class VolumeInfo(C.Structure):
+    """DREG container header (io.hpp:15-22): kind, dims, spacing."""
+
+    _fields_ = [("kind", C.c_int), ("dims", Dims3), ("spacing", Spacing3)]
+
+
+class ReportConfig(C.Structure):
+    """dreg::ReportConfig (io.hpp:43-54)."""
+
+    _fields_ = [
+        ("data_term", C.c_char_p),
+        ("order", C.c_int),
+        ("lambda_", C.c_double),
+        ("theta", C.c_double),
+        ("levels", C.c_int),
+        ("profile", C.c_char_p),
+        ("tol", C.c_double),
+        ("warp_improvement_threshold", C.c_double),
+        ("epsilon", C.c_double),
+        ("threads", C.c_int),
+    ]
+
+
+class RunReport(C.Structure):
+    """dreg::RunReport (io.hpp:56-62); label maps as parallel arrays."""
+
+    _fields_ = [
+        ("n_dice", C.c_int),
+        ("dice_labels", C.POINTER(C.c_int)),
+        ("dice", C.POINTER(C.c_double)),
+        ("n_hausdorff", C.c_int),
+        ("hausdorff_labels", C.POINTER(C.c_int)),
+        ("hausdorff_mm", C.POINTER(C.c_double)),
+        ("jacobian_pct_nonpositive", C.c_double),
+        ("runtime_seconds", C.c_double),
+        ("velocity_count", C.c_int),
+        ("config", ReportConfig),
     ]
 
 

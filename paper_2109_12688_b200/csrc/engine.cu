@@ -774,6 +774,41 @@ std::string graph_key(int P, const dreg_reg_cfg& c, const std::vector<Workspace*
     return k;
 }
 
+// L2 residency of the x-spectrum (DREG_L2_PERSIST = set-aside MB, 0 = off): every
+// kernel node of the registration graph gets an access-policy window over S with
+// hitProp persisting, so the spectrum written by one pass stays in L2 for the next
+// while the ADMM state streams past it.  Only pays when the chunk's spectrum
+// (3 * 2(M/2+1)/M * 4 B/voxel per pair) fits the set-aside.
+void apply_l2_window(dreg_cuda_ctx* c, Workspace& w, cudaGraph_t graph) {
+    const int mb = env_int("DREG_L2_PERSIST", 0);
+    if (mb <= 0) return;
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    const size_t want = std::min((size_t)mb << 20, (size_t)prop.persistingL2CacheMaxSize);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    const size_t bytes = std::min(sizeof(float2) * w.S.n, (size_t)prop.accessPolicyMaxWindowSize);
+    cudaKernelNodeAttrValue v{};
+    v.accessPolicyWindow.base_ptr = w.S.p;
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)want / (double)bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    size_t n = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(graph, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeKernel)
+            CK(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+    }
+    if (env_int("DREG_L2_VERBOSE", 0))
+        std::fprintf(stderr, "[dreg] L2 persist: set-aside %zu MB (max %zu MB), window %zu MB (max %zu MB), hit %.3f\n",
+                     want >> 20, (size_t)prop.persistingL2CacheMaxSize >> 20, bytes >> 20,
+                     (size_t)prop.accessPolicyMaxWindowSize >> 20, v.accessPolicyWindow.hitRatio);
+}
+
 void run_registration(dreg_cuda_ctx* c, const std::vector<Workspace*>& lv, int P, const dreg_reg_cfg& cfg) {
     cudaStream_t st = c->stream;
     Workspace& w = *lv.back();
@@ -797,6 +832,7 @@ void run_registration(dreg_cuda_ctx* c, const std::vector<Workspace*>& lv, int P
             throw;
         }
         CK(cudaStreamEndCapture(st, &graph));
+        apply_l2_window(c, w, graph);
         cudaGraphExec_t exec = nullptr;
         const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
         cudaGraphDestroy(graph);
@@ -1519,6 +1555,107 @@ int dreg_cuda_upsample_velocity(dreg_cuda_ctx* c, const float* v, dreg_dims3 sd,
         download_aos(c, w, w.PHI1.p, out);
         return DREG_OK;
     });
+}
+
+// ---- label metrics (metrics.hpp:31-42) -------------------------------------------
+int dreg_cuda_warp_labels(dreg_cuda_ctx* c, const uint16_t* lbl, const float* disp, dreg_dims3 d, uint16_t* out) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "warp_labels");
+        if (!lbl || !disp || !out) throw ArgFail("warp_labels: null buffer");
+        const VolGeom g{d.x, d.y, d.z, (long long)d.x * d.y * d.z};
+        DevArray<uint16_t> in, res;
+        DevArray<float> u;
+        in.alloc((size_t)g.N);
+        res.alloc((size_t)g.N);
+        u.alloc(3 * (size_t)g.N);
+        CK(cudaMemcpyAsync(in.p, lbl, sizeof(uint16_t) * g.N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(u.p, disp, sizeof(float) * 3 * g.N, cudaMemcpyHostToDevice, c->stream));
+        CK(launch_warp_labels(g, in.p, u.p, res.p, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, res.p, sizeof(uint16_t) * g.N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_label_metrics(dreg_cuda_ctx* c, const uint16_t* a, const uint16_t* b, dreg_dims3 d, dreg_spacing3 sp,
+                            int n_labels, const int* labels, double* dice_out, double* hd_out, int* hd_valid) {
+    return guarded(c, [&] {
+        check_dims(d, 1, "label metrics");
+        if (!a || !b || (n_labels > 0 && !labels)) throw ArgFail("label metrics: null buffer");
+        if (n_labels < 0 || n_labels > 65535) throw ArgFail("label metrics: label count out of range");
+        if (!(sp.x > 0.0) || !(sp.y > 0.0) || !(sp.z > 0.0))
+            throw ArgFail("label volume spacing must be positive");
+        if (n_labels == 0) return DREG_OK;
+        const VolGeom g{d.x, d.y, d.z, (long long)d.x * d.y * d.z};
+        DevArray<uint16_t> da, db;
+        DevArray<int> dl;
+        da.alloc((size_t)g.N);
+        db.alloc((size_t)g.N);
+        dl.alloc((size_t)n_labels);
+        CK(cudaMemcpyAsync(da.p, a, sizeof(uint16_t) * g.N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(db.p, b, sizeof(uint16_t) * g.N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(dl.p, labels, sizeof(int) * n_labels, cudaMemcpyHostToDevice, c->stream));
+        std::vector<unsigned long long> counts(3 * (size_t)n_labels);
+        std::vector<double> worst;
+        DevArray<unsigned long long> dc;
+        if (dice_out) {
+            dc.alloc(3 * (size_t)n_labels);
+            CK(launch_label_counts(g, da.p, db.p, dl.p, n_labels, dc.p, c->stream));
+            c->launches += 1;
+            CK(cudaMemcpyAsync(counts.data(), dc.p, sizeof(unsigned long long) * counts.size(), cudaMemcpyDeviceToHost,
+                               c->stream));
+        }
+        DevArray<double> scratch, dw;
+        DevArray<int> iscratch;
+        if (hd_out || hd_valid) {
+            const long long items = (long long)g.Nz * n_labels;
+            const int ctas = (int)std::min<long long>(items, 148LL * 4);
+            scratch.alloc(hausdorff_scratch_doubles(g, ctas));
+            iscratch.alloc(hausdorff_scratch_ints(g, ctas));
+            dw.alloc((size_t)items);
+            worst.resize((size_t)items);
+            CK(launch_hausdorff_slices(g, da.p, db.p, dl.p, n_labels, sp.x, sp.y, ctas, scratch.p, iscratch.p, dw.p,
+                                       c->stream));
+            c->launches += 1;
+            CK(cudaMemcpyAsync(worst.data(), dw.p, sizeof(double) * items, cudaMemcpyDeviceToHost, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        for (int j = 0; j < n_labels; ++j) {
+            if (dice_out) {  // metrics.cpp:144-147
+                const unsigned long long ia = counts[3 * j], ib = counts[3 * j + 1], both = counts[3 * j + 2];
+                dice_out[j] = ia + ib == 0 ? 1.0 : 2.0 * (double)both / (double)(ia + ib);
+            }
+            if (hd_out || hd_valid) {  // metrics.cpp:172-179: slice order, fp64
+                double total = 0.0;
+                int contributing = 0;
+                for (int z = 0; z < g.Nz; ++z) {
+                    const double wz = worst[(size_t)j * g.Nz + z];
+                    if (wz < 0.0) continue;
+                    total += std::sqrt(wz);
+                    ++contributing;
+                }
+                if (hd_valid) hd_valid[j] = contributing > 0;
+                if (hd_out) hd_out[j] = contributing > 0 ? total / contributing : std::nan("");
+            }
+        }
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_dice(dreg_cuda_ctx* c, const uint16_t* a, const uint16_t* b, dreg_dims3 d, int label, double* out) {
+    if (!out) return c ? fail(c, DREG_INVALID_ARGUMENT, "dice: null output") : DREG_INVALID_ARGUMENT;
+    return dreg_cuda_label_metrics(c, a, b, d, {1.0, 1.0, 1.0}, 1, &label, out, nullptr, nullptr);
+}
+
+int dreg_cuda_hausdorff_slice_avg(dreg_cuda_ctx* c, const uint16_t* a, const uint16_t* b, dreg_dims3 d,
+                                  dreg_spacing3 sp, int label, double* out) {
+    if (!out) return c ? fail(c, DREG_INVALID_ARGUMENT, "hausdorff_slice_avg: null output") : DREG_INVALID_ARGUMENT;
+    int valid = 0;
+    const int st = dreg_cuda_label_metrics(c, a, b, d, sp, 1, &label, nullptr, out, &valid);
+    if (st != DREG_OK) return st;
+    if (!valid) return fail(c, DREG_INVALID_ARGUMENT, "hausdorff_slice_avg: no slice has both masks non-empty");
+    return DREG_OK;
 }
 
 }  // extern "C"

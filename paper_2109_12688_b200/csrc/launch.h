@@ -135,6 +135,16 @@ cudaError_t launch_level_up(VolGeom src, VolGeom dst, const RegBuffers& Rs, cons
                             int npairs, cudaStream_t s);
 cudaError_t launch_upsample(VolGeom src, VolGeom dst, const float* in, float* out, int ncomp,
                             cudaStream_t s);
+// ---- label metrics (metrics_kernels.cu) ----
+cudaError_t launch_warp_labels(VolGeom g, const uint16_t* lbl, const float* disp_aos, uint16_t* out, cudaStream_t s);
+cudaError_t launch_label_counts(VolGeom g, const uint16_t* a, const uint16_t* b, const int* labels, int n_labels,
+                                unsigned long long* counts, cudaStream_t s);
+size_t hausdorff_scratch_doubles(VolGeom g, int ctas);
+size_t hausdorff_scratch_ints(VolGeom g, int ctas);
+cudaError_t launch_hausdorff_slices(VolGeom g, const uint16_t* a, const uint16_t* b, const int* labels, int n_labels,
+                                    double sx, double sy, int ctas, double* scratch, int* iscratch, double* worst,
+                                    cudaStream_t s);
+
 cudaError_t launch_aos_to_soa(long long N, const float* aos, float* soa, cudaStream_t s);
 cudaError_t launch_soa_to_aos(long long N, const float* soa, float* aos, cudaStream_t s);
 cudaError_t launch_add(long long n, const float* a, const float* b, float* out, cudaStream_t s);

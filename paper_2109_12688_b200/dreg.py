@@ -5,6 +5,7 @@ library (proj/core/include/dreg/*.hpp):
 
   ValueError    <- std::invalid_argument   (status DREG_INVALID_ARGUMENT)
   NumericError  <- dreg::numeric_error     (status DREG_NUMERIC, errors.hpp:15-17)
+  IoError       <- dreg::io_error          (status DREG_IO_ERROR; file I/O only)
   RuntimeError  <- CUDA / allocation       (status DREG_RUNTIME)
 
 Volumes are numpy float32 arrays shaped (z, y, x) (x fastest, volume.hpp:10) and
@@ -42,6 +43,10 @@ _lib = None
 
 class NumericError(RuntimeError):
     """dreg::numeric_error: non-finite values produced or encountered."""
+
+
+class IoError(RuntimeError):
+    """dreg::io_error: unreadable / malformed / unwritable DREG files."""
 
 
 def lib_path() -> str:
@@ -96,6 +101,15 @@ def load_library() -> C.CDLL:
     L.dreg_cuda_mean_sad.argtypes = [P, _F, _F, Dims3, _D]
     L.dreg_cuda_downsample.argtypes = [P, _F, Dims3, _F]
     L.dreg_cuda_upsample_velocity.argtypes = [P, _F, Dims3, Dims3, _F]
+    CP, SZ = C.c_char_p, C.c_size_t
+    L.dreg_volume_info_read.argtypes = [CP, C.POINTER(abi.VolumeInfo), CP, SZ]
+    L.dreg_volume_read.argtypes = [CP, C.c_int, C.POINTER(abi.VolumeInfo), V, SZ, CP, SZ]
+    L.dreg_volume_write.argtypes = [CP, C.c_int, Dims3, Spacing3, V, CP, SZ]
+    L.dreg_report_write.argtypes = [CP, C.POINTER(abi.RunReport), CP, SZ]
+    L.dreg_cuda_warp_labels.argtypes = [P, V, _F, Dims3, V]
+    L.dreg_cuda_dice.argtypes = [P, V, V, Dims3, C.c_int, _D]
+    L.dreg_cuda_hausdorff_slice_avg.argtypes = [P, V, V, Dims3, Spacing3, C.c_int, _D]
+    L.dreg_cuda_label_metrics.argtypes = [P, V, V, Dims3, Spacing3, C.c_int, V, V, V, V]
     _lib = L
     return L
 
@@ -143,6 +157,83 @@ def laplacian_symbol(order: int, dims) -> np.ndarray:
     if load_library().dreg_laplacian_symbol(order, d, out.ctypes.data_as(_D)):
         raise ValueError("laplacian_symbol: order must be in [1, 6] and every axis >= 2")
     return out
+
+
+# ---- DREG files and run reports (io.hpp; host only) ---------------------------------
+_KIND_DTYPE = {abi.DREG_KIND_SCALAR: np.float32, abi.DREG_KIND_VECTOR: np.float32, abi.DREG_KIND_LABEL: np.uint16}
+_KIND_OF = {"scalar": abi.DREG_KIND_SCALAR, "vector": abi.DREG_KIND_VECTOR, "label": abi.DREG_KIND_LABEL}
+
+
+def _io_check(st: int, err) -> None:
+    if st == abi.DREG_OK:
+        return
+    msg = err.value.decode(errors="replace")
+    if st == abi.DREG_IO_ERROR:
+        raise IoError(msg)
+    _raise(st, msg)
+
+
+def read_volume(path, expected_kind: int = -1):
+    """read_volume / read_scalar / read_vector / read_label (io.hpp:27-35).
+
+    Returns (kind, array, spacing): float32 (z, y, x) for scalars, float32 (z, y, x, 3)
+    for vector fields, uint16 (z, y, x) for labels; spacing = (sx, sy, sz)."""
+    L = load_library()
+    err = C.create_string_buffer(1024)
+    info = abi.VolumeInfo()
+    p = os.fsencode(str(path))
+    _io_check(L.dreg_volume_read(p, int(expected_kind), C.byref(info), None, 0, err, 1024), err)
+    shape = info.dims.shape() + ((3,) if info.kind == abi.DREG_KIND_VECTOR else ())
+    out = np.empty(shape, _KIND_DTYPE[info.kind])
+    _io_check(L.dreg_volume_read(p, int(expected_kind), C.byref(info), out.ctypes.data, out.nbytes, err, 1024), err)
+    return info.kind, out, (info.spacing.x, info.spacing.y, info.spacing.z)
+
+
+def read_scalar(path):
+    return read_volume(path, abi.DREG_KIND_SCALAR)[1:]
+
+
+def read_vector(path):
+    return read_volume(path, abi.DREG_KIND_VECTOR)[1:]
+
+
+read_deformation = read_vector
+
+
+def read_label(path):
+    return read_volume(path, abi.DREG_KIND_LABEL)[1:]
+
+
+def write_volume(path, data, spacing=(1.0, 1.0, 1.0), kind: str | None = None) -> None:
+    """write_volume (io.hpp:37-40).  kind defaults from the array: uint16 -> label,
+    (z, y, x, 3) float -> vector, (z, y, x) float -> scalar."""
+    if kind is None:
+        a = np.asarray(data)
+        kind = "label" if a.dtype == np.uint16 else ("vector" if a.ndim == 4 else "scalar")
+    k = _KIND_OF[kind]
+    a = np.ascontiguousarray(data, dtype=_KIND_DTYPE[k])
+    err = C.create_string_buffer(1024)
+    st = load_library().dreg_volume_write(os.fsencode(str(path)), k, abi.dims3(a), Spacing3(*spacing),
+                                          a.ctypes.data, err, 1024)
+    _io_check(st, err)
+
+
+def write_report(path, *, dice=None, hausdorff_mm=None, jacobian_pct_nonpositive=0.0, runtime_seconds=0.0,
+                 velocity_count=0, data_term="l1", order=0, lambda_=0.0, theta=0.0, levels=0, profile="capped",
+                 tol=0.0, warp_improvement_threshold=0.0, epsilon=0.0, threads=1) -> None:
+    """write_report (io.hpp:64-66); dice / hausdorff_mm map label -> value."""
+    dice = dict(dice or {})
+    hd = dict(hausdorff_mm or {})
+    dl = (C.c_int * max(len(dice), 1))(*dice.keys())
+    dv = (C.c_double * max(len(dice), 1))(*dice.values())
+    hl = (C.c_int * max(len(hd), 1))(*hd.keys())
+    hv = (C.c_double * max(len(hd), 1))(*hd.values())
+    cfg = abi.ReportConfig(data_term.encode(), order, lambda_, theta, levels, profile.encode(), tol,
+                           warp_improvement_threshold, epsilon, threads)
+    rep = abi.RunReport(len(dice), dl, dv, len(hd), hl, hv, jacobian_pct_nonpositive, runtime_seconds,
+                        velocity_count, cfg)
+    err = C.create_string_buffer(1024)
+    _io_check(load_library().dreg_report_write(os.fsencode(str(path)), C.byref(rep), err, 1024), err)
 
 
 class Context:
@@ -393,3 +484,54 @@ class Context:
         out = np.zeros(dd.shape() + (3,), np.float32)
         self._check(self.lib.dreg_cuda_upsample_velocity(self.h, _fp(v), abi.dims3(v), dd, _fp(out)))
         return out
+
+    # ---- label metrics (metrics.hpp:31-42) ----------------------------------------
+    def warp_labels(self, labels, disp) -> np.ndarray:
+        """Nearest-neighbour label warp at x + disp(x) (metrics.cpp:182-204)."""
+        lbl = np.ascontiguousarray(labels, dtype=np.uint16)
+        disp = _f32(disp)
+        if disp.shape != lbl.shape + (3,):
+            raise ValueError("warp_labels: dimension mismatch")
+        out = np.empty_like(lbl)
+        self._check(self.lib.dreg_cuda_warp_labels(self.h, lbl.ctypes.data, _fp(disp), abi.dims3(lbl), out.ctypes.data))
+        return out
+
+    def label_metrics(self, a, b, labels, spacing=(1.0, 1.0, 1.0)):
+        """Dice and slice-averaged Hausdorff for every label in one upload.
+        Returns (dice[list], hausdorff[list], valid[list])."""
+        a = np.ascontiguousarray(a, dtype=np.uint16)
+        b = np.ascontiguousarray(b, dtype=np.uint16)
+        if a.shape != b.shape:
+            raise ValueError("label metrics: dimension mismatch")
+        lab = np.ascontiguousarray(list(labels), dtype=np.int32)
+        n = len(lab)
+        dice = np.zeros(max(n, 1), np.float64)
+        hd = np.zeros(max(n, 1), np.float64)
+        ok = np.zeros(max(n, 1), np.int32)
+        self._check(self.lib.dreg_cuda_label_metrics(self.h, a.ctypes.data, b.ctypes.data, abi.dims3(a),
+                                                     Spacing3(*spacing), n, lab.ctypes.data, dice.ctypes.data,
+                                                     hd.ctypes.data, ok.ctypes.data))
+        return dice[:n].tolist(), hd[:n].tolist(), [bool(v) for v in ok[:n]]
+
+    def dice(self, a, b, label: int) -> float:
+        """2|A n B| / (|A| + |B|); 1 when both masks are empty (metrics.cpp:131-147)."""
+        a = np.ascontiguousarray(a, dtype=np.uint16)
+        b = np.ascontiguousarray(b, dtype=np.uint16)
+        if a.shape != b.shape:
+            raise ValueError("dice: dimension mismatch")
+        out = C.c_double()
+        self._check(self.lib.dreg_cuda_dice(self.h, a.ctypes.data, b.ctypes.data, abi.dims3(a), int(label),
+                                            C.byref(out)))
+        return out.value
+
+    def hausdorff_slice_avg(self, a, b, label: int, spacing=(1.0, 1.0, 1.0)) -> float:
+        """Per-z-slice symmetric Hausdorff (mm, in-plane spacing), averaged over slices
+        where both masks are non-empty; ValueError when none is (metrics.cpp:149-180)."""
+        a = np.ascontiguousarray(a, dtype=np.uint16)
+        b = np.ascontiguousarray(b, dtype=np.uint16)
+        if a.shape != b.shape:
+            raise ValueError("hausdorff_slice_avg: dimension mismatch")
+        out = C.c_double()
+        self._check(self.lib.dreg_cuda_hausdorff_slice_avg(self.h, a.ctypes.data, b.ctypes.data, abi.dims3(a),
+                                                           Spacing3(*spacing), int(label), C.byref(out)))
+        return out.value

@@ -38,6 +38,24 @@ def test_library_exports_every_declared_symbol():
         assert re.search(rf"\bT {f}\b", out), f
 
 
+def test_synth_library_exports_dreg_synth_h():
+    hdr = open(os.path.join(ROOT, "include", "dreg_synth.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    fns = sorted(set(re.findall(r"\b(dreg_[a-z0-9_]+)\s*\(", hdr)))
+    assert "dreg_synth_case" in fns and "dreg_synth_pair" in fns
+    path = os.path.join(ROOT, "paper_2109_12688_b200", "lib", "libdreg_synth.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    for f in fns:
+        assert re.search(rf"\bT {f}\b", out), f
+
+
+def test_cli_binary_links_the_product_library():
+    exe = os.path.join(ROOT, "paper_2109_12688_b200", "lib", "dreg")
+    out = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "libdreg_cuda.so" in out and "libdreg_synth.so" in out
+    assert "not found" not in out.split("libdreg_cuda.so")[1].splitlines()[0]
+
+
 def test_library_is_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", dreg.lib_path()], capture_output=True, text=True).stdout
     assert "sm_100a" in out
@@ -52,6 +70,9 @@ STRUCTS = {
     "dreg_level_log": abi.LevelLog,
     "dreg_pair_result": abi.PairResult,
     "dreg_jacobian_stats": abi.JacobianStats,
+    "dreg_volume_info": abi.VolumeInfo,
+    "dreg_report_config": abi.ReportConfig,
+    "dreg_run_report": abi.RunReport,
 }
 
 
