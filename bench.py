@@ -120,6 +120,17 @@ class ClockSampler:
 
 
 # ---- CPU reference --------------------------------------------------------------------
+def reference_cpu_lib():
+    """(library kind, FFT label) of the reference build used for CPU timing: the
+    unmodified reference objects over MKL DFTI when that build loads (a production FFT
+    like the FFTW the reference links), else over the portable parity FFT shim."""
+    from oracle.oracle import available
+
+    if available("reference_mkl") and os.environ.get("DREG_REF_FFT", "mkl") == "mkl":
+        return "reference_mkl", "FFTW3 API over MKL DFTI (libtorch_cpu), single-threaded plans"
+    return "reference", "FFTW3 API over the portable double FFT shim (~pocketfft speed)"
+
+
 def cpu_reference_sample(order: int, threads: int, seed0: int = 1000):
     """`threads` concurrent single-threaded reference solves (one config-2 velocity
     field, 50 accelerated ADMM iterations each) on distinct config-3 pairs.
@@ -127,7 +138,7 @@ def cpu_reference_sample(order: int, threads: int, seed0: int = 1000):
     from oracle.oracle import CpuLib
     from paper_2109_12688_b200 import abi, synth
 
-    ref = CpuLib("reference")
+    ref = CpuLib(reference_cpu_lib()[0])
     ref.set_threads(1)
     F, M = synth.make_batch(3, seed0, threads, SHAPE)
     cfg = reg_cfg(order).solver
@@ -211,7 +222,8 @@ def run_reference_arm(args, rank, world):
         "dtype": "f64",
         "data": "synthetic (seeded config-3 phantoms)",
         "config": {"workload": "config3 pairs (64x128x128), config-2 solver n=%d, 7 fields x 50 iterations" % args.order,
-                   "impl_detail": "unmodified reference core (oracle/_ref, FFTW3 API shim), one thread per pair"},
+                   "impl_detail": "unmodified reference core (oracle/_ref), one thread per pair; FFT: "
+                                  + reference_cpu_lib()[1]},
         "cpu_baseline": {
             "value": value,
             "unit": UNIT,
@@ -219,7 +231,8 @@ def run_reference_arm(args, rank, world):
             "kind": "reference",
             "sample": f"per step: {cores} concurrent single-threaded reference solve_velocity calls (one config-2 "
                       f"velocity field, 50 accelerated ADMM iterations) on distinct pairs; registrations/s = "
-                      f"cores / (step_time x {S:.3f} solves per registration: {S_src})",
+                      f"cores / (step_time x {S:.3f} solves per registration: {S_src}); FFT: "
+                      + reference_cpu_lib()[1],
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -426,7 +439,7 @@ def run_ours(args, rank, world, local_rank):
                 "kind": "reference",
                 "sample": f"{thr} concurrent single-threaded reference solve_velocity calls (one velocity field, 50 "
                           f"iterations) on distinct config-3 pairs took {dt:.2f} s; scaled by the {S:.2f} solves "
-                          f"per registration the GPU run executed on the same seeds",
+                          f"per registration the GPU run executed on the same seeds; FFT: " + reference_cpu_lib()[1],
             }
     print(json.dumps(line), flush=True)
 

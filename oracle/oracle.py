@@ -27,6 +27,8 @@ from paper_2109_12688_b200 import abi  # noqa: E402
 _PATHS = {
     "oracle": (os.path.join(_HERE, "lib", "libdreg_oracle.so"), "dro_"),
     "reference": (os.path.join(_HERE, "_ref", "libdreg_ref.so"), "ref_"),
+    # same reference objects over MKL DFTI (timing only; see fftw_shim/fftw_mkl.c)
+    "reference_mkl": (os.path.join(_HERE, "_ref", "libdreg_ref_mkl.so"), "ref_"),
 }
 
 _F = C.POINTER(C.c_float)
@@ -93,7 +95,7 @@ class CpuLib:
             "register_pair",
         ]:
             g(n).restype = C.c_int
-        if kind == "reference":
+        if kind in ("reference", "reference_mkl"):
             L.ref_set_thread_count.argtypes = [C.c_int]
             L.ref_hardware_threads.restype = C.c_int
 
@@ -103,7 +105,7 @@ class CpuLib:
             raise OracleError(st, self._g("last_error")().decode())
 
     def set_threads(self, n: int) -> None:
-        if self.kind == "reference":
+        if self.kind in ("reference", "reference_mkl"):
             self.lib.ref_set_thread_count(int(n))
 
     # -- API mirror ------------------------------------------------------------

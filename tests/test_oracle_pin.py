@@ -95,3 +95,22 @@ def test_oracle_fft_against_numpy(oracle, shape):
     ref = np.stack([np.fft.irfftn(np.fft.rfftn(v[..., c].astype(np.float64)) * (0.3 / (0.7 * K[:, :, :hx] + 0.3)),
                                   s=shape, axes=(0, 1, 2)) for c in range(3)], -1)
     assert np.abs(out - ref).max() <= 1e-6
+
+
+def test_mkl_timing_build_matches_parity_build(reference):
+    """The CPU-timing build of the reference (same objects, FFTW API over MKL DFTI,
+    bench.py's cpu_baseline / --impl reference) computes the same registration as the
+    parity build up to FFT rounding."""
+    from oracle.oracle import CpuLib, available
+
+    if not available("reference_mkl"):
+        pytest.skip("oracle/_ref/libdreg_ref_mkl.so not built")
+    mkl = CpuLib("reference_mkl")
+    f, m = synth.make_pair(1, 5, (16, 32, 32))
+    cfg = abi.reg_cfg(abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=50),
+                      max_warps=(3,), max_admm_iters=(50,))
+    p1, w1, r1 = reference.register_pair(f, m, cfg)
+    p2, w2, r2 = mkl.register_pair(f, m, cfg)
+    assert r1.velocity_count == r2.velocity_count
+    assert np.max(np.abs(p1 - p2)) < 1e-5
+    assert np.linalg.norm(p1 - p2) <= 1e-6 * np.linalg.norm(p1)
