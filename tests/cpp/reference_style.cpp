@@ -3,7 +3,10 @@
 // include/dreg_b200/dreg.hpp and linked with libdreg_cuda.so.  Exit 0 = all checks pass.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <stdexcept>
+#include <string>
 
 #include "dreg_b200/dreg.hpp"
 
@@ -75,6 +78,48 @@ int main() {
         threw = true;
     }
     CHECK(threw);
+    // io.hpp idioms (test_io.cpp): round trips, kind mismatch, report
+    const auto dir = std::filesystem::temp_directory_path();
+    const auto pphi = dir / "dreg_client_phi.dreg";
+    dreg::write_volume(pphi, res.phi);
+    const auto back = dreg::read_deformation(pphi);
+    CHECK(back.disp.data == res.phi.disp.data);
+    threw = false;
+    try {
+        (void)dreg::read_scalar(pphi);
+    } catch (const dreg::io_error&) {
+        threw = true;
+    }
+    CHECK(threw);
+    const auto any = dreg::read_volume(pphi);
+    CHECK(std::holds_alternative<dreg::VectorField>(any));
+
+    // metrics.hpp idioms (test_metrics.cpp): label warp, dice, hausdorff
+    dreg::LabelVolume tl(dims, {1.0, 1.0, 1.0}), sl(dims, {1.0, 1.0, 1.0});
+    for (int z = 0; z < dims.z; ++z)
+        for (int y = 0; y < dims.y; ++y)
+            for (int x = 0; x < dims.x; ++x) {
+                tl.at(x, y, z) = target.at(x, y, z) > 0.5f ? 1 : 0;
+                sl.at(x, y, z) = source.at(x, y, z) > 0.5f ? 1 : 0;
+            }
+    const auto plbl = dir / "dreg_client_labels.dreg";
+    dreg::write_volume(plbl, sl);
+    CHECK(dreg::read_label(plbl).labels == sl.labels);
+    const auto warped_lbl = dreg::warp_labels(sl, res.phi);
+    const double d_before = dreg::dice(sl, tl, 1), d_after = dreg::dice(warped_lbl, tl, 1);
+    CHECK(d_after >= d_before);
+    CHECK(dreg::hausdorff_slice_avg(tl, tl, 1) == 0.0);
+    dreg::RunReport report;
+    report.dice[1] = d_after;
+    report.hausdorff_mm[1] = dreg::hausdorff_slice_avg(warped_lbl, tl, 1);
+    report.velocity_count = res.velocity_count;
+    report.config = {"l2", 2, 0.05, 0.5, 1, "capped", 0.0, 0.02, 1e-6, dreg::thread_count()};
+    const auto prep = dir / "dreg_client_report.json";
+    dreg::write_report(prep, report);
+    std::ifstream rf(prep);
+    const std::string text((std::istreambuf_iterator<char>(rf)), std::istreambuf_iterator<char>());
+    CHECK(text.find("\"velocity_count\": " + std::to_string(res.velocity_count)) != std::string::npos);
+
     std::printf("reference-style C++ client OK: velocity_count %d, min det %.4f\n", res.velocity_count, js.min_det);
     return 0;
 }
