@@ -132,28 +132,25 @@ def reference_cpu_lib():
 
 
 def cpu_reference_sample(order: int, threads: int, seed0: int = 1000):
-    """`threads` concurrent single-threaded reference solves (one config-2 velocity
-    field, 50 accelerated ADMM iterations each) on distinct config-3 pairs.
-    Returns (seconds, threads)."""
+    """`threads` concurrent single-threaded reference register_pair calls (the
+    reference's public API, the metric's unit: normalise + smooth, up to 7 velocity
+    solves of 50 accelerated ADMM iterations, compositions, final warp) on distinct
+    config-3 pairs.  Returns (mean seconds per registration, registrations)."""
     from oracle.oracle import CpuLib
-    from paper_2109_12688_b200 import abi, synth
+    from paper_2109_12688_b200 import synth
 
     ref = CpuLib(reference_cpu_lib()[0])
     ref.set_threads(1)
     F, M = synth.make_batch(3, seed0, threads, SHAPE)
-    cfg = reg_cfg(order).solver
-    s = abi.SolverCfg.from_buffer_copy(cfg)
-    s.log_objective = 0
-    # the solve runs on the normalised, smoothed pair exactly as inside register_pair
-    prepped = []
-    for i in range(threads):
-        a, b = ref.normalize_intensity_pair(F[i], M[i])
-        prepped.append((ref.binomial_smooth(a), ref.binomial_smooth(b)))
+    cfg = reg_cfg(order)
     errs = []
+    per_call = [0.0] * threads
 
     def work(i):
         try:
-            ref.solve_velocity(prepped[i][0], prepped[i][1], s)
+            t = time.perf_counter()
+            ref.register_pair(F[i], M[i], cfg)
+            per_call[i] = time.perf_counter() - t
         except Exception as e:  # noqa: BLE001
             errs.append(e)
 
@@ -163,23 +160,13 @@ def cpu_reference_sample(order: int, threads: int, seed0: int = 1000):
         t.start()
     for t in ts:
         t.join()
-    dt = time.perf_counter() - t0
+    wall = time.perf_counter() - t0
     if errs:
         raise errs[0]
-    return dt, threads
-
-
-def recorded_solves(seeds):
-    """Mean number of solve_velocity calls per registration for these config-3 seeds,
-    from the CPU oracle's full registrations (tests/golden/config3_oracle.json, made by
-    tools/run_config3_oracle.py; bit-exact with the reference).  None if unavailable."""
-    path = os.path.join(ROOT, "tests", "golden", "config3_oracle.json")
-    if not os.path.exists(path):
-        return None
-    with open(path) as f:
-        rec = json.load(f)["pairs"]
-    vals = [rec[str(s)]["solves"] for s in seeds if str(s) in rec]
-    return sum(vals) / len(vals) if len(vals) == len(seeds) else None
+    # steady-state throughput of one registration per core: cores / mean call time
+    # (the wall time of the batch would charge the reference for its slowest pair)
+    cpu_reference_sample.last_wall = wall
+    return sum(per_call) / threads, threads
 
 
 def run_reference_arm(args, rank, world):
@@ -188,25 +175,20 @@ def run_reference_arm(args, rank, world):
     from oracle.oracle import available
 
     cores = args.cpu_threads or os.cpu_count() or 1
-    cfgd = reg_cfg(args.order)
-    K = cfgd.max_warps_per_level[0]
     if not available("reference"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdreg_ref.so not built"}))
         return
-    for _ in range(args.warmup):
+    # one warm-up sample is enough for a CPU arm (page-in, MKL first-use); each step is a
+    # full batch of `cores` registrations (~25-30 s), so more would only lengthen the run
+    for _ in range(min(args.warmup, 1)):
         cpu_reference_sample(args.order, cores)
-    times = []
+    times, walls = [], []
     for _ in range(args.steps):
         dt, _ = cpu_reference_sample(args.order, cores)
         times.append(dt)
+        walls.append(cpu_reference_sample.last_wall)
     t = sum(times) / len(times)
-    from paper_2109_12688_b200 import shard
-
-    S = recorded_solves(shard.pair_seeds(0, 1, args.pairs_per_gpu))
-    S_src = "recorded solves per registration of the same seeds (oracle records)"
-    if S is None:
-        S, S_src = float(K), "the config's cap of 7 fields"
-    value = cores / (t * S)
+    value = cores / t
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -215,7 +197,8 @@ def run_reference_arm(args, rank, world):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": t * 1000.0,
+        "ms_per_step": 1000.0 * sum(walls) / len(walls),
+        "mean_ms_per_registration": t * 1000.0,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -229,10 +212,9 @@ def run_reference_arm(args, rank, world):
             "unit": UNIT,
             "cores": cores,
             "kind": "reference",
-            "sample": f"per step: {cores} concurrent single-threaded reference solve_velocity calls (one config-2 "
-                      f"velocity field, 50 accelerated ADMM iterations) on distinct pairs; registrations/s = "
-                      f"cores / (step_time x {S:.3f} solves per registration: {S_src}); FFT: "
-                      + reference_cpu_lib()[1],
+            "sample": f"per step: {cores} concurrent single-threaded reference register_pair calls on distinct "
+                      f"config-3 pairs (config-2 solver, up to 7 fields x 50 iterations); registrations/s = "
+                      f"{cores} / mean per-call seconds; FFT: " + reference_cpu_lib()[1],
         },
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -431,15 +413,14 @@ def run_ours(args, rank, world, local_rank):
         if available("reference"):
             cores = args.cpu_threads or os.cpu_count() or 1
             dt, thr = cpu_reference_sample(args.order, cores)
-            S = float(solves.mean())
             line["cpu_baseline"] = {
-                "value": thr / (dt * S),
+                "value": thr / dt,
                 "unit": UNIT,
                 "cores": thr,
                 "kind": "reference",
-                "sample": f"{thr} concurrent single-threaded reference solve_velocity calls (one velocity field, 50 "
-                          f"iterations) on distinct config-3 pairs took {dt:.2f} s; scaled by the {S:.2f} solves "
-                          f"per registration the GPU run executed on the same seeds; FFT: " + reference_cpu_lib()[1],
+                "sample": f"{thr} concurrent single-threaded reference register_pair calls on distinct config-3 "
+                          f"pairs (seeds 1000..{999 + thr}, the GPU step's first pairs), mean {dt:.2f} s per call; "
+                          f"registrations/s = {thr} / mean; FFT: " + reference_cpu_lib()[1],
             }
     print(json.dumps(line), flush=True)
 

@@ -434,6 +434,32 @@ def test_register_config4_full_against_oracle_record(ctx):
     assert rel_l2(phi[::4, ::4, ::4], sub) <= PHI_REL_L2
 
 
+@pytest.mark.slow
+def test_register_config5_full_against_oracle_record(ctx):
+    """Full config 5 (256 x 256 x 192 texture, n = 2, 10 fields x 50 iterations; the
+    split three-pass plane path) vs the oracle's record (tests/golden/config5_oracle.json
+    + a [::8]^3 phi subsample, made by tools/run_config5_oracle.py): identical velocity /
+    solve / folding counts, SAD log within 1e-4, phi within the contract on the
+    subsample."""
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    rec = json.load(open(os.path.join(gold, "config5_oracle.json")))
+    sub = np.load(os.path.join(gold, "config5_phi_sub8.npz"))["phi"]
+    c = synth.CONFIGS["config5"]
+    f, m = synth.make_pair(c["synth"], c["seed"], c["shape"])
+    phi, warped, res = ctx.register_pair(f, m, synth.config_cfg("config5"))
+    assert res.status == 0
+    assert res.velocity_count == rec["velocity_count"] and res.solves == rec["solves"]
+    assert np.allclose(abi.level_logs(res)[0]["mean_sad"], rec["mean_sad"], rtol=1e-4, atol=1e-9)
+    js = ctx.jacobian_stats(phi)
+    print(f"config5 folding {js.nonpositive} (oracle {rec['folding']}) min det {js.min_det:.4f} "
+          f"(oracle {rec['min_det']:.4f}) sub max-abs {max_abs(phi[::8, ::8, ::8], sub):.2e} "
+          f"rel-L2 {rel_l2(phi[::8, ::8, ::8], sub):.2e}")
+    assert js.nonpositive == rec["folding"]
+    assert abs(js.min_det - rec["min_det"]) <= 1e-3
+    assert max_abs(phi[::8, ::8, ::8], sub) <= PHI_MAX_ABS
+    assert rel_l2(phi[::8, ::8, ::8], sub) <= PHI_REL_L2
+
+
 @pytest.mark.parametrize("shape", [(64, 128, 128), (32, 64, 64)])
 def test_pipelined_xpass_bit_identical_to_one_tile_kernel(shape):
     """The warp-specialised persistent x-pass (default for M in {64, 128}) and the
