@@ -1610,7 +1610,10 @@ int dreg_cuda_label_metrics(dreg_cuda_ctx* c, const uint16_t* a, const uint16_t*
         DevArray<int> iscratch;
         if (hd_out || hd_valid) {
             const long long items = (long long)g.Nz * n_labels;
-            const int ctas = (int)std::min<long long>(items, 148LL * 4);
+            // resident CTAs loop over (slice, label) items; cap the per-CTA scratch at 256 MB
+            const size_t per_cta = 8 * hausdorff_scratch_doubles(g, 1) + 4 * hausdorff_scratch_ints(g, 1);
+            const long long cap = std::max<long long>(1, (long long)((size_t)256 << 20) / (long long)per_cta);
+            const int ctas = (int)std::min<long long>(std::min<long long>(items, 148LL * 4), cap);
             scratch.alloc(hausdorff_scratch_doubles(g, ctas));
             iscratch.alloc(hausdorff_scratch_ints(g, ctas));
             dw.alloc((size_t)items);
