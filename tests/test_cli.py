@@ -202,3 +202,85 @@ def test_worker_threads_do_not_change_the_result(tmp_path):
     assert run("--threads", "2", *common, p2)[0] == 0
     with open(p1, "rb") as a, open(p2, "rb") as b:
         assert a.read() == b.read()
+
+
+# ---- the reference's CLI-driven acceptance criteria (acceptance_main.cpp) ----------
+@pytest.mark.gpu
+def test_acceptance_pipeline_through_cli(tmp_path):
+    """Criterion 4 (acceptance_main.cpp:215-258): a 3-voxel translation of a 64^3 case is
+    recovered end to end through the CLI: mean displacement inside the target label
+    within 0.5 voxel of (-3, 0, 0), dice >= 0.95, Hausdorff <= 2 x spacing, < 60 s."""
+    import time
+
+    pre = tmp_path / "c4"
+    assert run("synth", "--case", "translate", "--dims", "64,64,64", "--shift", "3,0,0", "--out-prefix", pre)[0] == 0
+    t0 = time.time()
+    rc, out = run("register", "--threads", "1", "--target", f"{pre}_target.dreg", "--source", f"{pre}_source.dreg",
+                  "--out", f"{pre}_phi.dreg", "--warped", f"{pre}_warped.dreg", "--data-term", "l1", "--order", "2",
+                  "--lambda", "5", "--theta", "0.1", "--profile", "capped", "--seed-report", f"{pre}_report.json",
+                  "--target-labels", f"{pre}_target_labels.dreg", "--source-labels", f"{pre}_source_labels.dreg")
+    elapsed = time.time() - t0
+    assert rc == 0, out
+    phi = dreg.read_deformation(f"{pre}_phi.dreg")[0].astype(np.float64)
+    lbl, sp = dreg.read_label(f"{pre}_target_labels.dreg")
+    mean = phi[lbl == 1].mean(axis=0)
+    err = float(np.linalg.norm(mean - np.array([-3.0, 0.0, 0.0])))
+    rep = json.loads(open(f"{pre}_report.json").read())
+    print(f"criterion 4: mean disp err {err:.3f} vox, dice {rep['dice']['1']}, "
+          f"hausdorff {rep['hausdorff_mm']['1']} mm, {elapsed:.2f} s")
+    assert err <= 0.5
+    assert rep["dice"]["1"] >= 0.95
+    assert rep["hausdorff_mm"]["1"] <= 2.0 * max(sp)
+    assert elapsed < 60.0
+
+
+@pytest.mark.gpu
+def test_acceptance_sweep_through_cli(tmp_path):
+    """Criterion 6 (acceptance_main.cpp:296-355): every data term x order in
+    {l1, l2} x {1, 2, 3} reaches dice >= 0.85 on the sphere->ellipsoid case, and with 5%
+    salt-and-pepper on the source the robust l1 term is at least as good as l2."""
+    pre = tmp_path / "c6"
+    assert run("synth", "--case", "sphere-ellipsoid", "--dims", "32,32,32", "--out-prefix", pre)[0] == 0
+
+    def reg(tag, dt, order, lam, src):
+        out = tmp_path / f"c6_{tag}"
+        rc, msg = run("register", "--threads", "1", "--target", f"{src}_target.dreg", "--source",
+                      f"{src}_source.dreg", "--out", f"{out}_phi.dreg", "--data-term", dt, "--order", order,
+                      "--lambda", lam, "--theta", "0.05", "--profile", "capped", "--seed-report",
+                      f"{out}_report.json", "--target-labels", f"{src}_target_labels.dreg", "--source-labels",
+                      f"{src}_source_labels.dreg")
+        assert rc == 0, msg
+        return json.loads(open(f"{out}_report.json").read())["dice"]["1"]
+
+    lam_for = {1: 1.0, 2: 5.0, 3: 5.0}
+    dices = {}
+    for dt in ("l1", "l2"):
+        for order in (1, 2, 3):
+            dices[f"{dt}{order}"] = reg(f"{dt}{order}", dt, order, lam_for[order], pre)
+    noisy = tmp_path / "c6_noisy"
+    assert run("synth", "--case", "sphere-ellipsoid", "--dims", "32,32,32", "--noise", "0.05", "--seed", "5",
+               "--out-prefix", noisy)[0] == 0
+    d1 = reg("noisy_l1", "l1", 2, 10.0, noisy)
+    d2 = reg("noisy_l2", "l2", 2, 10.0, noisy)
+    print("criterion 6:", dices, f"noisy l1={d1} l2={d2}")
+    assert all(d >= 0.85 for d in dices.values()), dices
+    assert d1 >= d2
+
+
+@pytest.mark.gpu
+def test_acceptance_reproducibility_through_cli(tmp_path):
+    """Criterion 7 (acceptance_main.cpp:358-395): identical invocations produce
+    byte-identical deformation files and reports identical modulo runtime."""
+    pre = tmp_path / "c7"
+    assert run("synth", "--case", "translate", "--dims", "32,32,32", "--shift", "2,0,0", "--out-prefix", pre)[0] == 0
+    common = ["register", "--threads", "1", "--target", f"{pre}_target.dreg", "--source", f"{pre}_source.dreg",
+              "--data-term", "l1", "--order", "2", "--lambda", "10", "--theta", "0.05", "--profile", "capped"]
+    assert run(*common, "--out", f"{pre}_phi_a.dreg", "--seed-report", f"{pre}_report_a.json")[0] == 0
+    assert run(*common, "--out", f"{pre}_phi_b.dreg", "--seed-report", f"{pre}_report_b.json")[0] == 0
+    with open(f"{pre}_phi_a.dreg", "rb") as a, open(f"{pre}_phi_b.dreg", "rb") as b:
+        assert a.read() == b.read()
+    ra = json.loads(open(f"{pre}_report_a.json").read())
+    rb = json.loads(open(f"{pre}_report_b.json").read())
+    ra.pop("runtime_seconds")
+    rb.pop("runtime_seconds")
+    assert ra == rb
