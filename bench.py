@@ -7,10 +7,10 @@ with seeds 1000 + i -- registered with the config-2 solver (SSD data term, n = 2
 lambda 0.1, theta (rho) 1.0, 7 composed velocity fields, 10 ADMM x 5 Nesterov = 50
 accelerated iterations per field, levels = 1).  A step registers `--pairs-per-gpu`
 (default 128) pairs on every GPU (weak scaling; at 2 GPUs x 128 pairs it is config 3's
-256 pairs), as two device chunks of 64 pairs (`--chunk`, default half the step): within
-one call the host copies of one chunk overlap the other chunk's registration (e2e), and
-64 pairs per launch keep the persistent x-pass's per-CTA tile ranges long (measured
-112.8 vs 108.5 registrations/s for 32-pair chunks).
+256 pairs).  Pairs per device launch follow the library's policy (`--chunk` overrides):
+device-resident batches run as one launch chunk of up to 256 pairs (long persistent
+x-pass tile ranges: 115.1 vs 112.9 registrations/s for 2 x 64 at 128 pairs), host-buffer
+batches as 64-pair chunks so one chunk's copies overlap the next chunk's registration.
 
   value : registrations/s over all ranks, inputs resident in HBM before the timed
           region (dreg_cuda_register_batch_device), L2 flushed between steps.
@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--pairs-per-gpu", type=int, default=128)
     ap.add_argument("--order", type=int, default=2)
-    ap.add_argument("--chunk", type=int, default=0, help="pairs per device launch (0 = half the step)")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="pairs per device launch (0 = library auto: up to 256 device-resident, 64 from host buffers)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
@@ -256,8 +257,9 @@ def run_ours(args, rank, world, local_rank):
     ctx = dreg.Context(local_rank)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
-    chunk = args.chunk or max(1, B // 2)
-    ctx.set_batch_chunk(chunk)
+    ctx.set_batch_chunk(args.chunk)  # 0 = library policy (engine.cu pick_chunk)
+    chunk = args.chunk or min(B, 256)
+    e2e_chunk = args.chunk or min(B, 64)
 
     def step():
         res = ctx.register_batch_device(B, tgt.data_ptr(), src.data_ptr(), SHAPE[::-1], cfg,
@@ -384,6 +386,7 @@ def run_ours(args, rank, world, local_rank):
                         "7 fields x 50 ADMM iterations, levels 1" % args.order,
             "pairs_per_gpu_per_step": B,
             "device_chunk_pairs": chunk,
+            "e2e_chunk_pairs": e2e_chunk,
             "l2": "flushed between timed steps (512 MiB write); per-step working set >> L2",
             "parallelism": f"pairs sharded over {world} GPU(s); NCCL all-gather of per-pair records only",
         },
