@@ -6,8 +6,8 @@ Workload (config["workload"]): config-3 phantoms -- the config-2 cardiac-shaped 
 with seeds 1000 + i -- registered with the config-2 solver (SSD data term, n = 2,
 lambda 0.1, theta (rho) 1.0, 7 composed velocity fields, 10 ADMM x 5 Nesterov = 50
 accelerated iterations per field, levels = 1).  A step registers `--pairs-per-gpu`
-(default 128) pairs on every GPU (weak scaling; at 2 GPUs x 128 pairs it is config 3's
-256 pairs).  Pairs per device launch follow the library's policy (`--chunk` overrides):
+(default 256: on one GPU exactly config 3's 256 pairs; weak scaling, so N GPUs register
+256 N pairs).  Pairs per device launch follow the library's policy (`--chunk` overrides):
 device-resident batches run as one launch chunk of up to 256 pairs (long persistent
 x-pass tile ranges: 115.1 vs 112.9 registrations/s for 2 x 64 at 128 pairs), host-buffer
 batches as 64-pair chunks so one chunk's copies overlap the next chunk's registration.
@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--pairs-per-gpu", type=int, default=128)
+    ap.add_argument("--pairs-per-gpu", type=int, default=256)
     ap.add_argument("--order", type=int, default=2)
     ap.add_argument("--chunk", type=int, default=0,
                     help="pairs per device launch (0 = library auto: up to 256 device-resident, 64 from host buffers)")
