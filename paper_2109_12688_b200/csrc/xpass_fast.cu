@@ -14,6 +14,7 @@
 // Position of frequency k = 8 p1 + b is R2 b + p1 (same scheme as fft_device.cuh).
 #include <algorithm>
 
+#include <cstdlib>
 #include "fft_device.cuh"
 #include "kernels.cuh"
 #include "launch.h"
@@ -715,6 +716,9 @@ static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = (int)((a.F.lines + kFTL - 1) / kFTL);
+    // DREG_XPASS_SMS (experiment knob): persistent CTAs, i.e. SMs the x-pass occupies
+    const char* lim = std::getenv("DREG_XPASS_SMS");
+    if (lim && std::atoi(lim) > 0) sms = std::min(sms, std::atoi(lim));
     const int grid = std::min(tiles * npairs, sms);
     k<<<grid, 32 * (FW + NPW), smem, s>>>(a, tiles, npairs);
     return cudaGetLastError();
