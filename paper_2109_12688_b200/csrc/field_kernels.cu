@@ -5,6 +5,7 @@
 // weights would break parity).
 #include <cfloat>
 
+#include <cstdlib>
 #include "kernels.cuh"
 #include "launch.h"
 #include "pointwise.cuh"
@@ -86,8 +87,9 @@ __device__ __forceinline__ void compose_warp_voxel(const VolGeom& g, const float
 
 // Two voxels per loop trip (restrict pointers let their gather chains interleave:
 // the kernel is gather-latency bound).
-__global__ void __launch_bounds__(kVT, 3) compose_decide_kernel(VolGeom g, RegBuffers R, Fields F, double thr,
-                                                                int max_warps) {
+template <int MINB>
+__global__ void __launch_bounds__(kVT, MINB) compose_decide_kernel(VolGeom g, RegBuffers R, Fields F, double thr,
+                                                                   int max_warps) {
     __shared__ double red[32];
     const int pair = blockIdx.y;
     PairState* st = F.st + pair;
@@ -147,7 +149,13 @@ __global__ void __launch_bounds__(kVT, 3) compose_decide_kernel(VolGeom g, RegBu
 
 cudaError_t launch_compose_decide(VolGeom g, const RegBuffers& R, Fields F, double thr, int max_warps,
                                   int npairs, cudaStream_t s) {
-    compose_decide_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F, thr, max_warps);
+    // DREG_COMPOSE_MINB: resident blocks per SM the register budget targets (3 or 4)
+    static const int minb = [] {
+        const char* e = std::getenv("DREG_COMPOSE_MINB");
+        return e ? std::atoi(e) : 3;
+    }();
+    if (minb == 4) compose_decide_kernel<4><<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F, thr, max_warps);
+    else compose_decide_kernel<3><<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F, thr, max_warps);
     return cudaGetLastError();
 }
 
