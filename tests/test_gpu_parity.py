@@ -221,6 +221,37 @@ def test_batch_matches_single_and_is_deterministic(ctx):
     assert all(np.array_equal(a, b) for a, b in zip(phis, phis2))
 
 
+def test_device_batch_auto_chunks_match_single(ctx):
+    """Device-resident batches run in launch chunks of up to 256 pairs (pick_chunk):
+    260 pairs = 256 + 4.  Pairs on both sides of the chunk boundary give the same phi
+    and warped image as registering them alone (tol = 0: the result of a pair does not
+    depend on the batch it runs in)."""
+    import torch
+
+    n, shape = 260, (16, 32, 32)
+    F, M = synth.make_batch(1, 500, n, shape)
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=20, log_objective=False)
+    cfg = abi.reg_cfg(s, 1, (3,), (20,))
+    N = int(np.prod(shape))
+    dev = torch.device("cuda", 0)
+    tgt = torch.from_numpy(F.reshape(n, N)).to(dev)
+    src = torch.from_numpy(M.reshape(n, N)).to(dev)
+    phi = torch.empty((n, 3, N), dtype=torch.float32, device=dev)
+    warped = torch.empty((n, N), dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    res = ctx.register_batch_device(n, tgt.data_ptr(), src.data_ptr(), shape[::-1], cfg, phi.data_ptr(),
+                                    warped.data_ptr())
+    torch.cuda.synchronize()
+    assert all(r.status == 0 for r in res)
+    ph = phi.cpu().numpy()
+    wp = warped.cpu().numpy()
+    for i in (0, 255, 256, 259):
+        p1, w1, r1 = ctx.register_pair(F[i], M[i], cfg)
+        assert r1.velocity_count == res[i].velocity_count
+        assert np.array_equal(p1, np.moveaxis(ph[i].reshape(3, *shape), 0, -1)), i
+        assert np.array_equal(w1, wp[i].reshape(shape)), i
+
+
 def test_register_nonfinite_input_raises(ctx):
     f, m = synth.make_pair(1, 8, (16, 16, 16))
     m[3, 4, 5] = np.nan
