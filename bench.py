@@ -281,8 +281,11 @@ def run_ours(args, rank, world, local_rank):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
+        sev[i][0].record(stream)
         res = step()
+        sev[i][1].record(stream)
         if i + 1 < args.steps:
             flush.zero_()
     e1.record(stream)
@@ -290,6 +293,7 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         tdist.barrier()
     launches = ctx.kernel_launches() - n0
+    step_ms = [round(a0.elapsed_time(a1), 2) for a0, a1 in sev]  # per-step registration time (flush excluded)
     clk = clocks.stop()
     ms_max = shard.max_over_ranks(e0.elapsed_time(e1), dev)
     value = world * B * args.steps / (ms_max / 1000.0)
@@ -376,6 +380,7 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps,
+        "step_ms_rank0": step_ms,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
