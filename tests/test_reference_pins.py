@@ -464,3 +464,64 @@ def test_accepted_sad_monotone_and_velocity_bound(lib, reference):
         lg = res.per_level[l]
         sad = [lg.mean_sad[i] for i in range(lg.warps + 1)]
         assert all(b <= a for a, b in zip(sad, sad[1:])), (l, sad)
+
+
+# ---- argument checks and identities (test_volume.cpp, test_registration.cpp) ----------
+def _expect_invalid(fn):
+    """std::invalid_argument in the reference: status 2 through the C ABI (ValueError on
+    the sm_100a path, OracleError(status=2) on the oracle)."""
+    with pytest.raises(Exception) as e:
+        fn()
+    assert isinstance(e.value, ValueError) or getattr(e.value, "status", None) == 2, repr(e.value)
+
+
+def test_gradient_rejects_short_axes(lib):
+    """test_volume.cpp:143-146: an axis shorter than 2 is invalid."""
+    _expect_invalid(lambda: lib.image_gradient(np.zeros((4, 4, 1), np.float32)))
+
+
+def test_jacobian_rejects_short_axes(lib):
+    """test_volume.cpp:250-253: an axis shorter than 3 is invalid."""
+    _expect_invalid(lambda: lib.jacobian_determinant(np.zeros((5, 5, 2, 3), np.float32)))
+
+
+def test_upsample_rejects_shrinking_target(lib):
+    """test_registration.cpp:121-124: a target smaller than the source is invalid."""
+    _expect_invalid(lambda: lib.upsample_velocity(np.zeros((4, 4, 4, 3), np.float32), (3, 4, 4)))
+
+
+def test_upsample_zero_and_uniform(lib):
+    """test_registration.cpp:101-119: zero stays zero, a uniform field doubles."""
+    assert not lib.upsample_velocity(np.zeros((4, 4, 4, 3), np.float32), (8, 8, 8)).any()
+    u = np.zeros((4, 4, 4, 3), np.float32)
+    u[..., 0] = 1.0
+    up = lib.upsample_velocity(u, (8, 8, 8))
+    assert np.allclose(up[..., 0], 2.0) and not up[..., 1:].any()
+
+
+def test_downsample_odd_axis_edge_replication(lib):
+    """test_registration.cpp:93-99: {3,2,2} of ones -> {2,1,1} of ones."""
+    out = lib.downsample(np.ones((2, 2, 3), np.float32))
+    assert out.shape == (1, 1, 2) and np.allclose(out, 1.0)
+
+
+def test_composition_agrees_with_warping_twice(lib, oracle):
+    """test_volume.cpp:171-212: warp(I, compose(phi, v)) ~ warp(warp(I, phi), v) two
+    voxels in from the faces, within 1e-3 of the image range."""
+    zz, yy, xx = np.mgrid[0:8, 0:8, 0:8].astype(np.float64)
+    bump = np.exp(-((xx - 3.5) ** 2 + (yy - 3.5) ** 2 + (zz - 3.5) ** 2) / 16.0)
+    img = (xx + 0.5 * yy + 0.25 * zz + 0.05 * bump).astype(np.float32)
+    phi = smooth_random_field((8, 8, 8), 51, 0.4, oracle)
+    v = smooth_random_field((8, 8, 8), 52, 0.4, oracle)
+    composed = lib.warp_image(img, lib.compose_deformation(phi, v))
+    twice = lib.warp_image(lib.warp_image(img, phi), v)
+    tol = 1e-3 * float(img.max() - img.min())
+    assert np.abs(composed - twice)[2:-2, 2:-2, 2:-2].max() <= tol
+
+
+def test_operations_deterministic(lib):
+    """test_volume.cpp:255-264: warp and gradient are bit-reproducible."""
+    img = random_volume((8, 8, 8), 77)
+    phi = random_field((8, 8, 8), 78, 1.0)
+    assert np.array_equal(lib.warp_image(img, phi), lib.warp_image(img, phi))
+    assert np.array_equal(lib.image_gradient(img), lib.image_gradient(img))
