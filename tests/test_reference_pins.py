@@ -525,3 +525,13 @@ def test_operations_deterministic(lib):
     phi = random_field((8, 8, 8), 78, 1.0)
     assert np.array_equal(lib.warp_image(img, phi), lib.warp_image(img, phi))
     assert np.array_equal(lib.image_gradient(img), lib.image_gradient(img))
+
+
+def test_downsample_identities(lib):
+    """test_registration.cpp:60-91: constant kept, 2x2x2 block -> its mean, ramp slope doubles."""
+    out = lib.downsample(np.full((8, 8, 8), 2.5, np.float32))
+    assert out.shape == (4, 4, 4) and np.allclose(out, 2.5)
+    assert np.allclose(lib.downsample(np.arange(8, dtype=np.float32).reshape(2, 2, 2)), 3.5)
+    ramp = np.broadcast_to(np.arange(8, dtype=np.float32), (4, 4, 8)).copy()
+    out = lib.downsample(ramp)
+    assert np.allclose(out[0, 0, :], 2.0 * np.arange(4) + 0.5)
