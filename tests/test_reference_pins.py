@@ -535,3 +535,19 @@ def test_downsample_identities(lib):
     ramp = np.broadcast_to(np.arange(8, dtype=np.float32), (4, 4, 8)).copy()
     out = lib.downsample(ramp)
     assert np.allclose(out[0, 0, :], 2.0 * np.arange(4) + 0.5)
+
+
+# ---- test_metrics.cpp (jacobian_stats) ---------------------------------------------
+def test_jacobian_stats_identity_translation_and_folding(lib):
+    """test_metrics.cpp:160-187: identity and translations give 0% / min det 1; the
+    field u_x = -2x folds every interior voxel (100%, min det -1)."""
+    u = np.zeros((6, 6, 6, 3), np.float32)
+    st = lib.jacobian_stats(u)
+    assert st.pct_nonpositive == 0.0 and abs(st.min_det - 1.0) < 1e-9 and st.interior == 64
+    u[...] = (2.0, -1.0, 0.5)
+    st = lib.jacobian_stats(u)
+    assert st.pct_nonpositive == 0.0 and abs(st.min_det - 1.0) < 1e-9
+    u = np.zeros((6, 6, 6, 3), np.float32)
+    u[..., 0] = -2.0 * np.arange(6, dtype=np.float32)[None, None, :]
+    st = lib.jacobian_stats(u)
+    assert abs(st.pct_nonpositive - 100.0) < 1e-9 and abs(st.min_det + 1.0) < 1e-9 and st.nonpositive == 64
