@@ -47,7 +47,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--pairs-per-gpu", type=int, default=256)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config (3 = the metric's batched workload; 1/2/4/5 single-pair lines)")
+    ap.add_argument("--dropin-pairs", type=int, default=16,
+                    help="pairs timed one per call through dreg_cuda_register_pair (pageable host buffers)")
+    ap.add_argument("--pairs", type=int, default=None,
+                    help="pairs per step over ALL ranks (config 3: 256, split 256/N per GPU: strong scaling)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: --pairs per GPU instead of in total (distinct seeds on every rank)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the launcher: N gloo ranks deal the seeds and gather fake records")
+    ap.add_argument("--allow-env", action="store_true",
+                    help="allow DREG_* experiment variables (they are echoed in the line either way)")
     ap.add_argument("--order", type=int, default=2)
     ap.add_argument("--chunk", type=int, default=0,
                     help="pairs per device launch (0 = library auto: up to 256 device-resident, 64 from host buffers)")
@@ -223,6 +234,27 @@ def run_reference_arm(args, rank, world):
 
 
 # ---- our arm ---------------------------------------------------------------------------
+def dreg_env() -> dict:
+    """DREG_* experiment variables in effect (echoed in the line; refused unless --allow-env)."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("DREG_")}
+
+
+def workload(args):
+    """(config name, numpy shape, synth id, RegCfg, workload text) of the bench line."""
+    from paper_2109_12688_b200 import synth
+
+    name = f"config{args.config}"
+    c = synth.CONFIGS[name]
+    cfg = synth.config_cfg(name, order=args.order if args.config in (2, 3) else None)
+    n = cfg.solver.order
+    text = {
+        "config3": f"config3 pairs at config-2 settings: 64x128x128, SSD, n={n}, lambda 0.1, theta 1.0, "
+                   "7 fields x 50 ADMM iterations, levels 1",
+    }.get(name, f"{name}: {'x'.join(map(str, c['shape']))}, SSD, n={n}, lambda {c['lambda_']}, "
+                f"theta {c['theta']}, {c['warps']} fields x {c['iters']} ADMM iterations, levels 1")
+    return name, tuple(c["shape"]), c["synth"], cfg, text, c["seed"]
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -233,21 +265,20 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         import torch.distributed as tdist
 
+    env = dreg_env()
+    if env and not args.allow_env:
+        raise SystemExit(f"bench.py: DREG_* experiment variables set {env}; unset them or pass --allow-env")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    B = args.pairs_per_gpu
-    N = SHAPE[0] * SHAPE[1] * SHAPE[2]
-    cfg = reg_cfg(args.order)
-    seeds = shard.pair_seeds(rank, world, B)
-    F = np.zeros((B,) + SHAPE, np.float32)
-    M = np.zeros((B,) + SHAPE, np.float32)
-    i = 0
-    while i < B:  # contiguous seed runs (wrap around the 256-pair pool)
-        j = i
-        while j + 1 < B and seeds[j + 1] == seeds[j] + 1:
-            j += 1
-        synth.make_batch(3, seeds[i], j - i + 1, SHAPE, out_fixed=F[i:j + 1], out_moving=M[i:j + 1])
-        i = j + 1
+    name, SHAPE_, synth_id, cfg, wl_text, seed_base = workload(args)
+    N = SHAPE_[0] * SHAPE_[1] * SHAPE_[2]
+    seeds = shard.rank_seeds(rank, world, args.pairs, args.weak, base=seed_base)
+    B = len(seeds)
+    if B < 1:
+        raise SystemExit(f"bench.py: rank {rank} has no pairs ({args.pairs} pairs over {world} ranks)")
+    F = np.zeros((B,) + SHAPE_, np.float32)
+    M = np.zeros((B,) + SHAPE_, np.float32)
+    synth.make_batch(synth_id, seeds[0], B, SHAPE_, out_fixed=F, out_moving=M)  # contiguous seed block
     tgt = torch.from_numpy(F.reshape(B, N)).to(dev)
     src = torch.from_numpy(M.reshape(B, N)).to(dev)
     phi = torch.empty((B, 3, N), dtype=torch.float32, device=dev)
@@ -260,11 +291,11 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_batch_chunk(args.chunk)  # 0 = library policy (engine.cu pick_chunk)
     chunk = args.chunk or min(B, 256)
     e2e_chunk = args.chunk or min(B, 64)
+    dims = SHAPE_[::-1]
 
     def step():
-        res = ctx.register_batch_device(B, tgt.data_ptr(), src.data_ptr(), SHAPE[::-1], cfg,
-                                        phi.data_ptr(), warped.data_ptr())
-        return res
+        return ctx.register_batch_device(B, tgt.data_ptr(), src.data_ptr(), dims, cfg, phi.data_ptr(),
+                                         warped.data_ptr())
 
     for _ in range(args.warmup):
         res = step()
@@ -296,27 +327,28 @@ def run_ours(args, rank, world, local_rank):
     step_ms = [round(a0.elapsed_time(a1), 2) for a0, a1 in sev]  # per-step registration time (flush excluded)
     clk = clocks.stop()
     ms_max = shard.max_over_ranks(e0.elapsed_time(e1), dev)
-    value = world * B * args.steps / (ms_max / 1000.0)
+    pairs_all = B * world if args.weak else args.pairs
+    value = pairs_all * args.steps / (ms_max / 1000.0)
 
     # per-pair records (status, velocity_count, solves, folding count, final SAD) -> NCCL all-gather
     recs = []
     for p in range(B):
-        js = ctx.jacobian_stats_device(phi[p].data_ptr(), SHAPE[::-1])
+        js = ctx.jacobian_stats_device(phi[p].data_ptr(), dims)
         r = res[p]
         lg = r.per_level[0]
         recs.append([r.status, r.velocity_count, r.solves, js.nonpositive, lg.mean_sad[lg.warps], js.min_det])
     rec = shard.gather_records(torch.tensor(recs, dtype=torch.float64, device=dev)).cpu().numpy()
 
     # roofline of the dominant kernel (fused x-pass), CUDA events on the launching stream
-    tk = ctx.time_kernels(20)
+    tk = ctx.time_kernels(20, cfg.solver)
 
     # e2e through the host-buffer C ABI (pinned host memory)
     e2e = None
     if not args.no_e2e:
-        hT = torch.from_numpy(F.reshape(B, *SHAPE)).pin_memory()
-        hS = torch.from_numpy(M.reshape(B, *SHAPE)).pin_memory()
-        hP = torch.empty((B, *SHAPE, 3), dtype=torch.float32).pin_memory()
-        hW = torch.empty((B, *SHAPE), dtype=torch.float32).pin_memory()
+        hT = torch.from_numpy(F.reshape(B, *SHAPE_)).pin_memory()
+        hS = torch.from_numpy(M.reshape(B, *SHAPE_)).pin_memory()
+        hP = torch.empty((B, *SHAPE_, 3), dtype=torch.float32).pin_memory()
+        hW = torch.empty((B, *SHAPE_), dtype=torch.float32).pin_memory()
         tl, sl = [x.numpy() for x in hT], [x.numpy() for x in hS]
         pl, wl = [x.numpy() for x in hP], [x.numpy() for x in hW]
         import ctypes as C
@@ -331,7 +363,7 @@ def run_ours(args, rank, world, local_rank):
         resb = (abi.PairResult * B)()
 
         def estep():
-            st = ctx.lib.dreg_cuda_register_batch(ctx.h, B, Ta, Sa, abi.dims3(SHAPE[::-1]), abi.Spacing3(1, 1, 1),
+            st = ctx.lib.dreg_cuda_register_batch(ctx.h, B, Ta, Sa, abi.dims3(dims), abi.Spacing3(1, 1, 1),
                                                   C.byref(cfg), Pa, Wa, resb)
             ctx._check(st)
 
@@ -348,10 +380,39 @@ def run_ours(args, rank, world, local_rank):
                 torch.cuda.synchronize(dev)
         et = shard.max_over_ranks(time.perf_counter() - t0, dev)
         e2e = {
-            "value": world * B * args.steps / et,
+            "value": pairs_all * args.steps / et,
             "unit": UNIT,
             "h2d_bytes_per_step": B * 2 * N * 4,
             "d2h_bytes_per_step": B * (3 * N + N) * 4,
+            "path": "dreg_cuda_register_batch (host C ABI), pinned host buffers, "
+                    f"{e2e_chunk}-pair chunks with copy/compute overlap",
+        }
+
+    # the reference user's call: one pair per dreg_cuda_register_pair on pageable host
+    # memory (what dreg::register_pair in include/dreg_b200/dreg.hpp does with its
+    # std::vector buffers), sequentially -- throughput and single-pair latency
+    dropin = None
+    if not args.no_e2e and rank == 0:
+        k = min(B, args.dropin_pairs)
+        tl = [np.ascontiguousarray(F[i]) for i in range(k)]
+        sl = [np.ascontiguousarray(M[i]) for i in range(k)]
+        ctx.register_pair(tl[0], sl[0], cfg)  # warm-up (single-pair workspace + graph)
+        lat = []
+        t0 = time.perf_counter()
+        for i in range(k):
+            t1 = time.perf_counter()
+            ctx.register_pair(tl[i], sl[i], cfg)  # fresh numpy (pageable) outputs every call
+            lat.append(time.perf_counter() - t1)
+        tt = time.perf_counter() - t0
+        dropin = {
+            "value": k / tt,
+            "unit": UNIT,
+            "pairs": k,
+            "single_pair_latency_ms": {"mean": 1e3 * statistics.mean(lat), "min": 1e3 * min(lat),
+                                       "max": 1e3 * max(lat)},
+            "h2d_bytes_per_pair": 2 * N * 4,
+            "d2h_bytes_per_pair": 4 * N * 4,
+            "path": "dreg_cuda_register_pair (= dreg::register_pair), pageable host buffers, one pair per call",
         }
 
     if rank != 0:
@@ -363,17 +424,19 @@ def run_ours(args, rank, world, local_rank):
             peak = float(json.load(f)["hbm_gbs"])
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     achieved = tk["xpass_bytes"] / (tk["xpass_ms"] / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "xpass_dram_bytes.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and name == "config3":
         with open(prof) as f:
             pj = json.load(f)
         if pj.get("pairs"):
             traffic = pj["dram_bytes_per_launch"] / pj["pairs"] * tk["pairs"]
+            traffic_src = ("recorded ncu constant, not measured in this run: dram__bytes_read.sum + "
+                           f"dram__bytes_write.sum of one x-pass launch ({pj.get('source', 'profiles/')}), "
+                           "scaled per pair to this launch")
     it_ms = tk["xpass_ms"] + tk["plane_ms"]
-    solves = rec[:, 2]
     line = {
-        "metric": METRIC,
+        "metric": METRIC if name == "config3" else f"3D registrations/sec ({'x'.join(map(str, SHAPE_))} fp32)",
         "value": value,
         "unit": UNIT,
         "n_gpus": world,
@@ -382,18 +445,21 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": ms_max / args.steps,
         "step_ms_rank0": step_ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.weak else "strong",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic (seeded config-3 phantoms, inputs generated on host then resident in HBM)",
+        "data": f"synthetic (seeded {name} phantoms, inputs generated on host then resident in HBM)",
         "config": {
-            "workload": "config3 pairs at config-2 settings: 64x128x128, SSD, n=%d, lambda 0.1, theta 1.0, "
-                        "7 fields x 50 ADMM iterations, levels 1" % args.order,
+            "workload": wl_text,
+            "pairs_per_step": pairs_all,
             "pairs_per_gpu_per_step": B,
+            "seeds_rank0": [seeds[0], seeds[-1]],
             "device_chunk_pairs": chunk,
             "e2e_chunk_pairs": e2e_chunk,
             "l2": "flushed between timed steps (512 MiB write); per-step working set >> L2",
-            "parallelism": f"pairs sharded over {world} GPU(s); NCCL all-gather of per-pair records only",
+            "parallelism": f"pairs sharded over {world} GPU(s) ({'weak' if args.weak else 'strong'}: "
+                           f"{B} pairs on rank 0); NCCL all-gather of per-pair records only",
+            "dreg_env": env,
         },
         "gpu_launches": int(launches),
         "roofline": {
@@ -405,17 +471,22 @@ def run_ours(args, rank, world, local_rank):
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": traffic,
+            "traffic_source": traffic_src,
+            "bytes_per_launch": tk["xpass_bytes"],
+            "pairs_per_launch": tk["pairs"],
             "xpass_ms": tk["xpass_ms"],
             "plane_ms": tk["plane_ms"],
             "plane_GBps": tk["plane_bytes"] / (tk["plane_ms"] / 1e3) / 1e9,
             "iteration_ms_per_pair": it_ms / tk["pairs"],
             "iteration_frac": (tk["xpass_bytes"] + tk["plane_bytes"]) / (it_ms / 1e3) / 1e9 / peak,
+            "precise": bool(tk.get("precise", 0)),
         },
         "clocks": clk,
         "e2e": e2e,
+        "e2e_dropin": dropin,
         "pairs": shard.summarize(rec),
     }
-    if world == 1 and not args.no_cpu:
+    if world == 1 and not args.no_cpu and name == "config3":
         from oracle.oracle import available
 
         if available("reference"):
@@ -433,13 +504,77 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+# ---- launcher ---------------------------------------------------------------------------
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks (one per
+    GPU, torch.distributed.run on 127.0.0.1).  Refuses when the box has fewer GPUs."""
+    if not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """Launcher check without GPUs: each gloo rank takes its seed block and all-gathers
+    fake per-pair records; rank 0 prints the dealing."""
+    import torch
+
+    from paper_2109_12688_b200 import shard
+
+    seeds = shard.rank_seeds(rank, world, args.pairs, args.weak)
+    rec = torch.tensor([[0, rank, 0, 0, float(s), 1.0] for s in seeds], dtype=torch.float64).reshape(-1, 6)
+    allrec = shard.gather_records(rec).numpy()
+    t = shard.max_over_ranks(float(rank))
+    if rank == 0:
+        by_rank = {}
+        for r in allrec:
+            by_rank.setdefault(int(r[1]), []).append(int(r[4]))
+        flat = [s for r in sorted(by_rank) for s in by_rank[r]]
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": "weak" if args.weak else "strong",
+                          "pairs_total": len(flat), "seeds_by_rank": {r: [v[0], v[-1], len(v)] for r, v in by_rank.items()},
+                          "disjoint": len(set(flat)) == len(flat), "max_over_ranks": t}), flush=True)
+
+
 def main():
     args = parse()
+    if args.pairs is None:
+        args.pairs = 256 if args.config == 3 else 1
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
+        return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.dry_run:
+        import torch.distributed as tdist
+
+        if world > 1:
+            tdist.init_process_group("gloo")
+        try:
+            run_dry(args, rank, world)
+        finally:
+            if world > 1:
+                tdist.destroy_process_group()
         return
     if world > 1:
         import torch

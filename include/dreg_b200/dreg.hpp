@@ -455,6 +455,77 @@ inline RegistrationResult register_pair(const ScalarVolume& target, const Scalar
     return r;
 }
 
+// ---- B200 extension: independent pairs sharded over the GPUs of one box ----------
+// (no reference counterpart).  One host thread and context per
+// device, one NCCL all-gather of the per-pair records.  Each result equals
+// register_pair's for the same pair.
+class MultiDevice {
+public:
+    explicit MultiDevice(const std::vector<int>& devices) {
+        if (devices.empty()) throw std::invalid_argument("MultiDevice: no devices");
+        const int st = dreg_cuda_multi_create(devices.data(), static_cast<int>(devices.size()), &m_);
+        if (st == DREG_INVALID_ARGUMENT) throw std::invalid_argument("MultiDevice: bad or repeated device index");
+        if (st != DREG_OK) throw std::runtime_error("MultiDevice: CUDA / NCCL initialisation failed");
+    }
+    MultiDevice(const MultiDevice&) = delete;
+    MultiDevice& operator=(const MultiDevice&) = delete;
+    ~MultiDevice() { dreg_cuda_multi_destroy(m_); }
+    int device_count() const { return dreg_cuda_multi_device_count(m_); }
+
+    std::vector<RegistrationResult> register_batch(const std::vector<ScalarVolume>& targets,
+                                                   const std::vector<ScalarVolume>& sources,
+                                                   const RegistrationConfig& cfg,
+                                                   std::vector<dreg_pair_record>* records = nullptr) {
+        if (targets.size() != sources.size()) throw std::invalid_argument("register_batch: pair count mismatch");
+        const std::size_t n = targets.size();
+        std::vector<RegistrationResult> out(n);
+        if (n == 0) return out;
+        const Dims3 d = targets[0].dims;
+        for (std::size_t i = 0; i < n; ++i) {
+            b200_detail::same(d, targets[i].dims, "register_batch");
+            b200_detail::same(d, sources[i].dims, "register_batch");
+        }
+        const dreg_reg_cfg c = to_c(cfg);
+        std::vector<const float*> tp(n), sp(n);
+        std::vector<float*> pp(n), wp(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            out[i].phi = DeformationField::identity(d, targets[i].spacing);
+            out[i].warped = ScalarVolume(d, targets[i].spacing);
+            tp[i] = targets[i].data.data();
+            sp[i] = sources[i].data.data();
+            pp[i] = out[i].phi.disp.data.data();
+            wp[i] = out[i].warped.data.data();
+        }
+        std::vector<dreg_pair_result> pr(n);
+        std::vector<dreg_pair_record> rec(n);
+        const int st = dreg_cuda_multi_register_batch(
+            m_, static_cast<int>(n), tp.data(), sp.data(), b200_detail::D(d),
+            {targets[0].spacing.x, targets[0].spacing.y, targets[0].spacing.z}, &c, pp.data(), wp.data(), pr.data(),
+            rec.data());
+        if (st == DREG_INVALID_ARGUMENT) throw std::invalid_argument(dreg_cuda_multi_last_error(m_));
+        if (st == DREG_NUMERIC) throw numeric_error(dreg_cuda_multi_last_error(m_));
+        if (st != DREG_OK) throw std::runtime_error(dreg_cuda_multi_last_error(m_));
+        for (std::size_t i = 0; i < n; ++i) {
+            out[i].velocity_count = pr[i].velocity_count;
+            for (int l = 0; l < pr[i].levels; ++l) {
+                const dreg_level_log& lg = pr[i].per_level[l];
+                LevelLog o;
+                o.dims = {lg.dims.x, lg.dims.y, lg.dims.z};
+                o.warps = lg.warps;
+                o.mean_sad.assign(lg.mean_sad, lg.mean_sad + lg.warps + 1);
+                o.solver_iterations.assign(lg.solver_iterations, lg.solver_iterations + lg.warps);
+                out[i].per_level.push_back(std::move(o));
+            }
+            out[i].elapsed_seconds = pr[i].elapsed_seconds;
+        }
+        if (records) *records = std::move(rec);
+        return out;
+    }
+
+private:
+    dreg_cuda_multi* m_ = nullptr;
+};
+
 inline ScalarVolume warp_image(const ScalarVolume& img, const DeformationField& phi) {
     b200_detail::same(img.dims, phi.disp.dims, "warp_image");
     ScalarVolume out(img.dims, img.spacing);

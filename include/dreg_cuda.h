@@ -105,6 +105,10 @@ typedef struct {
     int levels;
     dreg_level_log per_level[DREG_MAX_LEVELS];
     double elapsed_seconds;
+    /* jacobian_stats(phi) of the returned phi (metrics.cpp:211-228), computed on the
+     * device in the final pass: interior voxels with fp32 det J <= 0 and their min. */
+    int64_t folding_voxels;
+    double min_det;
 } dreg_pair_result;
 
 /* dreg::JacobianStats (metrics.hpp:44-48) plus the raw counts. */
@@ -171,6 +175,52 @@ int dreg_cuda_register_batch_device(dreg_cuda_ctx* ctx, int n_pairs, const float
                                     float* phi_dev_out, float* warped_dev_out,
                                     dreg_pair_result* results);
 
+/* ---- multi-GPU batch (BASELINE config 3) ------------------------
+ * Independent pairs sharded over the devices of one box: shard s takes the
+ * contiguous pair range dreg_shard_range(n_pairs, n_devices, s), registered by one
+ * host thread driving its own per-device context.  No field data crosses devices.
+ * The only collective is ONE ncclAllGather of fixed-size per-pair records
+ * (dreg_pair_record, written on each device by the final registration pass) over
+ * NVLink / NVSwitch; the gathered records are returned in pair order.  NCCL
+ * (libnccl.so.2) is loaded at dreg_cuda_multi_create.  The reference has no
+ * multi-device path: every per-pair result equals dreg_cuda_register_batch's. */
+typedef struct {
+    int32_t pair;             /* global pair index; -1 marks gather padding */
+    int32_t device;           /* CUDA device that registered it */
+    int32_t status;           /* per-pair DREG_* status */
+    int32_t velocity_count;
+    int32_t solves;
+    int32_t levels;
+    int64_t folding_voxels;   /* interior det J <= 0 of the returned phi (metrics.cpp:211-228) */
+    int64_t admm_iterations;  /* ADMM iterations of the accepted velocity solves, all levels */
+    double final_mean_sad;    /* mean SAD after the last accepted warp at the finest level */
+    double min_det;           /* interior min det J */
+    int64_t reserved;
+} dreg_pair_record;          /* 64 bytes */
+
+typedef struct dreg_cuda_multi dreg_cuda_multi;
+
+/* One context per listed device + an NCCL communicator clique (ncclCommInitAll). */
+int dreg_cuda_multi_create(const int* devices, int n_devices, dreg_cuda_multi** out);
+void dreg_cuda_multi_destroy(dreg_cuda_multi* m);
+const char* dreg_cuda_multi_last_error(const dreg_cuda_multi* m);
+int dreg_cuda_multi_device_count(const dreg_cuda_multi* m);
+/* dreg_cuda_register_batch over all devices; results (nullable) and records
+ * (nullable, n_pairs entries, pair order) are host arrays.  Returns the first
+ * non-OK per-pair status (per-pair statuses are in results / records). */
+int dreg_cuda_multi_register_batch(dreg_cuda_multi* m, int n_pairs, const float* const* targets,
+                                   const float* const* sources, dreg_dims3 dims, dreg_spacing3 spacing,
+                                   const dreg_reg_cfg* cfg, float* const* phi_out,
+                                   float* const* warped_out, dreg_pair_result* results,
+                                   dreg_pair_record* records);
+/* Host helpers (pure, no device): the contiguous block [begin, end) of shard `shard`
+ * (sizes differ by at most one), and the inverse of the all-gather layout -- n_shards
+ * blocks of `cap` records, shard s's pairs first then padding -- into pair order.
+ * unpack returns DREG_INVALID_ARGUMENT unless every pair 0..n_pairs-1 appears once. */
+int dreg_shard_range(int n_pairs, int n_shards, int shard, int* begin, int* end);
+int dreg_records_unpack(const dreg_pair_record* gathered, int n_shards, int cap, int n_pairs,
+                        dreg_pair_record* out);
+
 /* ---- hot path: one velocity solve (admm.hpp:76-77) ----------------------------- */
 int dreg_cuda_solve_velocity(dreg_cuda_ctx* ctx, const float* target,
                              const float* warped_source, dreg_dims3 dims,
@@ -183,6 +233,10 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* ctx, const float* target,
  * events on the context stream.  out[0] = x-pass ms/launch, out[1] = plane ms/launch,
  * out[2] / out[3] = their algorithmic HBM bytes per launch, out[4] = pairs per launch. */
 int dreg_cuda_time_kernels(dreg_cuda_ctx* ctx, int reps, double* out);
+/* Same, with `cfg`'s data term / order / lambda / theta and the precision the
+ * context's policy picks for cfg->max_iters; out[5] = 1 when the precise (fp64
+ * spectral arithmetic) kernels were timed.  out holds 6 doubles. */
+int dreg_cuda_time_iteration(dreg_cuda_ctx* ctx, const dreg_solver_cfg* cfg, int reps, double* out);
 
 /* ---- DREG volume container (io.hpp:15-41; README.md:99-114) ---------------------
  * Host-only file I/O, byte-compatible with the reference.  Status DREG_IO_ERROR with

@@ -107,6 +107,26 @@ class PairResult(C.Structure):
         ("levels", C.c_int),
         ("per_level", LevelLog * DREG_MAX_LEVELS),
         ("elapsed_seconds", C.c_double),
+        ("folding_voxels", C.c_int64),  # jacobian_stats of the returned phi, computed on device
+        ("min_det", C.c_double),
+    ]
+
+
+class PairRecord(C.Structure):
+    """dreg_pair_record: the per-pair record of the multi-device all-gather (64 bytes)."""
+
+    _fields_ = [
+        ("pair", C.c_int32),
+        ("device", C.c_int32),
+        ("status", C.c_int32),
+        ("velocity_count", C.c_int32),
+        ("solves", C.c_int32),
+        ("levels", C.c_int32),
+        ("folding_voxels", C.c_int64),
+        ("admm_iterations", C.c_int64),
+        ("final_mean_sad", C.c_double),
+        ("min_det", C.c_double),
+        ("reserved", C.c_int64),
     ]
 
 

@@ -56,6 +56,8 @@ struct PairState {
     double sad_prev;
     double final_change;
     float lo, hi;          // shared intensity range (registration.cpp:157-166)
+    double folding;        // interior voxels with det J <= 0 of the final phi (metrics.cpp:211-228)
+    double min_det;        // interior min det J (fp32-cast values, metrics.cpp:222)
     int solver_iterations[DREG_MAX_LEVELS][DREG_MAX_WARPS];
     double mean_sad[DREG_MAX_LEVELS][DREG_MAX_WARPS + 1];
     int level_warps[DREG_MAX_LEVELS];

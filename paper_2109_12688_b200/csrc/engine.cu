@@ -879,6 +879,8 @@ void fill_results(const PairState* hs, int P, const std::vector<dreg_dims3>& dl,
             for (int i = 0; i < lg.warps && i < DREG_MAX_WARPS; ++i) lg.solver_iterations[i] = s.solver_iterations[l][i];
         }
         r.elapsed_seconds = elapsed;
+        r.folding_voxels = (int64_t)s.folding;
+        r.min_det = s.min_det;
     }
 }
 
@@ -1052,7 +1054,8 @@ int dreg_cuda_set_use_graphs(dreg_cuda_ctx* c, int enable) {
 static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_host, const float* const* src_host,
                          const float* tgt_dev, const float* src_dev, dreg_dims3 d, const dreg_reg_cfg* cfg,
                          float* const* phi_host, float* const* warped_host, float* phi_dev, float* warped_dev,
-                         dreg_pair_result* results) {
+                         dreg_pair_result* results, dreg_pair_record* rec_dev = nullptr, int pair_base = 0,
+                         int device_tag = 0) {
     const auto t0 = std::chrono::steady_clock::now();
     if (n_pairs < 0) throw ArgFail("n_pairs must be >= 0");
     validate_reg(cfg, d);
@@ -1138,6 +1141,10 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
             CK(cudaStreamWaitEvent(st, c->ev_d2h[slot], 0));  // chunk j-2's outputs left the slot
         }
         run_registration(c, lv, P, *cfg);
+        if (rec_dev) {  // per-pair records for the multi-device all-gather
+            CK(launch_pack_records(w.st.p, P, pair_base + p0, device_tag, cfg->levels, rec_dev + p0, st));
+            c->launches += 1;
+        }
         if (host) {
             for (int p = 0; p < P; ++p)
                 if (phi_host && phi_host[p0 + p]) {
@@ -1176,6 +1183,19 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
         return first_bad;
     }
     return DREG_OK;
+}
+
+// Internal (engine_internal.h): host-buffer batch that also writes each pair's
+// dreg_pair_record into the device buffer rec_dev (the multi-device gather's send buffer).
+int dregb_register_batch_records(dreg_cuda_ctx* c, int n_pairs, const float* const* targets,
+                                 const float* const* sources, dreg_dims3 dims, const dreg_reg_cfg* cfg,
+                                 float* const* phi_out, float* const* warped_out, dreg_pair_result* results,
+                                 dreg_pair_record* rec_dev, int pair_base, int device_tag) {
+    return guarded(c, [&] {
+        if (n_pairs > 0 && (!targets || !sources)) throw ArgFail("null input arrays");
+        return register_impl(c, n_pairs, targets, sources, nullptr, nullptr, dims, cfg, phi_out, warped_out,
+                             nullptr, nullptr, results, rec_dev, pair_base, device_tag);
+    });
 }
 
 int dreg_cuda_register_pair(dreg_cuda_ctx* c, const float* target, const float* source, dreg_dims3 dims,
@@ -1258,55 +1278,78 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
 }
 
 // ---- measurement ----------------------------------------------------------------
-int dreg_cuda_time_kernels(dreg_cuda_ctx* c, int reps, double* out) {
-    return guarded(c, [&] {
-        if (!c->last) throw ArgFail("time_kernels: no workspace yet (run a registration first)");
-        if (reps < 1 || !out) throw ArgFail("time_kernels: reps >= 1 and out required");
-        Workspace& w = *c->last;
-        const int P = w.P;
-        cudaStream_t st = c->stream;
-        dreg_solver_cfg s;
-        dreg_solver_cfg_default(&s);
+// CUDA-event timing of one steady-state ADMM iteration (plane + x-pass X_GENERAL) on
+// the last workspace, with `s`'s parameters and its precision policy (fp64 spectral
+// arithmetic when the policy picks it for s->max_iters).  out: [xpass ms, plane ms,
+// x-pass algorithmic bytes, plane algorithmic bytes, pairs, precise].
+static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, int reps, double* out) {
+    if (!c->last) throw ArgFail("time_kernels: no workspace yet (run a registration first)");
+    if (reps < 1 || !out) throw ArgFail("time_kernels: reps >= 1 and out required");
+    Workspace& w = *c->last;
+    const int P = w.P;
+    cudaStream_t st = c->stream;
+    dreg_solver_cfg s;
+    dreg_solver_cfg_default(&s);
+    if (scfg) {
+        check_solver(scfg);
+        s = *scfg;
+    } else {
         s.data_term = 2;
         s.lambda = 0.1;
         s.theta = 1.0;
-        const SolverParams sp = solver_params(s);
-        XArgs xa = make_xargs(w, sp, false);
-        xa.k = 5;
-        xa.coef = 0.5;
-        PArgs pa = make_pargs(w, sp, false);
-        Launcher L{c};
-        L(launch_state_reset(w.st.p, P, st));
-        cudaEvent_t e[4];
-        for (auto& ev : e) CK(cudaEventCreate(&ev));
-        // warm-up
+    }
+    s.log_objective = 0;
+    const bool precise = c->precision == 2 || (c->precision == 0 && s.max_iters > 100);
+    const SolverParams sp = solver_params(s);
+    XArgs xa = make_xargs(w, sp, false, precise);
+    xa.k = 5;
+    xa.coef = 0.5;
+    PArgs pa = make_pargs(w, sp, false, precise);
+    Launcher L{c};
+    L(launch_state_reset(w.st.p, P, st));
+    cudaEvent_t e[4];
+    for (auto& ev : e) CK(cudaEventCreate(&ev));
+    // warm-up
+    L(launch_plane(pa, 0, P, st));
+    L(launch_xpass(xa, X_GENERAL, P, st));
+    float tx = 0.f, tp = 0.f;
+    for (int r = 0; r < reps; ++r) {
+        CK(cudaEventRecord(e[0], st));
         L(launch_plane(pa, 0, P, st));
+        CK(cudaEventRecord(e[1], st));
         L(launch_xpass(xa, X_GENERAL, P, st));
-        float tx = 0.f, tp = 0.f;
-        for (int r = 0; r < reps; ++r) {
-            CK(cudaEventRecord(e[0], st));
-            L(launch_plane(pa, 0, P, st));
-            CK(cudaEventRecord(e[1], st));
-            L(launch_xpass(xa, X_GENERAL, P, st));
-            CK(cudaEventRecord(e[2], st));
-            CK(cudaEventSynchronize(e[2]));
-            float a = 0.f, b = 0.f;
-            CK(cudaEventElapsedTime(&a, e[0], e[1]));
-            CK(cudaEventElapsedTime(&b, e[1], e[2]));
-            tp += a;
-            tx += b;
-        }
-        for (auto& ev : e) cudaEventDestroy(ev);
-        c->launches += L.count;
-        const double N = (double)w.geo.N;
-        const double spec = 2.0 * 3.0 * (double)w.geo.hx * (double)w.geo.lines * 8.0;  // read + write
-        out[0] = tx / reps;
-        out[1] = tp / reps;
-        out[2] = P * (28.0 * 4.0 * N + spec);  // 16 field words read + 12 written, spectrum in/out
-        out[3] = P * spec;
-        out[4] = P;
-        return DREG_OK;
+        CK(cudaEventRecord(e[2], st));
+        CK(cudaEventSynchronize(e[2]));
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, e[0], e[1]));
+        CK(cudaEventElapsedTime(&b, e[1], e[2]));
+        tp += a;
+        tx += b;
+    }
+    for (auto& ev : e) cudaEventDestroy(ev);
+    c->launches += L.count;
+    const double N = (double)w.geo.N;
+    const double spec = 2.0 * 3.0 * (double)w.geo.hx * (double)w.geo.lines * 8.0;  // read + write
+    out[0] = tx / reps;
+    out[1] = tp / reps;
+    out[2] = P * (28.0 * 4.0 * N + spec);  // 16 field words read + 12 written, spectrum in/out
+    out[3] = P * spec;
+    out[4] = P;
+    out[5] = precise ? 1.0 : 0.0;
+    return DREG_OK;
+}
+
+int dreg_cuda_time_kernels(dreg_cuda_ctx* c, int reps, double* out) {
+    return guarded(c, [&] {
+        double o[6];
+        const int r = time_iteration_impl(c, nullptr, reps, o);
+        for (int i = 0; i < 5; ++i) out[i] = o[i];
+        return r;
     });
+}
+
+int dreg_cuda_time_iteration(dreg_cuda_ctx* c, const dreg_solver_cfg* cfg, int reps, double* out) {
+    return guarded(c, [&] { return time_iteration_impl(c, cfg, reps, out); });
 }
 
 // ---- building blocks ------------------------------------------------------------

@@ -230,6 +230,8 @@ __global__ void state_reset_kernel(PairState* st, int npairs) {
     s.done_iter = -1;
     s.sad_prev = 0.0;
     s.final_change = 0.0;
+    s.folding = 0.0;
+    s.min_det = 0.0;
     for (int l = 0; l < DREG_MAX_LEVELS; ++l) s.level_warps[l] = 0;
 }
 
@@ -322,18 +324,45 @@ cudaError_t launch_level_init(VolGeom g, const RegBuffers& R, Fields F, int leve
     return cudaGetLastError();
 }
 
-// ---- end of registration: finiteness of phi, phi out, warp of the ORIGINAL source
+// det J of I + grad u at voxel (x, y, z) (volume.cpp:183-230): fp64 differences with
+// one-sided faces, cofactor expansion along row 0, rounded to fp32 like the stored
+// determinant volume (:224)
+__device__ __forceinline__ float jacobian_det(const VolGeom& g, const float* __restrict__ u, long long i, int x, int y,
+                                              int z) {
+    const long long N = g.N;
+    const size_t sy = (size_t)g.M, sz = (size_t)g.M * g.Ny;
+    double j[3][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float* uc = u + (size_t)c * N;
+        j[c][0] = diff1(uc, i, x, g.M, 1) + (c == 0 ? 1.0 : 0.0);
+        j[c][1] = diff1(uc, i, y, g.Ny, sy) + (c == 1 ? 1.0 : 0.0);
+        j[c][2] = diff1(uc, i, z, g.Nz, sz) + (c == 2 ? 1.0 : 0.0);
+    }
+    const double value = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
+                         j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
+                         j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
+    return (float)value;
+}
+
+__device__ __forceinline__ bool interior(const VolGeom& g, int x, int y, int z) {
+    return x >= 1 && x < g.M - 1 && y >= 1 && y < g.Ny - 1 && z >= 1 && z < g.Nz - 1;
+}
+
+// ---- end of registration: finiteness of phi, phi out, warp of the ORIGINAL source,
+// and the folding record of the final phi (jacobian_stats, metrics.cpp:211-228) -----
 __global__ void __launch_bounds__(kVT) finalize_kernel(VolGeom g, RegBuffers R, Fields F) {
     __shared__ double red[32];
     const int pair = blockIdx.y;
     PairState* st = F.st + pair;
     if (st->status) return;
     const long long N = g.N;
-    const float* phi = (st->cur ? R.PHI[1] : R.PHI[0]) + (size_t)pair * 3 * N;
+    const float* __restrict__ phi = (st->cur ? R.PHI[1] : R.PHI[0]) + (size_t)pair * 3 * N;
     const float* src = R.src_in[pair];
     float* po = R.phi_out ? R.phi_out[pair] : nullptr;
     float* wo = R.warped_out ? R.warped_out[pair] : nullptr;
-    double bad = 0.0;
+    const bool jac = g.M >= 3 && g.Ny >= 3 && g.Nz >= 3;
+    double bad = 0.0, nonpos = 0.0, mind = 1e300;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
          i += (long long)gridDim.x * blockDim.x) {
         int x, y, z;
@@ -346,12 +375,21 @@ __global__ void __launch_bounds__(kVT) finalize_kernel(VolGeom g, RegBuffers R, 
             po[2 * N + i] = u2;
         }
         if (wo) wo[i] = (float)trilinear(src, g.M, g.Ny, g.Nz, x + (double)u0, y + (double)u1, z + (double)u2);
+        if (jac && interior(g, x, y, z)) {
+            const double d = (double)jacobian_det(g, phi, i, x, y, z);
+            mind = fmin(mind, d);
+            nonpos += d <= 0.0 ? 1.0 : 0.0;
+        }
     }
-    const double vals[1] = {block_sum<kVT>(bad, red)};
-    double tot[1];
-    if (reduce_partials<kVT, 1>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red) &&
-        threadIdx.x == 0 && tot[0] > 0.0)
-        st->status = DREG_NUMERIC;  // registration.cpp:275-277
+    const double vals[3] = {block_sum<kVT>(bad, red), block_sum<kVT>(nonpos, red), block_min<kVT>(mind, red)};
+    double tot[3];
+    if (reduce_partials<kVT, 3>(vals, F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, gridDim.x, tot, red,
+                                0x4u) &&
+        threadIdx.x == 0) {
+        st->folding = tot[1];
+        st->min_det = jac ? tot[2] : 0.0;
+        if (tot[0] > 0.0) st->status = DREG_NUMERIC;  // registration.cpp:275-277
+    }
 }
 
 cudaError_t launch_finalize(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s) {
@@ -364,27 +402,14 @@ __global__ void __launch_bounds__(kVT) jacobian_kernel(VolGeom g, const float* _
                                                        double* part, double* out3, unsigned int* counter) {
     __shared__ double red[32];
     const long long N = g.N;
-    const size_t sy = (size_t)g.M, sz = (size_t)g.M * g.Ny;
     double nonpos = 0.0, mind = 1e300;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
          i += (long long)gridDim.x * blockDim.x) {
         int x, y, z;
         unflat(i, g.M, g.Ny, x, y, z);
-        double j[3][3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float* uc = u + (size_t)c * N;
-            j[c][0] = diff1(uc, i, x, g.M, 1) + (c == 0 ? 1.0 : 0.0);
-            j[c][1] = diff1(uc, i, y, g.Ny, sy) + (c == 1 ? 1.0 : 0.0);
-            j[c][2] = diff1(uc, i, z, g.Nz, sz) + (c == 2 ? 1.0 : 0.0);
-        }
-        // cofactor expansion along row 0 (volume.cpp:221-223), stored as fp32 (:224)
-        const double value = j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -
-                             j[0][1] * (j[1][0] * j[2][2] - j[1][2] * j[2][0]) +
-                             j[0][2] * (j[1][0] * j[2][1] - j[1][1] * j[2][0]);
-        const float dv = (float)value;
+        const float dv = jacobian_det(g, u, i, x, y, z);
         if (det) det[i] = dv;
-        if (x >= 1 && x < g.M - 1 && y >= 1 && y < g.Ny - 1 && z >= 1 && z < g.Nz - 1) {
+        if (interior(g, x, y, z)) {
             const double d = (double)dv;  // metrics.cpp:217-227 compares the fp32 value
             mind = fmin(mind, d);
             nonpos += d <= 0.0 ? 1.0 : 0.0;
@@ -713,6 +738,42 @@ cudaError_t launch_soa_to_aos(long long N, const float* soa, float* aos, cudaStr
 }
 cudaError_t launch_add(long long n, const float* a, const float* b, float* out, cudaStream_t s) {
     add_kernel<<<voxel_blocks(n), kVT, 0, s>>>(n, a, b, out);
+    return cudaGetLastError();
+}
+
+}  // namespace dregb
+
+namespace dregb {
+
+// Per-pair records for the multi-device all-gather (dreg_pair_record), one thread per
+// pair, written straight from the device-side pair state after the final pass.
+__global__ void pack_records_kernel(const PairState* st, int npairs, int pair_base, int device, int levels,
+                                    dreg_pair_record* out) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= npairs) return;
+    const PairState& s = st[p];
+    dreg_pair_record r;
+    r.pair = pair_base + p;
+    r.device = device;
+    r.status = s.status;
+    r.velocity_count = s.velocity_count;
+    r.solves = s.solves;
+    r.levels = levels;
+    r.folding_voxels = (int64_t)s.folding;
+    long long iters = 0;
+    for (int l = 0; l < levels && l < DREG_MAX_LEVELS; ++l)
+        for (int w = 0; w < s.level_warps[l] && w < DREG_MAX_WARPS; ++w) iters += s.solver_iterations[l][w];
+    r.admm_iterations = iters;
+    const int lf = levels - 1, wf = s.level_warps[lf] < DREG_MAX_WARPS ? s.level_warps[lf] : DREG_MAX_WARPS;
+    r.final_mean_sad = s.mean_sad[lf][wf];
+    r.min_det = s.min_det;
+    r.reserved = 0;
+    out[p] = r;
+}
+
+cudaError_t launch_pack_records(const PairState* st, int npairs, int pair_base, int device, int levels,
+                                dreg_pair_record* out, cudaStream_t s) {
+    pack_records_kernel<<<(npairs + 127) / 128, 128, 0, s>>>(st, npairs, pair_base, device, levels, out);
     return cudaGetLastError();
 }
 

@@ -145,6 +145,10 @@ cudaError_t launch_hausdorff_slices(VolGeom g, const uint16_t* a, const uint16_t
                                     double sx, double sy, int ctas, double* scratch, int* iscratch, double* worst,
                                     cudaStream_t s);
 
+// per-pair dreg_pair_record of the multi-device all-gather
+cudaError_t launch_pack_records(const PairState* st, int npairs, int pair_base, int device, int levels,
+                                dreg_pair_record* out, cudaStream_t s);
+
 cudaError_t launch_aos_to_soa(long long N, const float* aos, float* soa, cudaStream_t s);
 cudaError_t launch_soa_to_aos(long long N, const float* soa, float* aos, cudaStream_t s);
 cudaError_t launch_add(long long n, const float* a, const float* b, float* out, cudaStream_t s);

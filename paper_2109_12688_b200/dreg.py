@@ -88,6 +88,7 @@ def load_library() -> C.CDLL:
     ]
     L.dreg_cuda_solve_velocity.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F, C.POINTER(abi.SolverDiag)]
     L.dreg_cuda_time_kernels.argtypes = [P, C.c_int, _D]
+    L.dreg_cuda_time_iteration.argtypes = [P, C.POINTER(SolverCfg), C.c_int, _D]
     L.dreg_cuda_v_update.argtypes = [P, _F, _F, _F, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
     L.dreg_cuda_w_update.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
     L.dreg_cuda_regulariser_energy.argtypes = [P, _F, Dims3, C.c_int, _D]
@@ -110,6 +111,19 @@ def load_library() -> C.CDLL:
     L.dreg_cuda_dice.argtypes = [P, V, V, Dims3, C.c_int, _D]
     L.dreg_cuda_hausdorff_slice_avg.argtypes = [P, V, V, Dims3, Spacing3, C.c_int, _D]
     L.dreg_cuda_label_metrics.argtypes = [P, V, V, Dims3, Spacing3, C.c_int, V, V, V, V]
+    PR = C.POINTER(abi.PairRecord)
+    L.dreg_cuda_multi_create.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(P)]
+    L.dreg_cuda_multi_destroy.argtypes = [P]
+    L.dreg_cuda_multi_destroy.restype = None
+    L.dreg_cuda_multi_last_error.argtypes = [P]
+    L.dreg_cuda_multi_last_error.restype = C.c_char_p
+    L.dreg_cuda_multi_device_count.argtypes = [P]
+    L.dreg_cuda_multi_register_batch.argtypes = [
+        P, C.c_int, C.POINTER(_F), C.POINTER(_F), Dims3, Spacing3, C.POINTER(RegCfg),
+        C.POINTER(_F), C.POINTER(_F), C.POINTER(PairResult), PR,
+    ]
+    L.dreg_shard_range.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.dreg_records_unpack.argtypes = [PR, C.c_int, C.c_int, C.c_int, PR]
     _lib = L
     return L
 
@@ -122,11 +136,16 @@ def _f32(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.float32)
 
 
-def _raise(status: int, msg: str):
+def _raise(status: int, msg: str, results=None):
+    """Map a status to the reference's exception types.  Batch calls attach every
+    pair's result (per-pair `status`) to a NumericError as `.results`, so one bad pair
+    does not lose the other pairs' outputs."""
     if status == abi.DREG_INVALID_ARGUMENT:
         raise ValueError(msg)
     if status == abi.DREG_NUMERIC:
-        raise NumericError(msg)
+        e = NumericError(msg)
+        e.results = results
+        raise e
     raise RuntimeError(msg or f"dreg_cuda status {status}")
 
 
@@ -236,6 +255,68 @@ def write_report(path, *, dice=None, hausdorff_mm=None, jacobian_pct_nonpositive
     _io_check(load_library().dreg_report_write(os.fsencode(str(path)), C.byref(rep), err, 1024), err)
 
 
+def shard_range(n_pairs: int, n_shards: int, shard: int) -> tuple[int, int]:
+    """[begin, end) of a shard's contiguous pair block (dreg_shard_range)."""
+    b, e = C.c_int(), C.c_int()
+    st = load_library().dreg_shard_range(n_pairs, n_shards, shard, C.byref(b), C.byref(e))
+    if st != abi.DREG_OK:
+        raise ValueError("dreg_shard_range: bad arguments")
+    return b.value, e.value
+
+
+class MultiContext:
+    """Pairs sharded over several GPUs (dreg_cuda_multi): one host thread + context per
+    device inside the library, one NCCL all-gather of the per-pair records."""
+
+    def __init__(self, devices):
+        self.lib = load_library()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        st = self.lib.dreg_cuda_multi_create(devs, len(devices), C.byref(h))
+        if st != abi.DREG_OK:
+            raise RuntimeError(f"dreg_cuda_multi_create({list(devices)}) failed with status {st}")
+        self.h = h
+        self.devices = list(devices)
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.dreg_cuda_multi_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def register_batch(self, targets, sources, cfg: RegCfg, spacing=(1.0, 1.0, 1.0)):
+        """-> (phis, warped, results, records), records in pair order."""
+        targets = [_f32(t) for t in targets]
+        sources = [_f32(s) for s in sources]
+        n = len(targets)
+        shape = targets[0].shape
+        phis = [np.zeros(shape + (3,), np.float32) for _ in range(n)]
+        warps = [np.zeros(shape, np.float32) for _ in range(n)]
+        T = (_F * n)(*[_fp(t) for t in targets])
+        S = (_F * n)(*[_fp(s) for s in sources])
+        PO = (_F * n)(*[_fp(p) for p in phis])
+        WO = (_F * n)(*[_fp(w) for w in warps])
+        res = (PairResult * n)()
+        rec = (abi.PairRecord * n)()
+        st = self.lib.dreg_cuda_multi_register_batch(self.h, n, T, S, abi.dims3(targets[0]), Spacing3(*spacing),
+                                                     C.byref(cfg), PO, WO, res, rec)
+        if st != abi.DREG_OK:
+            _raise(st, self.lib.dreg_cuda_multi_last_error(self.h).decode(),
+                   (phis, warps, list(res), list(rec)) if st == abi.DREG_NUMERIC else None)
+        return phis, warps, list(res), list(rec)
+
+
 class Context:
     """One CUDA device context (dreg_cuda_ctx).  Not thread-safe; one per thread/GPU."""
 
@@ -326,23 +407,23 @@ class Context:
         PO = (_F * n)(*[_fp(p) for p in phis]) if phis else None
         WO = (_F * n)(*[_fp(w) for w in warps]) if warps else None
         res = (PairResult * n)()
-        self._check(
-            self.lib.dreg_cuda_register_batch(
-                self.h, n, T, S, abi.dims3(targets[0]), Spacing3(*spacing), C.byref(cfg), PO, WO, res
-            )
-        )
+        st = self.lib.dreg_cuda_register_batch(self.h, n, T, S, abi.dims3(targets[0]), Spacing3(*spacing),
+                                               C.byref(cfg), PO, WO, res)
+        if st != abi.DREG_OK:
+            _raise(st, self.lib.dreg_cuda_last_error(self.h).decode(),
+                   (phis, warps, list(res)) if st == abi.DREG_NUMERIC else None)
         return phis, warps, list(res)
 
     def register_batch_device(self, n: int, targets_ptr: int, sources_ptr: int, dims, cfg: RegCfg,
                               phi_ptr: int = 0, warped_ptr: int = 0):
         """Device-resident batch: [n][voxels] inputs, [n][3][voxels] SoA phi output."""
         res = (PairResult * n)()
-        self._check(
-            self.lib.dreg_cuda_register_batch_device(
-                self.h, n, C.c_void_p(targets_ptr), C.c_void_p(sources_ptr), abi.dims3(dims), Spacing3(1, 1, 1),
-                C.byref(cfg), C.c_void_p(phi_ptr or 0), C.c_void_p(warped_ptr or 0), res,
-            )
+        st = self.lib.dreg_cuda_register_batch_device(
+            self.h, n, C.c_void_p(targets_ptr), C.c_void_p(sources_ptr), abi.dims3(dims), Spacing3(1, 1, 1),
+            C.byref(cfg), C.c_void_p(phi_ptr or 0), C.c_void_p(warped_ptr or 0), res,
         )
+        if st != abi.DREG_OK:
+            _raise(st, self.lib.dreg_cuda_last_error(self.h).decode(), list(res) if st == abi.DREG_NUMERIC else None)
         return list(res)
 
     def solve_velocity(self, target, warped_source, cfg: SolverCfg):
@@ -369,11 +450,16 @@ class Context:
             "constraint_residual": res[:it].copy(),
         }
 
-    def time_kernels(self, reps: int = 20) -> dict:
-        """CUDA-event timing of the per-iteration kernels on the current workspace."""
-        out = np.zeros(5, np.float64)
-        self._check(self.lib.dreg_cuda_time_kernels(self.h, reps, out.ctypes.data_as(_D)))
-        return {"xpass_ms": out[0], "plane_ms": out[1], "xpass_bytes": out[2], "plane_bytes": out[3], "pairs": int(out[4])}
+    def time_kernels(self, reps: int = 20, solver: SolverCfg | None = None) -> dict:
+        """CUDA-event timing of the per-iteration kernels on the current workspace
+        (with `solver`'s parameters and precision policy when given)."""
+        out = np.zeros(6, np.float64)
+        if solver is None:
+            self._check(self.lib.dreg_cuda_time_kernels(self.h, reps, out.ctypes.data_as(_D)))
+        else:
+            self._check(self.lib.dreg_cuda_time_iteration(self.h, C.byref(solver), reps, out.ctypes.data_as(_D)))
+        return {"xpass_ms": out[0], "plane_ms": out[1], "xpass_bytes": out[2], "plane_bytes": out[3],
+                "pairs": int(out[4]), "precise": int(out[5])}
 
     # ---- building blocks ---------------------------------------------------------
     def v_update(self, target, warped, grad, w_hat, b_hat, cfg: SolverCfg) -> np.ndarray:

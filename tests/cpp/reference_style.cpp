@@ -120,6 +120,20 @@ int main() {
     const std::string text((std::istreambuf_iterator<char>(rf)), std::istreambuf_iterator<char>());
     CHECK(text.find("\"velocity_count\": " + std::to_string(res.velocity_count)) != std::string::npos);
 
+    // B200 extension: the same pairs sharded over the box's GPUs (here: device 0),
+    // NCCL all-gather of the per-pair records; results equal register_pair's
+    {
+        dreg::MultiDevice multi({0});
+        std::vector<dreg_pair_record> rec;
+        const auto mres = multi.register_batch({target, target}, {source, source}, cfg, &rec);
+        CHECK(mres.size() == 2 && rec.size() == 2);
+        for (int i = 0; i < 2; ++i) {
+            CHECK(mres[i].phi.disp.data == res.phi.disp.data);
+            CHECK(rec[i].pair == i && rec[i].velocity_count == res.velocity_count);
+            CHECK(rec[i].folding_voxels == 0 && rec[i].min_det == js.min_det);
+        }
+    }
+
     std::printf("reference-style C++ client OK: velocity_count %d, min det %.4f\n", res.velocity_count, js.min_det);
     return 0;
 }

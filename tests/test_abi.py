@@ -70,6 +70,7 @@ STRUCTS = {
     "dreg_level_log": abi.LevelLog,
     "dreg_pair_result": abi.PairResult,
     "dreg_jacobian_stats": abi.JacobianStats,
+    "dreg_pair_record": abi.PairRecord,
     "dreg_volume_info": abi.VolumeInfo,
     "dreg_report_config": abi.ReportConfig,
     "dreg_run_report": abi.RunReport,

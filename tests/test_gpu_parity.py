@@ -420,8 +420,10 @@ def test_batch_isolates_bad_pair(ctx, oracle):
     M[1, 2, 3, 4] = np.nan
     s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=20, log_objective=False)
     cfg = abi.reg_cfg(s, 1, (3,), (20,))
-    with pytest.raises(dreg.NumericError):
+    with pytest.raises(dreg.NumericError) as ei:
         ctx.register_batch(list(F), list(M), cfg)
+    phis_e, _, res_e = ei.value.results  # the other pairs' outputs survive the exception
+    assert [r.status for r in res_e] == [0, abi.DREG_NUMERIC, 0]
     import ctypes as C
 
     n = 3
@@ -438,6 +440,7 @@ def test_batch_isolates_bad_pair(ctx, oracle):
     for i in (0, 2):
         po, _, _ = oracle.register_pair(F[i], M[i], cfg)
         assert max_abs(phis[i], po) <= PHI_MAX_ABS
+        assert np.array_equal(phis_e[i], phis[i])
 
 
 @pytest.mark.slow
