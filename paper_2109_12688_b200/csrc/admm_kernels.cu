@@ -22,36 +22,40 @@ namespace dregb {
 constexpr int kXThreads = 256;
 constexpr int kPThreads = 512;
 
+// C = float2 (fp32 x-FFT) or double2 (precise mode: fp64 butterflies and twiddles)
+template <class C>
 struct XSmem {
-    float2* twx;
-    float2* xtw;
+    C* twx;
+    C* xtw;
     int* xpos;
-    float2* buf;
-    float2* Xs;
+    C* buf;
+    C* Xs;
     double* red;
 };
 
-__device__ __forceinline__ XSmem carve_x(unsigned char* smem, int L, int hx, int TL, int PM) {
-    XSmem s;
+template <class C>
+__device__ __forceinline__ XSmem<C> carve_x(unsigned char* smem, int L, int hx, int TL, int PM) {
+    XSmem<C> s;
     size_t off = 0;
-    s.twx = reinterpret_cast<float2*>(smem + off);
-    off += sizeof(float2) * L;
-    s.xtw = reinterpret_cast<float2*>(smem + off);
-    off += sizeof(float2) * (hx + 1);
-    s.buf = reinterpret_cast<float2*>(smem + off);
-    off += sizeof(float2) * 3 * TL * PM;
-    s.Xs = reinterpret_cast<float2*>(smem + off);
-    off += sizeof(float2) * hx * TL;
+    s.twx = reinterpret_cast<C*>(smem + off);
+    off += sizeof(C) * L;
+    s.xtw = reinterpret_cast<C*>(smem + off);
+    off += sizeof(C) * (hx + 1);
+    s.buf = reinterpret_cast<C*>(smem + off);
+    off += sizeof(C) * 3 * TL * PM;
+    s.Xs = reinterpret_cast<C*>(smem + off);
+    off += sizeof(C) * hx * TL;
     s.red = reinterpret_cast<double*>(smem + off);
     off += sizeof(double) * 32;
     s.xpos = reinterpret_cast<int*>(smem + off);
     return s;
 }
 
-size_t xpass_smem_bytes(int L, int hx, int TL, int PM) {
-    return sizeof(float2) * (L + hx + 1 + 3 * (size_t)TL * PM + (size_t)hx * TL) + sizeof(double) * 32 +
-           sizeof(int) * L;
+size_t xpass_smem_bytes_c(int L, int hx, int TL, int PM, size_t csz) {
+    return csz * (L + hx + 1 + 3 * (size_t)TL * PM + (size_t)hx * TL) + sizeof(double) * 32 + sizeof(int) * L;
 }
+
+size_t xpass_smem_bytes(int L, int hx, int TL, int PM) { return xpass_smem_bytes_c(L, hx, TL, PM, sizeof(float2)); }
 
 template <int VEC>
 __device__ __forceinline__ void ldv(const float* p, float* out) {
@@ -73,8 +77,9 @@ __device__ __forceinline__ void stv(float* p, const float* in) {
     }
 }
 
-template <int MODE, int DT, int VEC, bool F64 = false, int MINB = 3>
+template <int MODE, int DT, int VEC, bool F64 = false, int MINB = 3, class C = float2>
 __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass_kernel(XArgs a) {
+    using R = decltype(C::x);
     const int pair = blockIdx.y;
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
 
     extern __shared__ __align__(16) unsigned char smem[];
     const int L = a.px.n, M = a.F.M, hx = a.F.hx, TL = a.TL, PM = a.PM;
-    XSmem sm = carve_x(smem, L, hx, TL, PM);
+    XSmem<C> sm = carve_x<C>(smem, L, hx, TL, PM);
     const int tid = threadIdx.x, nthr = blockDim.x;
     const long long lines = a.F.lines;
     const long long L0 = (long long)blockIdx.x * TL;
@@ -93,11 +98,20 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
     const int lt = 31 - __clz(TL);  // TL is a power of two
     const int tm = TL - 1;
 
+    const C* twx_g;
+    const C* xtw_g;
+    if constexpr (sizeof(C) == 16) {
+        twx_g = a.twx64;
+        xtw_g = a.xtw64;
+    } else {
+        twx_g = a.twx;
+        xtw_g = a.xtw;
+    }
     for (int i = tid; i < L; i += nthr) {
-        sm.twx[i] = a.twx[i];
+        sm.twx[i] = twx_g[i];
         sm.xpos[i] = a.xpos[i];
     }
-    for (int i = tid; i <= hx; i += nthr) sm.xtw[i] = a.xtw[i];
+    for (int i = tid; i <= hx; i += nthr) sm.xtw[i] = xtw_g[i];
     __syncthreads();
 
     float* V = a.F.V + (size_t)pair * 3 * N;
@@ -132,27 +146,27 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             const float2* Sc = S + (size_t)c * hx * lines;
             for (int idx = tid; idx < hx * TL; idx += nthr) {
                 const int p = idx >> lt, l = idx & tm;
-                sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? Sc[(size_t)p * lines + L0 + l] : make_float2(0.f, 0.f);
+                sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? cvt_c<C>(Sc[(size_t)p * lines + L0 + l]) : CT<C>::make(0, 0);
             }
             __syncthreads();
-            float2* bc = sm.buf + (size_t)c * TL * PM;
+            C* bc = sm.buf + (size_t)c * TL * PM;
             if (!a.odd) {
                 // Z'[k] = E + i O with E = X[k] + conj(X[L-k]), O = (X[k] - conj(X[L-k])) W_M^{-k};
                 // imaginary parts of the self-conjugate bins ignored (1-D c2r semantics).
                 for (int idx = tid; idx < L * TL; idx += nthr) {
                     const int k = idx >> lt, l = idx & tm;
-                    float2 A = sm.Xs[k * TL + l];
-                    float2 B = sm.Xs[(L - k) * TL + l];
+                    C A = sm.Xs[k * TL + l];
+                    C B = sm.Xs[(L - k) * TL + l];
                     if (k == 0) { A.y = 0.f; B.y = 0.f; }
                     B.y = -B.y;
-                    const float2 e = cadd(A, B);
-                    const float2 o = cmulc(csub(A, B), sm.xtw[k]);
-                    bc[l * PM + sm.xpos[k]] = make_float2(e.x - o.y, e.y + o.x);
+                    const C e = cadd(A, B);
+                    const C o = cmulc(csub(A, B), sm.xtw[k]);
+                    bc[l * PM + sm.xpos[k]] = CT<C>::make(e.x - o.y, e.y + o.x);
                 }
             } else {
                 for (int idx = tid; idx < M * TL; idx += nthr) {
                     const int k = idx >> lt, l = idx & tm;
-                    float2 X;
+                    C X;
                     if (k < hx) {
                         X = sm.Xs[k * TL + l];
                         if (k == 0) X.y = 0.f;
@@ -173,14 +187,14 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
         for (int i = tid; i < 3 * nvox; i += nthr) {
             const int c = i / nvox, r = i - c * nvox;
             const int l = r / M, x = r - l * M;
-            float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+            C* bl = sm.buf + (size_t)(c * TL + l) * PM;
             const size_t gi = (size_t)c * N + base + r;
             if (MODE == X_FWD) {
-                const float u = a.add_bh ? V[gi] + BH[gi] : V[gi];
-                if (!a.odd) reinterpret_cast<float*>(bl)[x] = u;
-                else bl[x] = make_float2(u, 0.f);
+                const R u = a.add_bh ? (R)V[gi] + (R)BH[gi] : (R)V[gi];  // admm.cpp:77-80
+                if (!a.odd) reinterpret_cast<R*>(bl)[x] = u;
+                else bl[x] = CT<C>::make(u, 0);
             } else {
-                WP[gi] = !a.odd ? reinterpret_cast<const float*>(bl)[x] : bl[x].x;
+                WP[gi] = (float)(!a.odd ? reinterpret_cast<const R*>(bl)[x] : bl[x].x);
             }
         }
         if (MODE == X_INV) return;
@@ -215,10 +229,10 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             if (MODE != X_TAIL) ldv<VEC>(Dd + gi, dv);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+                const C* bl = sm.buf + (size_t)(c * TL + l) * PM;
 #pragma unroll
                 for (int j = 0; j < VEC; ++j) {
-                    w[c][j] = MODE == X_FIRST ? 0.f : (!a.odd ? reinterpret_cast<const float*>(bl)[x0 + j] : bl[x0 + j].x);
+                    w[c][j] = MODE == X_FIRST ? 0.f : (float)(!a.odd ? reinterpret_cast<const R*>(bl)[x0 + j] : bl[x0 + j].x);
                     if (MODE == X_FIRST) vp[c][j] = 0.f;
                     if (MODE != X_GENERAL) bo[c][j] = 0.f;
                 }
@@ -280,11 +294,12 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
                 }
                 stv<VEC>(V + (size_t)c * N + gi, vn[c]);
                 if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bh[c]);
-                float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+                C* bl = sm.buf + (size_t)(c * TL + l) * PM;
 #pragma unroll
                 for (int j = 0; j < VEC; ++j) {
-                    if (!a.odd) reinterpret_cast<float*>(bl)[x0 + j] = vn[c][j] + bh[c][j];
-                    else bl[x0 + j] = make_float2(vn[c][j] + bh[c][j], 0.f);
+                    const R u = (R)vn[c][j] + (R)bh[c][j];
+                    if (!a.odd) reinterpret_cast<R*>(bl)[x0 + j] = u;
+                    else bl[x0 + j] = CT<C>::make(u, 0);
                 }
             }
         }
@@ -299,14 +314,14 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
         if (MODE != X_FIRST) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+                const C* bl = sm.buf + (size_t)(c * TL + l) * PM;
                 if (!a.odd) {
-                    const float* wl = reinterpret_cast<const float*>(bl);
+                    const R* wl = reinterpret_cast<const R*>(bl);
 #pragma unroll
-                    for (int j = 0; j < VEC; ++j) w[c][j] = wl[x0 + j];
+                    for (int j = 0; j < VEC; ++j) w[c][j] = (float)wl[x0 + j];  // w stored as float (admm.cpp:97-99)
                 } else {
 #pragma unroll
-                    for (int j = 0; j < VEC; ++j) w[c][j] = bl[x0 + j].x;
+                    for (int j = 0; j < VEC; ++j) w[c][j] = (float)bl[x0 + j].x;
                 }
                 ldv<VEC>(V + (size_t)c * N + gi, vp[c]);
             }
@@ -354,10 +369,10 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
                     ldv<VEC>(WP + (size_t)c * N + gi, wp);
                     ldv<VEC>(BP + (size_t)c * N + gi, bp);
 #pragma unroll
-                    for (int j = 0; j < VEC; ++j) {
+                    for (int j = 0; j < VEC; ++j) {  // av + scale * (av - b), unfused like the reference
                         const double aw = w[c][j], ab = b[j];
-                        wh[c][j] = (float)(aw + coef * (aw - (double)wp[j]));
-                        bh[c][j] = (float)(ab + coef * (ab - (double)bp[j]));
+                        wh[c][j] = (float)__dadd_rn(aw, __dmul_rn(coef, __dsub_rn(aw, (double)wp[j])));
+                        bh[c][j] = (float)__dadd_rn(ab, __dmul_rn(coef, __dsub_rn(ab, (double)bp[j])));
                     }
                 } else {
                     // coefficient is exactly 0 (first step, or accelerate off)
@@ -370,10 +385,11 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
                 }
             }
         }
-        float g[3][VEC], dv[VEC];
+        float g[3][VEC], dv[VEC], tv[VEC];
 #pragma unroll
         for (int c = 0; c < 3; ++c) ldv<VEC>(G + (size_t)c * N + gi, g[c]);
         ldv<VEC>(Dd + gi, dv);
+        if (DT == 1) ldv<VEC>(a.F.T + (size_t)pair * N + gi, tv);  // l1: D = warped, residual from both
         float vn[3][VEC];
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
@@ -381,30 +397,35 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             const float bhj[3] = {bh[0][j], bh[1][j], bh[2][j]};
             const float gj[3] = {g[0][j], g[1][j], g[2][j]};
             float vj[3];
-            v_update_voxel<DT>(whj, bhj, gj, (double)dv[j], theta, inv_theta, eps, vj);
+            if (DT == 1) v_update_voxel_exact<1>(whj, bhj, gj, dv[j], tv[j], theta, eps, vj);
+            else v_update_voxel<DT>(whj, bhj, gj, (double)dv[j], theta, inv_theta, eps, vj);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 vn[c][j] = vj[c];
                 s_change += fabs((double)vj[c] - (double)vp[c][j]);
             }
             if (a.sp.log_objective) {
-                const double rho = ((double)gj[0] * vj[0] + (double)gj[1] * vj[1] + (double)gj[2] * vj[2]) +
-                                   (double)dv[j];
-                s_obj += DT == 1 ? fabs(rho) : 0.5 * rho * rho;
+                if (DT == 1) {
+                    s_obj += fabs(data_residual_exact(gj, vj, dv[j], tv[j]));
+                } else {
+                    const double rho = ((double)gj[0] * vj[0] + (double)gj[1] * vj[1] + (double)gj[2] * vj[2]) +
+                                       (double)dv[j];
+                    s_obj += 0.5 * rho * rho;
+                }
             }
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             stv<VEC>(V + (size_t)c * N + gi, vn[c]);
             if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bh[c]);
-            float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
+            C* bl = sm.buf + (size_t)(c * TL + l) * PM;
             if (!a.odd) {
-                float* ul = reinterpret_cast<float*>(bl);
+                R* ul = reinterpret_cast<R*>(bl);
 #pragma unroll
-                for (int j = 0; j < VEC; ++j) ul[x0 + j] = vn[c][j] + bh[c][j];
+                for (int j = 0; j < VEC; ++j) ul[x0 + j] = (R)vn[c][j] + (R)bh[c][j];
             } else {
 #pragma unroll
-                for (int j = 0; j < VEC; ++j) bl[x0 + j] = make_float2(vn[c][j] + bh[c][j], 0.f);
+                for (int j = 0; j < VEC; ++j) bl[x0 + j] = CT<C>::make((R)vn[c][j] + (R)bh[c][j], 0);
             }
         }
     }
@@ -416,7 +437,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
         if (nl < TL) {  // zero the unused lines so the batched FFT stays finite
             for (int idx = tid; idx < 3 * TL * PM; idx += nthr) {
                 const int l = (idx / PM) % TL;
-                if (l >= nl) sm.buf[idx] = make_float2(0.f, 0.f);
+                if (l >= nl) sm.buf[idx] = CT<C>::make(0, 0);
             }
         }
         __syncthreads();
@@ -426,18 +447,18 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             const int idx = cidx - c * hx * TL;
             const int k = idx >> lt, l = idx & tm;
             if (l >= nl) continue;
-            const float2* bl = sm.buf + (size_t)(c * TL + l) * PM;
-            float2 X;
+            const C* bl = sm.buf + (size_t)(c * TL + l) * PM;
+            C X;
             if (!a.odd) {
-                const float2 zk = bl[sm.xpos[k == L ? 0 : k]];
-                const float2 zc = cconj(bl[sm.xpos[k == 0 ? 0 : L - k]]);
-                const float2 e = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
-                const float2 o = make_float2(0.5f * (zk.y - zc.y), -0.5f * (zk.x - zc.x));
+                const C zk = bl[sm.xpos[k == L ? 0 : k]];
+                const C zc = cconj(bl[sm.xpos[k == 0 ? 0 : L - k]]);
+                const C e = CT<C>::make((R)0.5 * (zk.x + zc.x), (R)0.5 * (zk.y + zc.y));
+                const C o = CT<C>::make((R)0.5 * (zk.y - zc.y), (R)-0.5 * (zk.x - zc.x));
                 X = cadd(e, cmul(sm.xtw[k], o));
             } else {
                 X = bl[sm.xpos[k]];
             }
-            if (!(a.dbg_skip & 4)) S[((size_t)c * hx + k) * lines + L0 + l] = X;
+            if (!(a.dbg_skip & 4)) S[((size_t)c * hx + k) * lines + L0 + l] = to_f2(X);
         }
     }
 
@@ -581,7 +602,20 @@ static cudaError_t launch_x_mode(const XArgs& a, int npairs, cudaStream_t s) {
     if (vec == 4 && a.F.M % 4) vec = 2;
     if (vec == 2 && a.F.M % 2) vec = 1;
     void (*k)(XArgs);
-    if (a.f64) k = vec == 4 ? xpass_kernel<MODE, DT, 4, true> : (vec == 2 ? xpass_kernel<MODE, DT, 2, true> : xpass_kernel<MODE, DT, 1, true>);
+    if (a.precise) {  // fp64 x-FFT (C = double2) + fp64 point-wise; a.TL is the precise tile height
+        const size_t smem64 = xpass_smem_bytes_c(a.px.n, a.F.hx, a.TL, a.PM, sizeof(double2));
+        k = vec == 4 ? xpass_kernel<MODE, DT, 4, true, 2, double2>
+                     : (vec == 2 ? xpass_kernel<MODE, DT, 2, true, 2, double2> : xpass_kernel<MODE, DT, 1, true, 2, double2>);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem64);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        k<<<grid, kXThreads, smem64, s>>>(a);
+        return cudaGetLastError();
+    }
+    // l1: fp64 point-wise with the reference's rounding points (the shrinkage branch
+    // amplifies rounding differences); l2: fp32 unless DREG_F64
+    if (a.f64 || DT == 1) k = vec == 4 ? xpass_kernel<MODE, DT, 4, true> : (vec == 2 ? xpass_kernel<MODE, DT, 2, true> : xpass_kernel<MODE, DT, 1, true>);
     else if (a.minb == 4) k = vec == 4 ? xpass_kernel<MODE, DT, 4, false, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2, false, 4> : xpass_kernel<MODE, DT, 1, false, 4>);
     else k = vec == 4 ? xpass_kernel<MODE, DT, 4> : (vec == 2 ? xpass_kernel<MODE, DT, 2> : xpass_kernel<MODE, DT, 1>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

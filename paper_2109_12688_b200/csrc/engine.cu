@@ -138,7 +138,7 @@ float one_minus_cos(int k, int n) {  // 1 - cos(2 pi k / n) = 2 sin^2(pi k / n);
 struct Geometry {
     int M = 0, Ny = 0, Nz = 0, hx = 0;
     long long N = 0, lines = 0;
-    int L = 0, odd = 0, TL = 0, PM = 0, PY = 0, xvec = 1, tma = 0;
+    int L = 0, odd = 0, TL = 0, TLp = 0, PM = 0, PY = 0, xvec = 1, tma = 0;
     AxisPlan px{}, py{}, pz{};
     DevArray<float2> twx, xtw, twy, twz;
     DevArray<int> xpos;
@@ -172,6 +172,9 @@ struct Geometry {
         }
         while (TL > 4 && xpass_smem_bytes(L, hx, TL, PM) > 110 * 1024) TL /= 2;
         xsmem = xpass_smem_bytes(L, hx, TL, PM);
+        TLp = TL;  // precise (double2) generic x-pass: same budget, half the lines
+        while (TLp > 4 && xpass_smem_bytes_c(L, hx, TLp, PM, sizeof(double2)) > 110 * 1024) TLp /= 2;
+        if ((lines + TLp - 1) / TLp > kMaxPartials) TLp = TL;  // keep the partial-sum slots in range
         psmem = plane_smem_bytes(Ny, Nz, PY);
         if (xsmem > 227 * 1024) throw ArgFail("x extent too large for the shared-memory x-pass");
         if ((lines + TL - 1) / TL > kMaxPartials) throw ArgFail("grid has too many x-lines");
@@ -275,6 +278,7 @@ struct Workspace {
     int diag_iters = 0;
     DevArray<float> V, BH, WP, BP, G, D, I0, I1, PHI0, PHI1, W0, W1;
     DevArray<float2> S;
+    DevArray<float2> S2;  // scratch spectrum for the logged objective (solve_velocity only; lazy)
     DevArray<PairState> st;
     DevArray<double> part, diag, energy;
     DevArray<float> stage_t, stage_s, stage3, phi_soa, warped;
@@ -361,6 +365,7 @@ struct Workspace {
         F.BP = BP.p;
         F.G = G.p;
         F.D = D.p;
+        F.T = I0.p;
         F.S = S.p;
         F.st = st_shared ? st_shared : st.p;
         F.part = part.p;
@@ -607,7 +612,8 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.fx_variant = env_int("DREG_FX", 22);
     a.pipe = env_int("DREG_PIPE", 1);
     a.pipe_all = env_int("DREG_PIPE_ALL", 0);
-    a.fd_lines.init((unsigned)(3 * w.geo.TL));
+    if (precise) a.TL = w.geo.TLp;
+    a.fd_lines.init((unsigned)(3 * a.TL));
     return a;
 }
 
@@ -659,49 +665,41 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     sp.log_objective = log_obj ? 1 : 0;
     const int I = s.max_iters;
     const std::vector<double> coef = nesterov_coefs(I, s.accelerate != 0);
-    if (with_setup) L(launch_grad_diff(w.vg(), w.regbufs(), w.fields(diag), P, st));
+    if (with_setup) L(launch_grad_diff(w.vg(), w.regbufs(), w.fields(diag), s.data_term == 1, P, st));
     // precision policy: the accelerated iteration amplifies per-iteration
     // rounding, so long solves get fp64 spectral arithmetic (storage stays fp32)
     const int pol = L.c->precision;
-    const bool precise = pol == 2 || (pol == 0 && I > 100);
+    const bool precise = pol == 2 || (pol == 0 && (I > 100 || s.data_term == 1));
     XArgs xa = make_xargs(w, sp, diag, precise);
     PArgs pa = make_pargs(w, sp, diag, precise);
     pa.need_tail = need_tail ? 1 : 0;
+    if (log_obj && !w.S2.p) throw ArgFail("log_objective needs the workspace's scratch spectrum");
     auto energy = [&](int k) {
-        // objective_k = data term + lambda * spectral_energy(v_k)   (admm.cpp:288-292)
+        // objective_k = data term + lambda * spectral_energy(v_k)   (admm.cpp:288-292):
+        // r2c(v_k) goes to the scratch spectrum S2, so the iteration's own spectrum S is
+        // never touched and v does not depend on log_objective
         XArgs fa = xa;
         fa.k = k;
         fa.add_bh = 0;
+        fa.F.S = w.S2.p;
         PArgs ea = pa;
         ea.k = k;
-        ea.F.S = w.S.p;
+        ea.F.S = w.S2.p;
         L(launch_xpass(fa, X_FWD, P, st));
         L(launch_plane(ea, 1, P, st));
+        L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, k, P, st));
     };
     xa.k = 0;
     xa.coef = 0.0;
-    // With the objective logged, each iteration's S = r2c(u_k) is briefly replaced by
-    // r2c(v_k) for the energy and then rebuilt (identical bits: u_k = v_k + b_hat_k).
     L(launch_xpass(xa, X_FIRST, P, st));
-    if (log_obj) {
-        energy(0);
-        xa.k = 0;
-        xa.add_bh = 0;  // b_hat_0 = 0 is implicit (never stored): u_0 = v_0
-        L(launch_xpass(xa, X_FWD, P, st));  // restore S = r2c(u_0)
-        L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, 0, P, st));
-    }
+    if (log_obj) energy(0);
     for (int k = 1; k < I; ++k) {
         pa.k = k - 1;
         L(launch_plane(pa, 0, P, st));
         xa.k = k;
         xa.coef = coef[k - 1];
         L(launch_xpass(xa, k == 1 ? X_SECOND : X_GENERAL, P, st));
-        if (log_obj) {
-            energy(k);
-            xa.add_bh = 1;
-            L(launch_xpass(xa, X_FWD, P, st));
-            L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, k, P, st));
-        }
+        if (log_obj) energy(k);
     }
     if (need_tail) {
         pa.k = I - 1;
@@ -1245,6 +1243,7 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
         if (!target || !warped_source || !velocity_out) throw ArgFail("null buffer");
         Workspace& w = c->workspace(d, 1);
         w.ensure_diag(cfg->max_iters);
+        if (cfg->log_objective && !w.S2.p) w.S2.alloc(w.S.n);
         const size_t N = (size_t)w.geo.N;
         cudaStream_t st = c->stream;
         Launcher L{c};
@@ -1299,7 +1298,7 @@ static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, in
         s.theta = 1.0;
     }
     s.log_objective = 0;
-    const bool precise = c->precision == 2 || (c->precision == 0 && s.max_iters > 100);
+    const bool precise = c->precision == 2 || (c->precision == 0 && (s.max_iters > 100 || s.data_term == 1));
     const SolverParams sp = solver_params(s);
     XArgs xa = make_xargs(w, sp, false, precise);
     xa.k = 5;

@@ -29,7 +29,7 @@ __device__ __forceinline__ void unflat(long long i, int M, int Ny, int& x, int& 
 }
 
 // ---- per-solve setup: grad(warped) + (warped - target) -------------------------
-__global__ void __launch_bounds__(kVT) grad_diff_kernel(VolGeom g, RegBuffers R, Fields F) {
+__global__ void __launch_bounds__(kVT) grad_diff_kernel(VolGeom g, RegBuffers R, Fields F, int keep_warped) {
     const int pair = blockIdx.y;
     PairState* st = F.st + pair;
     if (!st->active || st->status) return;
@@ -51,12 +51,12 @@ __global__ void __launch_bounds__(kVT) grad_diff_kernel(VolGeom g, RegBuffers R,
         G[i] = (float)diff1(W, i, x, g.M, 1);
         G[N + i] = (float)diff1(W, i, y, g.Ny, sy);
         G[2 * N + i] = (float)diff1(W, i, z, g.Nz, sz);
-        D[i] = (float)((double)W[i] - (double)T[i]);
+        D[i] = keep_warped ? W[i] : (float)((double)W[i] - (double)T[i]);
     }
 }
 
-cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s) {
-    grad_diff_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F);
+cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, bool keep_warped, int npairs, cudaStream_t s) {
+    grad_diff_kernel<<<dim3(voxel_blocks(g.N), npairs), kVT, 0, s>>>(g, R, F, keep_warped ? 1 : 0);
     return cudaGetLastError();
 }
 

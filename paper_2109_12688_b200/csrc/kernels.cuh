@@ -17,7 +17,8 @@ struct Fields {
     float* WP;         // w_{k-1} (w_prev)    [P][3][N]
     float* BP;         // b_{k-1} (b_prev)    [P][3][N]
     float* G;          // grad(warped)        [P][3][N]
-    float* D;          // warped - target     [P][N]
+    float* D;          // warped - target     [P][N]; l1 data term: the warped image itself
+    const float* T;    // target (I0)         [P][N]; l1: residual = g.u + warped - target
     float2* S;         // x-spectrum, plane-major [P][3][hx][lines]
     PairState* st;     // [P]
     double* part;      // partial sums        [P][3][kMaxPartials]

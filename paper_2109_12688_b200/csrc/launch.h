@@ -72,6 +72,7 @@ struct PArgs {
 };
 
 size_t xpass_smem_bytes(int L, int hx, int TL, int PM);
+size_t xpass_smem_bytes_c(int L, int hx, int TL, int PM, size_t complex_bytes);
 size_t plane_smem_bytes(int Ny, int Nz, int PY);
 // radix split used by the specialised plane kernel for an axis of length n (0 = unsupported)
 int plane_fast_r1(int n);
@@ -99,8 +100,10 @@ cudaError_t launch_state_reset(PairState* st, int npairs, cudaStream_t s);
 // diag[k].objective += lambda * energy (admm.cpp:288-292)
 cudaError_t launch_objective_accumulate(Fields F, const double* energy, double lambda, int k, int npairs,
                                         cudaStream_t s);
-// Per-solve setup: grad(warped[cur]) and warped - target (volume.cpp:123-159).
-cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, int npairs, cudaStream_t s);
+// Per-solve setup: grad(warped[cur]) and D = warped - target (volume.cpp:123-159); with
+// keep_warped (l1 data term) D = warped, and the x-pass forms g.u + warped - target in
+// fp64 exactly like admm.cpp:35-36.
+cudaError_t launch_grad_diff(VolGeom g, const RegBuffers& R, Fields F, bool keep_warped, int npairs, cudaStream_t s);
 // compose + warp + SAD + accept/revert/stop (volume.cpp:161-181, registration.cpp:250-271)
 cudaError_t launch_compose_decide(VolGeom g, const RegBuffers& R, Fields F, double thr, int max_warps,
                                   int npairs, cudaStream_t s);

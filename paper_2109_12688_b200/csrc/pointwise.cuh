@@ -36,6 +36,50 @@ __device__ __forceinline__ void v_update_voxel(const float wh[3], const float bh
 }
 
 
+// The reference's v-update with its exact operation order and no FMA contraction
+// (explicit _rn intrinsics), from the UNROUNDED warped / target values (admm.cpp:23-63:
+// residual = g.u + double(warped) - double(target); Vec3 dot = (x x' + y y') + z z').
+// Used by the fused x-pass for the l1 data term, whose shrinkage branch |zhat| <= 1
+// is decided on this value.
+template <int DT>
+__device__ __forceinline__ void v_update_voxel_exact(const float wh[3], const float bh[3], const float g[3],
+                                                     float warped, float target, double theta, double eps,
+                                                     float v[3]) {
+    const double gx = g[0], gy = g[1], gz = g[2];
+    const double ux = __dsub_rn((double)wh[0], (double)bh[0]);
+    const double uy = __dsub_rn((double)wh[1], (double)bh[1]);
+    const double uz = __dsub_rn((double)wh[2], (double)bh[2]);
+    const double gg = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
+    if (DT == 1) {
+        const double gu = __dadd_rn(__dadd_rn(__dmul_rn(gx, ux), __dmul_rn(gy, uy)), __dmul_rn(gz, uz));
+        const double residual = __dsub_rn(__dadd_rn(gu, (double)warped), (double)target);
+        const double zhat = __ddiv_rn(__dmul_rn(theta, residual), __dadd_rn(gg, eps));
+        const double clip = __ddiv_rn(zhat, fmax(fabs(zhat), 1.0));
+        const double s = __ddiv_rn(clip, theta);
+        v[0] = (float)__dsub_rn(ux, __dmul_rn(gx, s));
+        v[1] = (float)__dsub_rn(uy, __dmul_rn(gy, s));
+        v[2] = (float)__dsub_rn(uz, __dmul_rn(gz, s));
+    } else {
+        const double diff = __dsub_rn((double)warped, (double)target);
+        const double rx = __dsub_rn(__dmul_rn(ux, theta), __dmul_rn(gx, diff));
+        const double ry = __dsub_rn(__dmul_rn(uy, theta), __dmul_rn(gy, diff));
+        const double rz = __dsub_rn(__dmul_rn(uz, theta), __dmul_rn(gz, diff));
+        const double grhs = __dadd_rn(__dadd_rn(__dmul_rn(gx, rx), __dmul_rn(gy, ry)), __dmul_rn(gz, rz));
+        const double s = __ddiv_rn(grhs, __dmul_rn(theta, __dadd_rn(theta, gg)));
+        const double it = __ddiv_rn(1.0, theta);
+        v[0] = (float)__dsub_rn(__dmul_rn(rx, it), __dmul_rn(gx, s));
+        v[1] = (float)__dsub_rn(__dmul_rn(ry, it), __dmul_rn(gy, s));
+        v[2] = (float)__dsub_rn(__dmul_rn(rz, it), __dmul_rn(gz, s));
+    }
+}
+
+// rho = g.v + double(warped) - double(target) (data_term_value, admm.cpp:239-250)
+__device__ __forceinline__ double data_residual_exact(const float g[3], const float v[3], float warped, float target) {
+    const double gv = __dadd_rn(__dadd_rn(__dmul_rn((double)g[0], (double)v[0]), __dmul_rn((double)g[1], (double)v[1])),
+                                __dmul_rn((double)g[2], (double)v[2]));
+    return __dsub_rn(__dadd_rn(gv, (double)warped), (double)target);
+}
+
 // fp32 form of the same update (the point-wise path of the fused x-pass).
 // l2: v = u - g (g.u + d) / (theta + |g|^2), algebraically equal to the reference's
 //     rhs/theta - g (g.rhs) / (theta (theta + |g|^2)), rhs = theta u - d g;

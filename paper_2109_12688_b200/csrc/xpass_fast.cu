@@ -13,6 +13,7 @@
 //    blocks {j, 8-j} hold every partner pair (k, L-k) and one thread finishes both.
 // Position of frequency k = 8 p1 + b is R2 b + p1 (same scheme as fft_device.cuh).
 #include <algorithm>
+#include <type_traits>
 
 #include <cstdlib>
 #include "fft_device.cuh"
@@ -303,6 +304,134 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
     }
 }
 
+// phase 2 for the l1 data term: the same updates in fp64 with the reference's rounding
+// points -- b = float(b_hat + v - w) (admm.cpp:142-153), w_hat / b_hat =
+// float(a + c (a - a_prev)) (:130-139), the v-update from the unrounded warped and
+// target values (v_update_voxel_exact) -- and fp64 change / residual / objective sums.
+// The shrinkage's branch |zhat| <= 1 amplifies any rounding difference, so the l1 path
+// spends the extra fp64 issue (it is not the bench path).
+template <int MODE, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0>
+__device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid,
+                                                     double& fc, double& fr, double& fo) {
+    constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
+    const long long N = a.F.N;
+    float* V = a.F.V + (size_t)pair * 3 * N;
+    float* BH = a.F.BH + (size_t)pair * 3 * N;
+    float* WP = a.F.WP + (size_t)pair * 3 * N;
+    float* BP = a.F.BP + (size_t)pair * 3 * N;
+    const float* G = a.F.G + (size_t)pair * 3 * N;
+    const float* Wd = a.F.D + (size_t)pair * N;  // l1: D holds the warped image itself
+    const float* Td = a.F.T + (size_t)pair * N;
+    const double theta = a.sp.theta, eps = a.sp.epsilon, coef = a.coef;
+    const bool accel = a.sp.accelerate != 0;
+    const size_t base = (size_t)L0 * M;
+    const int nvox = nl * M;
+#pragma unroll UNR
+    for (int i0 = tid * VEC; i0 < nvox; i0 += NTP * VEC) {
+        const int l = i0 / M, x0 = i0 - l * M;
+        const size_t gi = base + i0;
+        float w[3][VEC], vp[3][VEC], bo[3][VEC], wp[3][VEC], bp[3][VEC], g[3][VEC], wv[VEC], tv[VEC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (MODE != X_FIRST) ldvN<VEC, HINT>(V + (size_t)c * N + gi, vp[c]);
+            if (MODE == X_GENERAL) ldvN<VEC, HINT>(BH + (size_t)c * N + gi, bo[c]);
+            if (MODE == X_GENERAL && accel) {
+                ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
+                ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);
+            }
+            if (MODE != X_TAIL) ldvN<VEC, HINT>(G + (size_t)c * N + gi, g[c]);
+        }
+        if (MODE != X_TAIL) {
+            ldvN<VEC, HINT>(Wd + gi, wv);
+            ldvN<VEC, HINT>(Td + gi, tv);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const C* wl = buf + (c * TL + l) * PM;
+            if (MODE != X_FIRST) ld_reals<VEC>(wl, x0, w[c]);  // w = float(c2r), as stored by w_update_into
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) {
+                if (MODE == X_FIRST) {
+                    w[c][jj] = 0.f;
+                    vp[c][jj] = 0.f;
+                }
+                if (MODE != X_GENERAL) bo[c][jj] = 0.f;
+            }
+        }
+        if (MODE == X_TAIL) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int jj = 0; jj < VEC; ++jj) {
+                    const double dd = (double)vp[c][jj] - (double)w[c][jj];
+                    fr += dd * dd;
+                }
+            continue;
+        }
+        float wh[3][VEC], bh[3][VEC], vn[3][VEC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int jj = 0; jj < VEC; ++jj) {
+                if (MODE == X_FIRST) {
+                    wh[c][jj] = 0.f;
+                    bh[c][jj] = 0.f;
+                    continue;
+                }
+                const double dv = (double)vp[c][jj], dw = (double)w[c][jj];
+                const double dd = dv - dw;
+                fr += dd * dd;
+                const float b = (float)__dsub_rn(__dadd_rn((double)bo[c][jj], dv), dw);
+                if (MODE == X_GENERAL && accel) {
+                    wh[c][jj] = (float)__dadd_rn(dw, __dmul_rn(coef, __dsub_rn(dw, (double)wp[c][jj])));
+                    const double db = (double)b;
+                    bh[c][jj] = (float)__dadd_rn(db, __dmul_rn(coef, __dsub_rn(db, (double)bp[c][jj])));
+                } else {
+                    wh[c][jj] = w[c][jj];
+                    bh[c][jj] = b;
+                }
+                bo[c][jj] = b;
+            }
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj) {
+            const float whj[3] = {wh[0][jj], wh[1][jj], wh[2][jj]};
+            const float bhj[3] = {bh[0][jj], bh[1][jj], bh[2][jj]};
+            const float gj[3] = {g[0][jj], g[1][jj], g[2][jj]};
+            float vj[3];
+            v_update_voxel_exact<1>(whj, bhj, gj, wv[jj], tv[jj], theta, eps, vj);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                vn[c][jj] = vj[c];
+                fc += fabs((double)vj[c] - (double)vp[c][jj]);
+            }
+            if (a.sp.log_objective) fo += fabs(data_residual_exact(gj, vj, wv[jj], tv[jj]));
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (MODE != X_FIRST && accel) {
+                stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
+                stvN<VEC>(BP + (size_t)c * N + gi, bo[c]);
+            }
+            stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
+            if (MODE != X_FIRST) stvN<VEC>(BH + (size_t)c * N + gi, bh[c]);
+            st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);  // u = v + b_hat (admm.cpp:77-80)
+        }
+    }
+}
+
+// phase 2 dispatch: fp32 (l2, the bench path) or the exact fp64 form (l1)
+template <int MODE, int DT, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0, class Acc>
+__device__ __forceinline__ void pointwise_any(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid, Acc& fc,
+                                              Acc& fr, Acc& fo) {
+    if constexpr (DT == 1)
+        pointwise_tile_exact<MODE, R2, VEC, UNR, C, NTP, HINT>(a, buf, pair, L0, nl, tid, fc, fr, fo);
+    else
+        pointwise_tile<MODE, DT, R2, VEC, UNR, C, NTP, HINT>(a, buf, pair, L0, nl, tid, fc, fr, fo);
+}
+
+template <int DT>
+using AccT = typename std::conditional<DT == 1, double, float>::type;
+
 // phase 3: r2c of u (real, natural order in buf) -> spectrum rows in global.
 template <int R2, class C, class Sync, int NF = kFT>
 __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, float2* S, long long lines,
@@ -372,11 +501,11 @@ __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, flo
 // Per-pair reduction of one tile's partials (slot = tile index within the pair) and
 // the solve-level bookkeeping done by the pair's last tile.
 template <int MODE, class Sync, int NTP = kFT>
-__device__ __forceinline__ void finish_tile(const XArgs& a, int pair, unsigned slot, unsigned ntiles, float fc,
-                                            float fr, float fo, double* red, int* s_last, int tid, Sync sync) {
+__device__ __forceinline__ void finish_tile(const XArgs& a, int pair, unsigned slot, unsigned ntiles, double fc,
+                                            double fr, double fo, double* red, int* s_last, int tid, Sync sync) {
     PairState* st = a.F.st + pair;
-    const double vals[3] = {group_sum<NTP>((double)fc, red, tid, sync), group_sum<NTP>((double)fr, red, tid, sync),
-                            group_sum<NTP>((double)fo, red, tid, sync)};
+    const double vals[3] = {group_sum<NTP>(fc, red, tid, sync), group_sum<NTP>(fr, red, tid, sync),
+                            group_sum<NTP>(fo, red, tid, sync)};
     double tot[3];
     if (group_reduce_partials<NTP, 3>(vals, a.F.part + (size_t)pair * 3 * kMaxPartials, &st->counter, ntiles, tot,
                                       red, s_last, tid, sync, slot) &&
@@ -443,8 +572,8 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
     if (!F64 && MODE != X_FIRST) cp_async_wait_all();
     __syncthreads();
     if (MODE != X_FIRST) c2r_tile<R2>(buf, twx, xtw, tid, sync);
-    float fc = 0.f, fr = 0.f, fo = 0.f;
-    pointwise_tile<MODE, DT, R2, VEC, UNR>(a, buf, pair, L0, nl, tid, fc, fr, fo);
+    AccT<DT> fc = 0, fr = 0, fo = 0;
+    pointwise_any<MODE, DT, R2, VEC, UNR>(a, buf, pair, L0, nl, tid, fc, fr, fo);
     if (MODE != X_TAIL)
         r2c_tile<R2>(buf, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid, sync);
     finish_tile<MODE>(a, pair, blockIdx.x, gridDim.x, fc, fr, fo, red, &s_last, tid, sync);
@@ -595,10 +724,10 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             const int slot = cur / T, pair = plist[slot], tile = cur - slot * T;
             const long long L0 = (long long)tile * TL;
             const int nl = (int)min((long long)TL, lines - L0);
-            float fc = 0.f, fr = 0.f, fo = 0.f;
+            AccT<DT> fc = 0, fr = 0, fo = 0;
             if (!(a.dbg_skip & 2))
-                pointwise_tile<MODE, DT, R2, VEC, UNR, float2, NTP, HINT>(a, ring + b * BUF, pair, L0, nl, tid,
-                                                                                  fc, fr, fo);
+                pointwise_any<MODE, DT, R2, VEC, UNR, float2, NTP, HINT>(a, ring + b * BUF, pair, L0, nl, tid, fc,
+                                                                         fr, fo);
             ring_bar<kBarU, NALL, true>(b);
             if (run_start < 0) run_start = tile;
             acc[0] += (double)fc;

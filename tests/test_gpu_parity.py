@@ -152,6 +152,41 @@ def test_solve_velocity(ctx, oracle, data_term, shape):
     assert abs(d["final_change"] - do["final_change"]) <= 1e-4 * max(do["final_change"], 1e-12)
 
 
+@pytest.mark.parametrize("precision", [1, 2])
+@pytest.mark.parametrize("shape", [(16, 16, 16), (16, 32, 64), (16, 24, 48)])
+@pytest.mark.parametrize("data_term", [1, 2])
+def test_velocity_independent_of_log_objective(ctx, precision, shape, data_term):
+    """The logged objective's r2c(v_k) goes to a scratch spectrum, so v is bit-identical
+    with log_objective on and off (the reference's solve does not depend on it,
+    admm.cpp:288-292), for fp32 and fp64 spectral arithmetic and for the generic
+    (M = 16, 48) and specialised (M = 64) x-pass."""
+    f, m = synth.make_pair(1, 9, shape)
+    ctx.set_precision(precision)
+    try:
+        on = abi.solver_cfg(data_term=data_term, order=2, lambda_=0.1, theta=1.0, max_iters=12, log_objective=True)
+        off = abi.solver_cfg(data_term=data_term, order=2, lambda_=0.1, theta=1.0, max_iters=12, log_objective=False)
+        v1, d1 = ctx.solve_velocity(f, m, on)
+        v0, d0 = ctx.solve_velocity(f, m, off)
+    finally:
+        ctx.set_precision(0)
+    assert np.array_equal(v0, v1)
+    assert d1["objective"].shape == (12,) and np.all(np.isfinite(d1["objective"]))
+
+
+@pytest.mark.parametrize("shape", [(16, 24, 48), (12, 20, 30)])
+def test_long_solve_generic_width_precise(ctx, oracle, shape):
+    """> 100 iterations at x extents the specialised x-pass does not cover (M = 48, 30):
+    the auto policy runs the generic x-pass with fp64 butterflies (precise mode), and
+    the 150-iteration accelerated solve stays within the 1e-4 contract of the oracle."""
+    f, m = synth.make_pair(1, 13, shape)
+    cfg = abi.solver_cfg(data_term=2, order=3, lambda_=0.05, theta=0.5, max_iters=150, log_objective=False)
+    v, d = ctx.solve_velocity(f, m, cfg)
+    vo, do = oracle.solve_velocity(f, m, cfg)
+    print(f"{shape}: max-abs {max_abs(v, vo):.2e} rel-L2 {rel_l2(v, vo):.2e}")
+    assert d["iterations"] == do["iterations"] == 150
+    assert max_abs(v, vo) <= PHI_MAX_ABS and rel_l2(v, vo) <= PHI_REL_L2, (max_abs(v, vo), rel_l2(v, vo))
+
+
 def test_solve_velocity_tol_early_exit(ctx, oracle):
     f, m = synth.make_pair(1, 6, (16, 16, 16))
     cfg = abi.solver_cfg(data_term=2, order=1, lambda_=2.0, theta=0.05, max_iters=200, tol=1e-4, log_objective=False)
