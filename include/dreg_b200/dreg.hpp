@@ -51,19 +51,59 @@ struct Spacing3 {
     double x = 1.0;
     double y = 1.0;
     double z = 1.0;
+    friend bool operator==(const Spacing3& a, const Spacing3& b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
+    friend bool operator!=(const Spacing3& a, const Spacing3& b) { return !(a == b); }
 };
 
+// volume.hpp:32-49: fp64 3-vector with the reference's operators (value type; host math)
 struct Vec3 {
-    double x = 0.0, y = 0.0, z = 0.0;
+    double x = 0.0;
+    double y = 0.0;
+    double z = 0.0;
+
+    Vec3& operator+=(const Vec3& o) {
+        x += o.x;
+        y += o.y;
+        z += o.z;
+        return *this;
+    }
+    Vec3& operator-=(const Vec3& o) {
+        x -= o.x;
+        y -= o.y;
+        z -= o.z;
+        return *this;
+    }
+    Vec3& operator*=(double s) {
+        x *= s;
+        y *= s;
+        z *= s;
+        return *this;
+    }
+    friend Vec3 operator+(Vec3 a, const Vec3& b) { return a += b; }
+    friend Vec3 operator-(Vec3 a, const Vec3& b) { return a -= b; }
+    friend Vec3 operator*(Vec3 a, double s) { return a *= s; }
+    friend Vec3 operator*(double s, Vec3 a) { return a *= s; }
+    [[nodiscard]] double dot(const Vec3& o) const { return x * o.x + y * o.y + z * o.z; }
+    [[nodiscard]] double squared_norm() const { return dot(*this); }
+    [[nodiscard]] double norm() const { return std::sqrt(squared_norm()); }
 };
+
+namespace b200_detail {
+// volume.cpp:15-22 (check_geometry)
+inline void check_geometry(const Dims3& d, const Spacing3& s) {
+    if (d.x < 1 || d.y < 1 || d.z < 1) throw std::invalid_argument("volume dims must be positive");
+    if (!(s.x > 0.0) || !(s.y > 0.0) || !(s.z > 0.0)) throw std::invalid_argument("voxel spacing must be positive");
+}
+}  // namespace b200_detail
 
 struct ScalarVolume {
     Dims3 dims;
     Spacing3 spacing;
     std::vector<float> data;
     ScalarVolume() = default;
-    ScalarVolume(Dims3 d, Spacing3 s, float fill = 0.0f) : dims(d), spacing(s), data(d.voxels(), fill) {
-        if (d.x < 1 || d.y < 1 || d.z < 1) throw std::invalid_argument("volume dims must be positive");
+    ScalarVolume(Dims3 d, Spacing3 s, float fill = 0.0f) : dims(d), spacing(s) {
+        b200_detail::check_geometry(d, s);
+        data.assign(d.voxels(), fill);
     }
     [[nodiscard]] std::size_t index(int x, int y, int z) const {
         return static_cast<std::size_t>(x) + static_cast<std::size_t>(dims.x) *
@@ -79,10 +119,22 @@ struct VectorField {
     Spacing3 spacing;
     std::vector<float> data;  // 3 * voxels, interleaved (vx, vy, vz)
     VectorField() = default;
-    VectorField(Dims3 d, Spacing3 s) : dims(d), spacing(s), data(3 * d.voxels(), 0.0f) {
-        if (d.x < 1 || d.y < 1 || d.z < 1) throw std::invalid_argument("volume dims must be positive");
+    VectorField(Dims3 d, Spacing3 s) : dims(d), spacing(s) {
+        b200_detail::check_geometry(d, s);
+        data.assign(3 * d.voxels(), 0.0f);
+    }
+    [[nodiscard]] std::size_t index(int x, int y, int z) const {
+        return static_cast<std::size_t>(x) + static_cast<std::size_t>(dims.x) *
+                                                 (static_cast<std::size_t>(y) + static_cast<std::size_t>(dims.y) *
+                                                                                    static_cast<std::size_t>(z));
     }
     [[nodiscard]] Vec3 get(std::size_t v) const { return {data[3 * v], data[3 * v + 1], data[3 * v + 2]}; }
+    void set(std::size_t v, const Vec3& val) {
+        data[3 * v] = static_cast<float>(val.x);
+        data[3 * v + 1] = static_cast<float>(val.y);
+        data[3 * v + 2] = static_cast<float>(val.z);
+    }
+    [[nodiscard]] Vec3 at(int x, int y, int z) const { return get(index(x, y, z)); }
 };
 
 struct DeformationField {
@@ -363,13 +415,56 @@ inline VectorField w_update(const VectorField& v, const VectorField& b_hat, cons
                             const SolverConfig& cfg) {
     b200_detail::same(v.dims, b_hat.dims, "w_update");
     b200_detail::same(v.dims, kernel.dims, "w_update: kernel");
+    // The device builds (-Delta_h)^n's symbol on the fly from 1-D tables, so it can only
+    // apply kernels laplacian_symbol(order, dims) returns -- the only ones the reference
+    // ever passes (admm.cpp:260).  Anything else is refused rather than ignored.
+    if (kernel.values.size() != v.dims.voxels() || kernel.values != laplacian_symbol(kernel.order, kernel.dims).values)
+        throw std::invalid_argument("w_update: kernel is not laplacian_symbol(order, dims); arbitrary spectral "
+                                    "kernels are not supported by the device path");
     SolverConfig c = cfg;
-    c.order = kernel.order;  // the device builds the symbol of this order on the fly
+    c.order = kernel.order;
     const dreg_solver_cfg s = b200_detail::S(c);
     VectorField out(v.dims, v.spacing);
     b200_detail::check(dreg_cuda_w_update(b200_detail::ctx(), v.data.data(), b_hat.data.data(), b200_detail::D(v.dims),
                                           &s, out.data.data()));
     return out;
+}
+
+// admm.hpp:68
+inline double data_term_value(const ScalarVolume& target, const ScalarVolume& warped_source, const VectorField& grad,
+                              const VectorField& v, int s) {
+    b200_detail::same(target.dims, warped_source.dims, "data_term_value");
+    b200_detail::same(target.dims, grad.dims, "data_term_value");
+    b200_detail::same(target.dims, v.dims, "data_term_value");
+    double out = 0.0;
+    b200_detail::check(dreg_cuda_data_term_value(b200_detail::ctx(), target.data.data(), warped_source.data.data(),
+                                                 grad.data.data(), v.data.data(), b200_detail::D(target.dims), s,
+                                                 &out));
+    return out;
+}
+
+// volume.hpp:107,110 -- evaluated on the device (one round trip per call: sample many
+// points at once with the vector overloads below)
+inline std::vector<double> trilinear_sample(const ScalarVolume& vol, const std::vector<Vec3>& points) {
+    std::vector<double> out(points.size());
+    static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be three packed doubles");
+    b200_detail::check(dreg_cuda_trilinear_sample(b200_detail::ctx(), vol.data.data(), 1, b200_detail::D(vol.dims),
+                                                  reinterpret_cast<const double*>(points.data()),
+                                                  static_cast<int64_t>(points.size()), out.data()));
+    return out;
+}
+inline std::vector<Vec3> trilinear_sample(const VectorField& field, const std::vector<Vec3>& points) {
+    std::vector<Vec3> out(points.size());
+    b200_detail::check(dreg_cuda_trilinear_sample(b200_detail::ctx(), field.data.data(), 3,
+                                                  b200_detail::D(field.dims),
+                                                  reinterpret_cast<const double*>(points.data()),
+                                                  static_cast<int64_t>(points.size()),
+                                                  reinterpret_cast<double*>(out.data())));
+    return out;
+}
+inline double trilinear_sample(const ScalarVolume& vol, const Vec3& p) { return trilinear_sample(vol, std::vector<Vec3>{p})[0]; }
+inline Vec3 trilinear_sample(const VectorField& field, const Vec3& p) {
+    return trilinear_sample(field, std::vector<Vec3>{p})[0];
 }
 
 inline SolveResult solve_velocity(const ScalarVolume& target, const ScalarVolume& warped_source,
@@ -410,11 +505,15 @@ inline RegistrationConfig make_registration_config(Profile profile, SolverConfig
 }
 
 inline dreg_reg_cfg to_c(const RegistrationConfig& cfg) {
+    validate(cfg.solver);  // registration.cpp:183, before the level checks
     if (cfg.levels < 1) throw std::invalid_argument("register_pair: levels must be >= 1");
     if (cfg.max_warps_per_level.size() != static_cast<std::size_t>(cfg.levels) ||
         cfg.max_admm_iters_per_level.size() != static_cast<std::size_t>(cfg.levels))
         throw std::invalid_argument("register_pair: per-level caps must list one entry per level");
-    if (cfg.levels > DREG_MAX_LEVELS) throw std::invalid_argument("register_pair: too many levels");
+    if (!(cfg.warp_improvement_threshold > 0.0 && cfg.warp_improvement_threshold < 1.0))
+        throw std::invalid_argument("register_pair: warp improvement threshold must be in (0,1)");
+    if (cfg.levels > DREG_MAX_LEVELS)  // needs axes >= 4 << 10: registration.cpp:195 rejects any smaller grid
+        throw std::invalid_argument("register_pair: dims too small for the level count");
     dreg_reg_cfg c;
     std::memset(&c, 0, sizeof c);
     c.solver = b200_detail::S(cfg.solver);

@@ -40,8 +40,13 @@ extern "C" {
 #define DREG_NUMERIC 4
 #define DREG_RUNTIME 5
 
-#define DREG_MAX_LEVELS 8
-#define DREG_MAX_WARPS 64
+/* Capacities of the fixed-size per-level arrays below.  The reference has no limits,
+ * but (a) levels > 10 need every axis >= 4 << 10 = 4096 voxels (registration.cpp:195),
+ * far beyond one device's memory, and (b) 256 composed fields per level is 5x the
+ * converged profile's cap (registration.cpp:62-83).  Configs past these are rejected
+ * with DREG_INVALID_ARGUMENT; see INTEGRATION.md. */
+#define DREG_MAX_LEVELS 10
+#define DREG_MAX_WARPS 256
 
 #define DREG_PROFILE_CAPPED 0
 #define DREG_PROFILE_CONVERGED 1
@@ -315,6 +320,15 @@ int dreg_cuda_v_update(dreg_cuda_ctx* ctx, const float* target, const float* war
                        const float* grad, const float* w_hat, const float* b_hat,
                        dreg_dims3 dims, const dreg_solver_cfg* cfg, float* out);
 /* w_update (admm.hpp:64-65): spectral solve with the order-cfg->order kernel */
+/* data_term_value (admm.hpp:68, admm.cpp:239-250): sum over voxels of |rho| (s = 1)
+ * or rho^2 / 2 (s = 2), rho = grad.v + warped - target; grad and v AoS host fields. */
+int dreg_cuda_data_term_value(dreg_cuda_ctx* ctx, const float* target, const float* warped_source,
+                              const float* grad, const float* v, dreg_dims3 dims, int s, double* out);
+/* trilinear_sample (volume.hpp:107,110; volume.cpp:55-99) at n points given as (x, y, z)
+ * voxel coordinates (3n doubles): ncomp 1 samples a scalar volume (out: n doubles),
+ * ncomp 3 an AoS vector field (out: 3n doubles). */
+int dreg_cuda_trilinear_sample(dreg_cuda_ctx* ctx, const float* field, int ncomp, dreg_dims3 dims,
+                               const double* points, int64_t n, double* out);
 int dreg_cuda_w_update(dreg_cuda_ctx* ctx, const float* v, const float* b_hat,
                        dreg_dims3 dims, const dreg_solver_cfg* cfg, float* out);
 /* regulariser_energy (regularizer.hpp:45) */

@@ -453,6 +453,17 @@ static void trilinear_vec(const float* f, dreg_dims3 d, double px, double py, do
     }
 }
 
+/* volume.hpp:107,110: trilinear_sample at n points (x, y, z); ncomp 1 = scalar volume,
+ * 3 = AoS vector field */
+int dro_trilinear_sample(const float* f, int ncomp, dreg_dims3 d, const double* pts, int64_t n, double* out) {
+    if ((ncomp != 1 && ncomp != 3) || n < 0) return fail(DREG_INVALID_ARGUMENT, "trilinear_sample: bad arguments");
+    for (int64_t i = 0; i < n; ++i) {
+        if (ncomp == 1) out[i] = trilinear_scalar(f, d, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+        else trilinear_vec(f, d, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], out + 3 * i);
+    }
+    return DREG_OK;
+}
+
 /* ---- volume.cpp:101-121 (warp_image) ---------------------------------------- */
 int dro_warp_image(const float* img, const float* disp, dreg_dims3 d, float* out) {
     if (!dims_ok(d)) return fail(DREG_INVALID_ARGUMENT, "volume dims must be positive");

@@ -34,6 +34,7 @@ int dro_v_update(const float* target, const float* warped, const float* grad,
                  const dreg_solver_cfg* c, float* out);
 int dro_w_update(const float* v, const float* b_hat, dreg_dims3 d, const dreg_solver_cfg* c,
                  float* out);
+int dro_trilinear_sample(const float* f, int ncomp, dreg_dims3 d, const double* pts, int64_t n, double* out);
 int dro_data_term_value(const float* target, const float* warped, const float* grad,
                         const float* v, dreg_dims3 d, int s, double* out);
 int dro_solve_velocity(const float* target, const float* warped, dreg_dims3 d,

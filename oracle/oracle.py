@@ -82,6 +82,7 @@ class CpuLib:
             "v_update",
             "w_update",
             "data_term_value",
+            "trilinear_sample",
             "solve_velocity",
             "warp_image",
             "image_gradient",
@@ -155,6 +156,16 @@ class CpuLib:
             self._g("data_term_value")(_fp(target), _fp(warped), _fp(grad), _fp(v), abi.dims3(target), s, C.byref(out))
         )
         return out.value
+
+    def trilinear_sample(self, field, points) -> np.ndarray:
+        field = _f32(field)
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        ncomp = 3 if field.ndim == 4 else 1
+        out = np.zeros((pts.shape[0], 3) if ncomp == 3 else pts.shape[0], np.float64)
+        dims = abi.dims3(field[..., 0] if ncomp == 3 else field)
+        self._check(self._g("trilinear_sample")(_fp(field), ncomp, dims, pts.ctypes.data_as(_D), C.c_int64(pts.shape[0]),
+                                                out.ctypes.data_as(_D)))
+        return out
 
     def solve_velocity(self, target, warped, cfg: abi.SolverCfg):
         target, warped = _f32(target), _f32(warped)

@@ -147,6 +147,24 @@ int ref_w_update(const float* v, const float* b_hat, dreg_dims3 d, const dreg_so
     });
 }
 
+int ref_trilinear_sample(const float* f, int ncomp, dreg_dims3 d, const double* pts, int64_t n, double* out) {
+    return guard([&] {
+        if (ncomp == 1) {
+            const auto vol = scalar(f, d);
+            for (int64_t i = 0; i < n; ++i)
+                out[i] = dreg::trilinear_sample(vol, dreg::Vec3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+        } else {
+            const auto fld = vec(f, d);
+            for (int64_t i = 0; i < n; ++i) {
+                const dreg::Vec3 r = dreg::trilinear_sample(fld, dreg::Vec3{pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]});
+                out[3 * i] = r.x;
+                out[3 * i + 1] = r.y;
+                out[3 * i + 2] = r.z;
+            }
+        }
+    });
+}
+
 int ref_data_term_value(const float* target, const float* warped, const float* grad,
                         const float* v, dreg_dims3 d, int s, double* out) {
     return guard([&] {

@@ -13,8 +13,8 @@ DREG_IO_ERROR = 3
 DREG_NUMERIC = 4
 DREG_RUNTIME = 5
 
-DREG_MAX_LEVELS = 8
-DREG_MAX_WARPS = 64
+DREG_MAX_LEVELS = 10
+DREG_MAX_WARPS = 256
 
 DREG_KIND_SCALAR = 0
 DREG_KIND_VECTOR = 1

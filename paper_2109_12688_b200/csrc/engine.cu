@@ -546,6 +546,13 @@ void check_solver(const dreg_solver_cfg* s) {
     }
 }
 
+// volume.cpp:15-22 (check_geometry): containers reject non-positive spacing.  The
+// registration itself works in voxel units (volume.hpp:25-26), so spacing is only
+// validated, like the reference's ScalarVolume constructor does.
+void check_spacing(dreg_spacing3 s) {
+    if (!(s.x > 0.0) || !(s.y > 0.0) || !(s.z > 0.0)) throw ArgFail("voxel spacing must be positive");
+}
+
 void check_dims(dreg_dims3 d, int min_extent, const char* what) {
     if (d.x < 1 || d.y < 1 || d.z < 1) throw ArgFail("volume dims must be positive");
     if (d.x < min_extent || d.y < min_extent || d.z < min_extent)
@@ -751,7 +758,7 @@ void enqueue_registration(Launcher& L, const std::vector<Workspace*>& lv, int P,
         if (l == 0) L(launch_level_init(g, R, F, 0, P, st));
         else L(launch_level_up(lv[l - 1]->vg(), g, lv[l - 1]->regbufs(), R, F, l, P, st));
         s.max_iters = cfg.max_admm_iters_per_level[l];
-        const int K = cfg.max_warps_per_level[l];
+        const int K = std::max(0, cfg.max_warps_per_level[l]);
         for (int wi = 0; wi < K; ++wi) {
             enqueue_solve(L, w, P, s, false, false, true, st);
             L(launch_compose_decide(g, R, F, cfg.warp_improvement_threshold, K, P, st));
@@ -841,21 +848,28 @@ void run_registration(dreg_cuda_ctx* c, const std::vector<Workspace*>& lv, int P
     c->launches += it->second.second;
 }
 
+// registration.cpp:182-198, in the reference's order.  Per-level ADMM caps are checked
+// only on levels that run a solve (the reference validates them inside solve_velocity);
+// a negative warp cap runs no warps, like the reference's `warp < max_warps` loop.
 void validate_reg(const dreg_reg_cfg* cfg, dreg_dims3 d) {
     if (!cfg) throw ArgFail("registration config is null");
     check_solver(&cfg->solver);
     if (cfg->levels < 1) throw ArgFail("register_pair: levels must be >= 1");
-    if (cfg->levels > DREG_MAX_LEVELS) throw ArgFail("register_pair: per-level caps must list one entry per level");
     if (!(cfg->warp_improvement_threshold > 0.0 && cfg->warp_improvement_threshold < 1.0))
         throw ArgFail("register_pair: warp improvement threshold must be in (0,1)");
-    const int min_extent = 4 << (cfg->levels - 1);
     if (d.x < 1 || d.y < 1 || d.z < 1) throw ArgFail("volume dims must be positive");
+    const long long min_extent = cfg->levels > 40 ? (1LL << 42) : (4LL << (cfg->levels - 1));
     if (d.x < min_extent || d.y < min_extent || d.z < min_extent)
         throw ArgFail("register_pair: dims too small for the level count");
+    if (cfg->levels > DREG_MAX_LEVELS)
+        throw ArgFail("register_pair: more than " + std::to_string(DREG_MAX_LEVELS) + " levels (axes >= " +
+                      std::to_string(4 << (DREG_MAX_LEVELS - 1)) + " voxels) exceed one device");
     for (int l = 0; l < cfg->levels; ++l) {
-        if (cfg->max_admm_iters_per_level[l] < 1) throw ArgFail("solver: max_iters must be >= 1");
-        if (cfg->max_warps_per_level[l] < 0) throw ArgFail("register_pair: negative warp cap");
-        if (cfg->max_warps_per_level[l] > DREG_MAX_WARPS) throw ArgFail("register_pair: warp cap above 64");
+        if (cfg->max_warps_per_level[l] > DREG_MAX_WARPS)
+            throw ArgFail("register_pair: warp cap above " + std::to_string(DREG_MAX_WARPS) +
+                          " (per-level log capacity, dreg_cuda.h)");
+        if (cfg->max_warps_per_level[l] >= 1 && cfg->max_admm_iters_per_level[l] < 1)
+            throw ArgFail("solver: max_iters must be >= 1");
     }
 }
 
@@ -1199,12 +1213,12 @@ int dregb_register_batch_records(dreg_cuda_ctx* c, int n_pairs, const float* con
 int dreg_cuda_register_pair(dreg_cuda_ctx* c, const float* target, const float* source, dreg_dims3 dims,
                             dreg_spacing3 spacing, const dreg_reg_cfg* cfg, float* phi_out, float* warped_out,
                             dreg_pair_result* result) {
-    (void)spacing;
     const float* t[1] = {target};
     const float* s[1] = {source};
     float* po[1] = {phi_out};
     float* wo[1] = {warped_out};
     return guarded(c, [&] {
+        check_spacing(spacing);
         if (!target || !source) throw ArgFail("null input volume");
         return register_impl(c, 1, t, s, nullptr, nullptr, dims, cfg, po, wo, nullptr, nullptr, result);
     });
@@ -1214,8 +1228,8 @@ int dreg_cuda_register_batch(dreg_cuda_ctx* c, int n_pairs, const float* const* 
                              const float* const* sources, dreg_dims3 dims, dreg_spacing3 spacing,
                              const dreg_reg_cfg* cfg, float* const* phi_out, float* const* warped_out,
                              dreg_pair_result* results) {
-    (void)spacing;
     return guarded(c, [&] {
+        check_spacing(spacing);
         if (n_pairs > 0 && (!targets || !sources)) throw ArgFail("null input arrays");
         return register_impl(c, n_pairs, targets, sources, nullptr, nullptr, dims, cfg, phi_out, warped_out,
                              nullptr, nullptr, results);
@@ -1226,8 +1240,8 @@ int dreg_cuda_register_batch_device(dreg_cuda_ctx* c, int n_pairs, const float* 
                                     const float* sources_dev, dreg_dims3 dims, dreg_spacing3 spacing,
                                     const dreg_reg_cfg* cfg, float* phi_dev_out, float* warped_dev_out,
                                     dreg_pair_result* results) {
-    (void)spacing;
     return guarded(c, [&] {
+        check_spacing(spacing);
         if (n_pairs > 0 && (!targets_dev || !sources_dev)) throw ArgFail("null input arrays");
         return register_impl(c, n_pairs, nullptr, nullptr, targets_dev, sources_dev, dims, cfg, nullptr, nullptr,
                              phi_dev_out, warped_dev_out, results);
@@ -1388,6 +1402,55 @@ int dreg_cuda_v_update(dreg_cuda_ctx* c, const float* target, const float* warpe
     });
 }
 
+int dreg_cuda_data_term_value(dreg_cuda_ctx* c, const float* target, const float* warped, const float* grad,
+                              const float* v, dreg_dims3 d, int s, double* out) {
+    return guarded(c, [&] {
+        if (s != 1 && s != 2) throw ArgFail("data_term_value: s must be 1 or 2");
+        if (!target || !warped || !grad || !v || !out) throw ArgFail("data_term_value: null buffer");
+        check_dims(d, 1, "data_term_value");
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        CK(cudaMemcpyAsync(w.I0.p, target, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(w.I1.p, warped, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+        upload_aos(c, w, grad, w.G.p);
+        upload_aos(c, w, v, w.V.p);
+        CK(launch_data_term(w.vg(), w.I0.p, w.I1.p, w.G.p, w.V.p, s, w.part.p, w.scal.p, w.counter.p, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
+int dreg_cuda_trilinear_sample(dreg_cuda_ctx* c, const float* field, int ncomp, dreg_dims3 d, const double* points,
+                               int64_t n, double* out) {
+    return guarded(c, [&] {
+        if (ncomp != 1 && ncomp != 3) throw ArgFail("trilinear_sample: ncomp must be 1 or 3");
+        if (n < 0 || (n > 0 && (!field || !points || !out))) throw ArgFail("trilinear_sample: null buffer");
+        check_dims(d, 1, "trilinear_sample");
+        if (n == 0) return DREG_OK;
+        Workspace& w = c->workspace(d, 1);
+        const size_t N = (size_t)w.geo.N;
+        DevArray<double> pts, res;
+        pts.alloc(3 * (size_t)n);
+        res.alloc((size_t)ncomp * (size_t)n);
+        CK(cudaMemcpyAsync(pts.p, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+        const float* f;
+        if (ncomp == 1) {
+            CK(cudaMemcpyAsync(w.W0.p, field, sizeof(float) * N, cudaMemcpyHostToDevice, c->stream));
+            f = w.W0.p;
+        } else {
+            upload_aos(c, w, field, w.PHI0.p);
+            f = w.PHI0.p;
+        }
+        CK(launch_trilinear_points(w.vg(), f, ncomp, pts.p, n, res.p, c->stream));
+        c->launches += 1;
+        CK(cudaMemcpyAsync(out, res.p, sizeof(double) * ncomp * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return DREG_OK;
+    });
+}
+
 int dreg_cuda_w_update(dreg_cuda_ctx* c, const float* v, const float* b_hat, dreg_dims3 d, const dreg_solver_cfg* cfg,
                        float* out) {
     return guarded(c, [&] {
@@ -1400,10 +1463,11 @@ int dreg_cuda_w_update(dreg_cuda_ctx* c, const float* v, const float* b_hat, dre
         Launcher L{c};
         L(launch_state_reset(w.st.p, 1, c->stream));
         const SolverParams sp = solver_params(*cfg);
-        XArgs xa = make_xargs(w, sp, false);
+        const bool precise = c->precision == 2;  // fp64 butterflies / multiplier on request
+        XArgs xa = make_xargs(w, sp, false, precise);
         xa.add_bh = 1;
         L(launch_xpass(xa, X_FWD, 1, c->stream));
-        PArgs pa = make_pargs(w, sp, false);
+        PArgs pa = make_pargs(w, sp, false, precise);
         L(launch_plane(pa, 0, 1, c->stream));
         L(launch_xpass(xa, X_INV, 1, c->stream));
         c->launches += L.count;

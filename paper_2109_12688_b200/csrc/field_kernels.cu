@@ -778,3 +778,62 @@ cudaError_t launch_pack_records(const PairState* st, int npairs, int pair_base, 
 }
 
 }  // namespace dregb
+
+namespace dregb {
+
+// data_term_value (admm.cpp:239-250): sum of |rho| (s = 1) or rho^2 / 2 (s = 2),
+// rho = g.v + warped - target in the reference's operation order; fixed-order
+// fp64 reduction (run-to-run identical).
+__global__ void __launch_bounds__(kVT) data_term_kernel(VolGeom g, const float* T, const float* W, const float* G,
+                                                        const float* V, int s, double* part, double* out,
+                                                        unsigned int* counter) {
+    __shared__ double red[32];
+    const long long N = g.N;
+    double acc = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float gv[3] = {G[i], G[N + i], G[2 * N + i]};
+        const float vv[3] = {V[i], V[N + i], V[2 * N + i]};
+        const double rho = data_residual_exact(gv, vv, W[i], T[i]);
+        acc += s == 1 ? fabs(rho) : 0.5 * rho * rho;
+    }
+    const double vals[1] = {block_sum<kVT>(acc, red)};
+    double tot[1];
+    if (reduce_partials<kVT, 1>(vals, part, counter, gridDim.x, tot, red) && threadIdx.x == 0) out[0] = tot[0];
+}
+
+cudaError_t launch_data_term(VolGeom g, const float* target, const float* warped, const float* grad_soa,
+                             const float* v_soa, int s, double* part, double* out, unsigned int* counter,
+                             cudaStream_t st) {
+    data_term_kernel<<<voxel_blocks(g.N), kVT, 0, st>>>(g, target, warped, grad_soa, v_soa, s, part, out, counter);
+    return cudaGetLastError();
+}
+
+// trilinear_sample at arbitrary points (volume.cpp:55-99): clamp-then-floor per axis,
+// fp64 lerps x -> y -> z; ncomp 1 (scalar volume) or 3 (SoA vector field).
+__global__ void trilinear_points_kernel(VolGeom g, const float* f, int ncomp, const double* pts, long long n,
+                                        double* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double px = pts[3 * i], py = pts[3 * i + 1], pz = pts[3 * i + 2];
+        if (ncomp == 1) {
+            out[i] = trilinear(f, g.M, g.Ny, g.Nz, px, py, pz);
+        } else {
+            double r[3];
+            trilinear3(f, (size_t)g.N, g.M, g.Ny, g.Nz, px, py, pz, r);
+            out[3 * i] = r[0];
+            out[3 * i + 1] = r[1];
+            out[3 * i + 2] = r[2];
+        }
+    }
+}
+
+cudaError_t launch_trilinear_points(VolGeom g, const float* field, int ncomp, const double* pts, long long n,
+                                    double* out, cudaStream_t st) {
+    long long b = (n + kVT - 1) / kVT;
+    b = b < 1 ? 1 : (b > 1184 ? 1184 : b);
+    trilinear_points_kernel<<<(unsigned)b, kVT, 0, st>>>(g, field, ncomp, pts, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace dregb

@@ -148,6 +148,13 @@ cudaError_t launch_hausdorff_slices(VolGeom g, const uint16_t* a, const uint16_t
                                     double sx, double sy, int ctas, double* scratch, int* iscratch, double* worst,
                                     cudaStream_t s);
 
+// data_term_value (admm.cpp:239-250) into out[0]
+cudaError_t launch_data_term(VolGeom g, const float* target, const float* warped, const float* grad_soa,
+                             const float* v_soa, int s, double* part, double* out, unsigned int* counter,
+                             cudaStream_t st);
+// trilinear_sample at n points (x, y, z) (volume.cpp:55-99); ncomp 1 or 3 (SoA field)
+cudaError_t launch_trilinear_points(VolGeom g, const float* field, int ncomp, const double* pts, long long n,
+                                    double* out, cudaStream_t st);
 // per-pair dreg_pair_record of the multi-device all-gather
 cudaError_t launch_pack_records(const PairState* st, int npairs, int pair_base, int device, int levels,
                                 dreg_pair_record* out, cudaStream_t s);

@@ -208,8 +208,9 @@ int dreg_cuda_multi_register_batch(dreg_cuda_multi* m, int n_pairs, const float*
                                    const float* const* sources, dreg_dims3 dims, dreg_spacing3 spacing,
                                    const dreg_reg_cfg* cfg, float* const* phi_out, float* const* warped_out,
                                    dreg_pair_result* results, dreg_pair_record* records) {
-    (void)spacing;
     if (!m) return DREG_INVALID_ARGUMENT;
+    if (!(spacing.x > 0.0) || !(spacing.y > 0.0) || !(spacing.z > 0.0))
+        return fail(m, DREG_INVALID_ARGUMENT, "voxel spacing must be positive");
     if (n_pairs < 0) return fail(m, DREG_INVALID_ARGUMENT, "n_pairs must be >= 0");
     if (n_pairs > 0 && (!targets || !sources)) return fail(m, DREG_INVALID_ARGUMENT, "null input arrays");
     const int D = (int)m->devices.size();

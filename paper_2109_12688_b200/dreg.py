@@ -92,6 +92,8 @@ def load_library() -> C.CDLL:
     L.dreg_cuda_v_update.argtypes = [P, _F, _F, _F, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
     L.dreg_cuda_w_update.argtypes = [P, _F, _F, Dims3, C.POINTER(SolverCfg), _F]
     L.dreg_cuda_regulariser_energy.argtypes = [P, _F, Dims3, C.c_int, _D]
+    L.dreg_cuda_data_term_value.argtypes = [P, _F, _F, _F, _F, Dims3, C.c_int, _D]
+    L.dreg_cuda_trilinear_sample.argtypes = [P, _F, C.c_int, Dims3, _D, C.c_int64, _D]
     L.dreg_cuda_warp_image.argtypes = [P, _F, _F, Dims3, _F]
     L.dreg_cuda_image_gradient.argtypes = [P, _F, Dims3, _F]
     L.dreg_cuda_compose_deformation.argtypes = [P, _F, _F, Dims3, _F]
@@ -487,6 +489,26 @@ class Context:
         v, b_hat = _f32(v), _f32(b_hat)
         out = np.zeros_like(v)
         self._check(self.lib.dreg_cuda_w_update(self.h, _fp(v), _fp(b_hat), abi.dims3(v), C.byref(cfg), _fp(out)))
+        return out
+
+    def data_term_value(self, target, warped, grad, v, s: int) -> float:
+        """admm.hpp:68 / admm.cpp:239-250."""
+        target, warped, grad, v = map(_f32, (target, warped, grad, v))
+        out = C.c_double()
+        self._check(self.lib.dreg_cuda_data_term_value(self.h, _fp(target), _fp(warped), _fp(grad), _fp(v),
+                                                       abi.dims3(target), int(s), C.byref(out)))
+        return out.value
+
+    def trilinear_sample(self, field, points) -> np.ndarray:
+        """volume.hpp:107,110 at points [n, 3] (x, y, z): scalar field (z,y,x) -> [n];
+        vector field (z,y,x,3) -> [n, 3]."""
+        field = _f32(field)
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        ncomp = 3 if field.ndim == 4 else 1
+        out = np.zeros((pts.shape[0], 3) if ncomp == 3 else pts.shape[0], np.float64)
+        dims = abi.dims3(field[..., 0] if ncomp == 3 else field)
+        self._check(self.lib.dreg_cuda_trilinear_sample(self.h, _fp(field), ncomp, dims, pts.ctypes.data_as(_D),
+                                                        pts.shape[0], out.ctypes.data_as(_D)))
         return out
 
     def regulariser_energy(self, w, order: int) -> float:

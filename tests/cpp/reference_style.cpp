@@ -120,6 +120,54 @@ int main() {
     const std::string text((std::istreambuf_iterator<char>(rf)), std::istreambuf_iterator<char>());
     CHECK(text.find("\"velocity_count\": " + std::to_string(res.velocity_count)) != std::string::npos);
 
+    // volume.hpp value-type API: Vec3 arithmetic, VectorField set / at / index,
+    // Spacing3 equality, geometry validation (volume.cpp:15-22)
+    {
+        const dreg::Vec3 a{1.0, 2.0, 3.0}, b{0.5, -1.0, 2.0};
+        CHECK((a + b).x == 1.5 && (a - b).y == 3.0 && (2.0 * a).z == 6.0 && (a * 0.5).x == 0.5);
+        CHECK(a.dot(b) == 0.5 - 2.0 + 6.0 && a.squared_norm() == 14.0 && std::abs(a.norm() - std::sqrt(14.0)) < 1e-15);
+        dreg::VectorField f(dims, {1.0, 1.0, 1.0});
+        f.set(f.index(3, 4, 5), {0.25, -0.5, 1.0});
+        CHECK(f.at(3, 4, 5).y == -0.5 && f.get(f.index(3, 4, 5)).z == 1.0);
+        CHECK((dreg::Spacing3{1.0, 2.0, 3.0} == dreg::Spacing3{1.0, 2.0, 3.0}));
+        CHECK(!(dreg::Spacing3{1.0, 2.0, 3.0} == dreg::Spacing3{1.0, 2.0, 2.5}));
+        threw = false;
+        try {
+            dreg::ScalarVolume bad(dims, {1.0, 0.0, 1.0});
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+        // trilinear_sample (volume.hpp:107,110): lattice points are exact, clamping applies
+        CHECK(dreg::trilinear_sample(target, dreg::Vec3{2.0, 3.0, 4.0}) == target.at(2, 3, 4));
+        CHECK(dreg::trilinear_sample(target, dreg::Vec3{-5.0, 3.0, 4.0}) == target.at(0, 3, 4));
+        const dreg::Vec3 fv = dreg::trilinear_sample(f, dreg::Vec3{3.0, 4.0, 5.0});
+        CHECK(fv.x == 0.25 && fv.y == -0.5 && fv.z == 1.0);
+        const double mid = dreg::trilinear_sample(target, dreg::Vec3{2.5, 3.0, 4.0});
+        CHECK(std::abs(mid - 0.5 * (target.at(2, 3, 4) + target.at(3, 3, 4))) < 1e-7);
+        // data_term_value (admm.hpp:68): v = 0 leaves rho = warped - target
+        const auto grad = dreg::image_gradient(source);
+        const dreg::VectorField zero(dims, {1.0, 1.0, 1.0});
+        double l1 = 0.0;
+        for (std::size_t i = 0; i < target.data.size(); ++i)
+            l1 += std::abs(static_cast<double>(source.data[i]) - static_cast<double>(target.data[i]));
+        CHECK(std::abs(dreg::data_term_value(target, source, grad, zero, 1) - l1) <= 1e-12 * l1);
+        // w_update applies laplacian_symbol kernels and refuses any other kernel
+        dreg::SolverConfig wc = solver;
+        wc.lambda = 2.0;
+        auto kern = dreg::laplacian_symbol(2, dims);
+        const auto w = dreg::w_update(f, zero, kern, wc);
+        CHECK(dreg::all_finite(w));
+        kern.values[5] *= 1.5;
+        threw = false;
+        try {
+            (void)dreg::w_update(f, zero, kern, wc);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+
     // B200 extension: the same pairs sharded over the box's GPUs (here: device 0),
     // NCCL all-gather of the per-pair records; results equal register_pair's
     {

@@ -137,6 +137,30 @@ def test_regulariser_energy(ctx, oracle, shape, order):
     assert abs(e - r) <= 2e-6 * abs(r)
 
 
+def test_trilinear_sample_points(ctx, reference):
+    """volume.hpp:107,110 (trilinear_sample) on the device vs the reference's own
+    function: fp64 lerps, so equal to ~1e-15 relative (device FMA contraction)."""
+    from test_oracle_pin import _points
+
+    shape = (7, 9, 8)
+    img, fld = random_volume(shape, 61), random_field(shape, 62, 2.0)
+    pts = _points(shape, 63)
+    for f in (img, fld):
+        a, b = ctx.trilinear_sample(f, pts), reference.trilinear_sample(f, pts)
+        assert np.allclose(a, b, rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_data_term_value(ctx, reference, s):
+    """admm.cpp:239-250 on the device (fp64 reduction) vs the reference."""
+    shape = (16, 24, 20)
+    t, w = random_volume(shape, 64), random_volume(shape, 65)
+    g, v = random_field(shape, 66, 1.0), random_field(shape, 67, 0.5)
+    a, b = ctx.data_term_value(t, w, g, v, s), reference.data_term_value(t, w, g, v, s)
+    assert abs(a - b) <= 1e-12 * abs(b)
+    assert ctx.data_term_value(t, w, g, v, s) == a  # fixed-order reduction: run-to-run identical
+
+
 # ---- solve_velocity (admm.cpp:252-314) ----------------------------------------------
 @pytest.mark.parametrize("data_term", [1, 2])
 @pytest.mark.parametrize("shape", [(16, 16, 16), (32, 64, 64)])
@@ -447,6 +471,28 @@ def test_register_generic_grids(ctx, oracle, shape):
     f, m = synth.make_pair(1, 23, shape)
     s = abi.solver_cfg(data_term=2, order=2, lambda_=0.2, theta=0.5, max_iters=30, log_objective=False)
     _reg_parity(ctx, oracle, f, m, abi.reg_cfg(s, 1, (3,), (30,)))
+
+
+def test_register_cap_edge_cases(ctx, reference):
+    """registration.cpp:182-198,250: a negative warp cap runs no warps (and its level's
+    ADMM cap is never validated), caps above the old 64 are accepted, and > 10 levels
+    fail with the reference's 'dims too small' on any grid one device can hold."""
+    f, m = synth.make_pair(1, 21, (16, 16, 16))
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=10, log_objective=False)
+    for cfg in (abi.reg_cfg(s, 2, (-3, 2), (0, 10)), abi.reg_cfg(s, 1, (100,), (3,))):
+        cfg.warp_improvement_threshold = 1e-9
+        phi, _, res = ctx.register_pair(f, m, cfg)
+        phi_r, _, res_r = reference.register_pair(f, m, cfg)
+        assert res.velocity_count == res_r.velocity_count
+        assert abi.level_logs(res)[0]["warps"] == abi.level_logs(res_r)[0]["warps"]
+        assert max_abs(phi, phi_r) <= PHI_MAX_ABS and rel_l2(phi, phi_r) <= PHI_REL_L2
+    bad = abi.reg_cfg(s, 1, (2,), (0,))  # a level that runs a solve with max_iters 0
+    with pytest.raises(ValueError):
+        ctx.register_pair(f, m, bad)
+    with pytest.raises(ValueError):
+        reference.register_pair(f, m, bad)
+    with pytest.raises(ValueError):
+        ctx.register_pair(f, m, abi.reg_cfg(s, 1, (2,), (10,)), spacing=(1.0, 0.0, 1.0))
 
 
 def test_batch_isolates_bad_pair(ctx, oracle):

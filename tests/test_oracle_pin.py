@@ -114,3 +114,30 @@ def test_mkl_timing_build_matches_parity_build(reference):
     assert r1.velocity_count == r2.velocity_count
     assert np.max(np.abs(p1 - p2)) < 1e-5
     assert np.linalg.norm(p1 - p2) <= 1e-6 * np.linalg.norm(p1)
+
+
+def _points(shape, seed, n=500):
+    """sample points inside, on and outside the grid (clamp rule, volume.cpp:36-41)"""
+    z, y, x = shape
+    rng = np.random.default_rng(seed)
+    p = rng.uniform(-2.0, [x + 1.0, y + 1.0, z + 1.0], (n, 3))
+    p[:8] = [[0, 0, 0], [x - 1, y - 1, z - 1], [0.5, 0.5, 0.5], [x - 1.25, 0, 0], [-1, -1, -1],
+             [x + 3, y + 3, z + 3], [1, 2, 3], [2.5, 0.0, 1.0]]
+    return p
+
+
+def test_trilinear_sample_bit_exact(oracle, reference):
+    """volume.hpp:107,110: scalar and vector trilinear_sample, restatement vs reference."""
+    shape = (7, 9, 8)
+    img, fld = random_volume(shape, 61), random_field(shape, 62, 2.0)
+    pts = _points(shape, 63)
+    assert np.array_equal(oracle.trilinear_sample(img, pts), reference.trilinear_sample(img, pts))
+    assert np.array_equal(oracle.trilinear_sample(fld, pts), reference.trilinear_sample(fld, pts))
+
+
+@pytest.mark.parametrize("s", [1, 2])
+def test_data_term_value_bit_exact(oracle, reference, s):
+    shape = (6, 8, 10)
+    t, w = random_volume(shape, 64), random_volume(shape, 65)
+    g, v = random_field(shape, 66, 1.0), random_field(shape, 67, 0.5)
+    assert oracle.data_term_value(t, w, g, v, s) == reference.data_term_value(t, w, g, v, s)
