@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
     float* BP = a.F.BP + (size_t)pair * 3 * N;
     const float* G = a.F.G + (size_t)pair * 3 * N;
     const float* Dd = a.F.D + (size_t)pair * N;
-    float2* S = a.F.S + (size_t)pair * 3 * hx * lines;
+    C* S = spectrum_of<C>(a.F, pair);  // fp32 storage, fp64 in precise mode
 
     if (a.prefetch && (MODE == X_GENERAL || MODE == X_SECOND)) {
         // Stream this tile's field rows into L2 while the spectrum loads and the
@@ -143,10 +143,10 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
     // ---- phase 1: x c2r of the filtered spectrum -> w_{k-1} (real, in smem) ----
     if (MODE != X_FIRST && MODE != X_FWD) {
         for (int c = 0; c < 3; ++c) {
-            const float2* Sc = S + (size_t)c * hx * lines;
+            const C* Sc = S + (size_t)c * hx * lines;
             for (int idx = tid; idx < hx * TL; idx += nthr) {
                 const int p = idx >> lt, l = idx & tm;
-                sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? cvt_c<C>(Sc[(size_t)p * lines + L0 + l]) : CT<C>::make(0, 0);
+                sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? Sc[(size_t)p * lines + L0 + l] : CT<C>::make(0, 0);
             }
             __syncthreads();
             C* bc = sm.buf + (size_t)c * TL * PM;
@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
 #pragma unroll
         for (int c = 0; c < 3; ++c) ldv<VEC>(G + (size_t)c * N + gi, g[c]);
         ldv<VEC>(Dd + gi, dv);
-        if (DT == 1) ldv<VEC>(a.F.T + (size_t)pair * N + gi, tv);  // l1: D = warped, residual from both
+        // l1 / precise: D holds the warped image, the residual is formed from both (exact form)
+        constexpr bool EXACT = DT == 1 || sizeof(C) == 16;
+        if (EXACT) ldv<VEC>(a.F.T + (size_t)pair * N + gi, tv);
         float vn[3][VEC];
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             const float bhj[3] = {bh[0][j], bh[1][j], bh[2][j]};
             const float gj[3] = {g[0][j], g[1][j], g[2][j]};
             float vj[3];
-            if (DT == 1) v_update_voxel_exact<1>(whj, bhj, gj, dv[j], tv[j], theta, eps, vj);
+            if (EXACT) v_update_voxel_exact<DT>(whj, bhj, gj, dv[j], tv[j], theta, eps, vj);
             else v_update_voxel<DT>(whj, bhj, gj, (double)dv[j], theta, inv_theta, eps, vj);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -405,8 +407,9 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
                 s_change += fabs((double)vj[c] - (double)vp[c][j]);
             }
             if (a.sp.log_objective) {
-                if (DT == 1) {
-                    s_obj += fabs(data_residual_exact(gj, vj, dv[j], tv[j]));
+                if (EXACT) {
+                    const double rho = data_residual_exact(gj, vj, dv[j], tv[j]);
+                    s_obj += DT == 1 ? fabs(rho) : 0.5 * rho * rho;
                 } else {
                     const double rho = ((double)gj[0] * vj[0] + (double)gj[1] * vj[1] + (double)gj[2] * vj[2]) +
                                        (double)dv[j];
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             } else {
                 X = bl[sm.xpos[k]];
             }
-            if (!(a.dbg_skip & 4)) S[((size_t)c * hx + k) * lines + L0 + l] = to_f2(X);
+            if (!(a.dbg_skip & 4)) S[((size_t)c * hx + k) * lines + L0 + l] = X;
         }
     }
 

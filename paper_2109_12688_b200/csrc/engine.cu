@@ -145,6 +145,7 @@ struct Geometry {
     DevArray<float> sx, sy, sz, sy_fast, sz_fast;
     DevArray<double2> twx64, xtw64, twy64, twz64;  // precise-mode tables
     DevArray<double> sx64, sy64, sz64;
+    DevArray<double> cx64, cy64, cz64;  // reference axis cosines for the precise multiplier
     int fast = 0, prefetch = 1;
     size_t xsmem = 0, psmem = 0;
 
@@ -236,6 +237,17 @@ struct Geometry {
             sd.assign(Nz, 0.0);
             for (int pos = 0; pos < Nz; ++pos) sd[pos] = s64(freq_of_pos(pz, pos), Nz);
             up(sz64, sd);
+            // axis_cosines (regularizer.cpp:24-31): the same expression, c[0] forced to 1
+            auto cos_ref = [](int k, int n) { return k == 0 ? 1.0 : std::cos(2.0 * kPi * k / n); };
+            sd.assign(hx, 0.0);
+            for (int p = 0; p < hx; ++p) sd[p] = cos_ref(p, M);
+            up(cx64, sd);
+            sd.assign(Ny, 0.0);
+            for (int pos = 0; pos < Ny; ++pos) sd[pos] = cos_ref(freq_of_pos(py, pos), Ny);
+            up(cy64, sd);
+            sd.assign(Nz, 0.0);
+            for (int pos = 0; pos < Nz; ++pos) sd[pos] = cos_ref(freq_of_pos(pz, pos), Nz);
+            up(cz64, sd);
         }
         // 1 = plane_fast_kernel; >= 2 (default 3) = register-blocked plane_reg_kernel where
         // it applies (first stages radix 8 on y and Nz / 16 on z, second stages in smem)
@@ -279,6 +291,7 @@ struct Workspace {
     DevArray<float> V, BH, WP, BP, G, D, I0, I1, PHI0, PHI1, W0, W1;
     DevArray<float2> S;
     DevArray<float2> S2;  // scratch spectrum for the logged objective (solve_velocity only; lazy)
+    DevArray<double2> S64, S264;  // fp64 spectrum (+ scratch) of the precise mode (lazy)
     DevArray<PairState> st;
     DevArray<double> part, diag, energy;
     DevArray<float> stage_t, stage_s, stage3, phi_soa, warped;
@@ -340,6 +353,10 @@ struct Workspace {
         clear_graphs();
     }
 
+    void ensure_s64() {  // precise mode's fp64 spectrum (allocated before any graph capture)
+        if (!S64.p) S64.alloc(S.n);
+    }
+
     void ensure_diag(int iters) {
         if (iters > diag_iters) {
             diag.alloc((size_t)P * iters * 3);
@@ -367,6 +384,7 @@ struct Workspace {
         F.D = D.p;
         F.T = I0.p;
         F.S = S.p;
+        F.S64 = S64.p;
         F.st = st_shared ? st_shared : st.p;
         F.part = part.p;
         F.diag = with_diag ? diag.p : nullptr;
@@ -635,6 +653,10 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     p.lambda64 = sp.lambda;
     p.theta64 = sp.theta;
     p.scale64 = sp.theta / (double)w.geo.N;
+    p.cx64 = w.geo.cx64.p;
+    p.cy64 = w.geo.cy64.p;
+    p.cz64 = w.geo.cz64.p;
+    p.inv_count = 1.0 / (double)w.geo.N;
     p.F = w.fields(diag);
     p.py = w.geo.py;
     p.pz = w.geo.pz;
@@ -662,6 +684,13 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     return p;
 }
 
+// Precision policy: 0 auto -- fp64 spectral arithmetic and storage for
+// solves over 100 iterations (the accelerated iteration amplifies rounding) and for the
+// l1 data term (its shrinkage branch does); 1 always fp32; 2 always fp64.
+bool solve_precise(int policy, const dreg_solver_cfg& s) {
+    return policy == 2 || (policy == 0 && (s.max_iters > 100 || s.data_term == 1));
+}
+
 // One accelerated-ADMM velocity solve for all active pairs (admm.cpp:252-314):
 // grad/diff setup, then I iterations of (plane, xpass).  need_tail adds the last
 // w-update (only the constraint-residual diagnostic depends on it).
@@ -672,11 +701,13 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     sp.log_objective = log_obj ? 1 : 0;
     const int I = s.max_iters;
     const std::vector<double> coef = nesterov_coefs(I, s.accelerate != 0);
-    if (with_setup) L(launch_grad_diff(w.vg(), w.regbufs(), w.fields(diag), s.data_term == 1, P, st));
+
     // precision policy: the accelerated iteration amplifies per-iteration
     // rounding, so long solves get fp64 spectral arithmetic (storage stays fp32)
-    const int pol = L.c->precision;
-    const bool precise = pol == 2 || (pol == 0 && (I > 100 || s.data_term == 1));
+    const bool precise = solve_precise(L.c->precision, s);
+    if (precise && !w.S64.p) throw ArgFail("precise solve needs the workspace's fp64 spectrum");
+    // the exact fp64 point-wise form (l1, precise) reads warped and target themselves
+    if (with_setup) L(launch_grad_diff(w.vg(), w.regbufs(), w.fields(diag), s.data_term == 1 || precise, P, st));
     XArgs xa = make_xargs(w, sp, diag, precise);
     PArgs pa = make_pargs(w, sp, diag, precise);
     pa.need_tail = need_tail ? 1 : 0;
@@ -689,9 +720,11 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
         fa.k = k;
         fa.add_bh = 0;
         fa.F.S = w.S2.p;
+        fa.F.S64 = w.S264.p;
         PArgs ea = pa;
         ea.k = k;
         ea.F.S = w.S2.p;
+        ea.F.S64 = w.S264.p;
         L(launch_xpass(fa, X_FWD, P, st));
         L(launch_plane(ea, 1, P, st));
         L(launch_objective_accumulate(w.fields(true), w.energy.p, sp.lambda, k, P, st));
@@ -901,7 +934,7 @@ void fill_results(const PairState* hs, int P, const std::vector<dreg_dims3>& dl,
 // registration; device-resident batches have no copies to hide and take up to 256
 // pairs per launch, which keeps the persistent x-pass's per-CTA tile ranges long
 // (measured at 128 config-3 pairs: 64 -> 112.9, 128 -> 115.1 registrations/s).
-int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs, bool host) {
+int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs, bool host, bool precise) {
     if (c->chunk > 0) return std::min(c->chunk, n_pairs);
     Geometry tmp;
     tmp.M = d.x;
@@ -912,7 +945,7 @@ int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs, bool host) {
     tmp.lines = (long long)d.y * d.z;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t per = Workspace::bytes_per_pair(tmp);
+    const size_t per = Workspace::bytes_per_pair(tmp) + (precise ? sizeof(double2) * 3 * (size_t)tmp.hx * tmp.lines : 0);
     size_t fit = (size_t)(0.6 * (double)free_b) / std::max<size_t>(per, 1);
     {
         auto it = c->wss.find(std::make_tuple(d.x, d.y, d.z));
@@ -1077,7 +1110,15 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     // chunk j's registration (copy streams + double-buffered staging).  A single chunk
     // is not split for overlap: measured at 32 config-2 pairs, 2 x 16 ran 2% slower
     // end to end than 1 x 32 (tools/e2e_probe.py).
-    const int chunk = pick_chunk(c, d, n_pairs, host);
+    bool precise_any = false;
+    {
+        dreg_solver_cfg s = cfg->solver;
+        for (int l = 0; l < cfg->levels; ++l) {
+            s.max_iters = cfg->max_admm_iters_per_level[l];
+            precise_any |= cfg->max_warps_per_level[l] > 0 && solve_precise(c->precision, s);
+        }
+    }
+    const int chunk = pick_chunk(c, d, n_pairs, host, precise_any);
     // level grids, coarsest first (registration.cpp:208-214: dims halved, rounded up)
     std::vector<dreg_dims3> dl((size_t)cfg->levels);
     dl.back() = d;
@@ -1087,6 +1128,13 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     for (int l = 0; l < cfg->levels; ++l) lv[l] = &c->workspace(dl[l], chunk, dl);
     Workspace& w = c->workspace(d, chunk, dl);
     lv.back() = &w;
+    {  // fp64 spectra for the levels whose solves run in precise mode (before graph capture)
+        dreg_solver_cfg s = cfg->solver;
+        for (int l = 0; l < cfg->levels; ++l) {
+            s.max_iters = cfg->max_admm_iters_per_level[l];
+            if (cfg->max_warps_per_level[l] > 0 && solve_precise(c->precision, s)) lv[l]->ensure_s64();
+        }
+    }
     c->ensure_host(w.P);
     c->ensure_states(n_pairs);
     const size_t N = (size_t)w.geo.N;
@@ -1258,6 +1306,10 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
         Workspace& w = c->workspace(d, 1);
         w.ensure_diag(cfg->max_iters);
         if (cfg->log_objective && !w.S2.p) w.S2.alloc(w.S.n);
+        if (solve_precise(c->precision, *cfg)) {
+            w.ensure_s64();
+            if (cfg->log_objective && !w.S264.p) w.S264.alloc(w.S.n);
+        }
         const size_t N = (size_t)w.geo.N;
         cudaStream_t st = c->stream;
         Launcher L{c};
@@ -1312,7 +1364,8 @@ static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, in
         s.theta = 1.0;
     }
     s.log_objective = 0;
-    const bool precise = c->precision == 2 || (c->precision == 0 && (s.max_iters > 100 || s.data_term == 1));
+    const bool precise = solve_precise(c->precision, s);
+    if (precise) w.ensure_s64();
     const SolverParams sp = solver_params(s);
     XArgs xa = make_xargs(w, sp, false, precise);
     xa.k = 5;
@@ -1463,7 +1516,8 @@ int dreg_cuda_w_update(dreg_cuda_ctx* c, const float* v, const float* b_hat, dre
         Launcher L{c};
         L(launch_state_reset(w.st.p, 1, c->stream));
         const SolverParams sp = solver_params(*cfg);
-        const bool precise = c->precision == 2;  // fp64 butterflies / multiplier on request
+        const bool precise = c->precision == 2;  // fp64 butterflies / multiplier / storage on request
+        if (precise) w.ensure_s64();
         XArgs xa = make_xargs(w, sp, false, precise);
         xa.add_bh = 1;
         L(launch_xpass(xa, X_FWD, 1, c->stream));

@@ -51,6 +51,15 @@ __device__ __forceinline__ C cvt_c(float2 v) {
 }
 __device__ __forceinline__ float2 to_f2(float2 v) { return v; }
 __device__ __forceinline__ float2 to_f2(double2 v) { return make_float2((float)v.x, (float)v.y); }
+// spectrum storage element <-> transform element (identity when they match)
+template <class D>
+__device__ __forceinline__ D cconv(float2 v) {
+    return CT<D>::make(v.x, v.y);
+}
+template <class D>
+__device__ __forceinline__ D cconv(double2 v) {
+    return CT<D>::make(v.x, v.y);
+}
 
 template <bool INV, class C>
 __device__ __forceinline__ C rot_mi(C z) {  // multiply by -i (fwd) / +i (inv)

@@ -20,11 +20,22 @@ struct Fields {
     float* D;          // warped - target     [P][N]; l1 data term: the warped image itself
     const float* T;    // target (I0)         [P][N]; l1: residual = g.u + warped - target
     float2* S;         // x-spectrum, plane-major [P][3][hx][lines]
+    double2* S64;      // the same in fp64 for the precise mode (nullptr unless allocated)
     PairState* st;     // [P]
     double* part;      // partial sums        [P][3][kMaxPartials]
     double* diag;      // per-iteration diagnostics [P][max_iters][3] (nullable)
     int diag_stride;   // max_iters
 };
+
+// The x-spectrum of one pair in the storage precision that goes with transform type C:
+// fp32 (F.S) for the fast path, fp64 (F.S64) in precise mode, so the 3-D transform's
+// intermediate is never rounded to fp32 (the reference keeps it in double, fft.cpp:45-46).
+template <class C>
+__device__ __forceinline__ C* spectrum_of(const Fields& F, int pair) {
+    const size_t off = (size_t)pair * 3 * F.hx * (size_t)F.lines;
+    if constexpr (sizeof(C) == 16) return reinterpret_cast<C*>(F.S64) + off;
+    else return reinterpret_cast<C*>(F.S) + off;
+}
 
 // Registration-level buffers.
 struct RegBuffers {

@@ -60,6 +60,13 @@ struct PArgs {
     const double* sy64;
     const double* sz64;
     double lambda64, theta64, scale64;
+    // precise multiplier with the reference's own arithmetic (regularizer.cpp:24-31,51-79,
+    // admm.cpp:92): axis cosines cos(2 pi k / n) (cos 0 := 1) at x-frequency p and at the
+    // digit-reversed y / z positions of the generic plans, and 1 / voxels
+    const double* cx64;
+    const double* cy64;
+    const double* cz64;
+    double inv_count;
     float lambda, theta, scale;  // scale = theta / voxels
     float lam_n, n_f;            // lambda N / theta and N: multiplier 1 / (lam_n K + n_f)
     int pf_ahead;                // plane_reg_kernel: L2-prefetch the plane this many blocks ahead (0 = off)

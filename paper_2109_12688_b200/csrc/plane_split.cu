@@ -53,18 +53,18 @@ __global__ void __launch_bounds__(kST) plane_y_kernel(PArgs a, int ZT, FastDiv f
     const int plane = blockIdx.y;  // c * hx + p
     const int z0 = blockIdx.x * ZT;
     const int nz = min(ZT, Nz - z0);
-    float2* Sp = a.F.S + ((size_t)pair * 3 * hx + plane) * (size_t)a.F.lines + (size_t)z0 * Ny;
+    C* Sp = spectrum_of<C>(a.F, pair) + (size_t)plane * (size_t)a.F.lines + (size_t)z0 * Ny;
     const C* twg = tabs<C>(a).twy;
     for (int i = tid; i < Ny; i += kST) tw[i] = twg[i];
     for (int i = tid; i < ZT * Ny; i += kST) {
         const int r = i / Ny, y = i - r * Ny;
-        rows[r * PY + y] = r < nz ? cvt_c<C>(Sp[i]) : CT<C>::make(0, 0);
+        rows[r * PY + y] = r < nz ? Sp[i] : CT<C>::make(0, 0);
     }
     __syncthreads();
     fft_lines<INV>(rows, ZT, fd_zt, PY, 1, a.py, (const C*)tw, tid, kST);
     for (int i = tid; i < nz * Ny; i += kST) {
         const int r = i / Ny, y = i - r * Ny;
-        Sp[i] = to_f2(rows[r * PY + y]);
+        Sp[i] = rows[r * PY + y];
     }
 }
 
@@ -86,18 +86,39 @@ __global__ void __launch_bounds__(kST) plane_z_kernel(PArgs a, int YT, FastDiv f
     const int c = plane / hx, p = plane - c * hx;
     const int y0 = blockIdx.x * YT;
     const int ny = min(YT, Ny - y0);
-    float2* Sp = a.F.S + ((size_t)pair * 3 * hx + plane) * (size_t)a.F.lines;
+    C* Sp = spectrum_of<C>(a.F, pair) + (size_t)plane * (size_t)a.F.lines;
     const C* twg = tabs<C>(a).twz;
     for (int i = tid; i < Nz; i += kST) tw[i] = twg[i];
     for (int i = tid; i < Nz * YT; i += kST) {
         const int z = i / YT, yy = i - z * YT;
-        cols[z * PC + yy] = yy < ny ? cvt_c<C>(Sp[(size_t)z * Ny + y0 + yy]) : CT<C>::make(0, 0);
+        cols[z * PC + yy] = yy < ny ? Sp[(size_t)z * Ny + y0 + yy] : CT<C>::make(0, 0);
     }
     __syncthreads();
     fft_lines<false>(cols, YT, fd_yt, 1, PC, a.pz, (const C*)tw, tid, kST);
     constexpr bool F64 = std::is_same<C, double2>::value;
     const R sxp = F64 ? (R)a.sx64[p] : (R)a.sx[p];
-    if (MODE == 0) {
+    if (MODE == 0 && F64) {
+        // spec *= theta / (lambda K + theta) * inv_count with K = (2 ((3 - cy) - cz - cx))^n,
+        // operation for operation as admm.cpp:92 / regularizer.cpp:69-76 (no contraction)
+        const double lam = a.lambda64, th = a.theta64, cxp = a.cx64[p];
+        for (int i = tid; i < Nz * YT; i += kST) {
+            const int z = i / YT, yy = i - z * YT;
+            if (yy >= ny) continue;
+            const double yz = __dsub_rn(__dsub_rn(3.0, a.cy64[y0 + yy]), a.cz64[z]);
+            const double base = __dmul_rn(2.0, __dsub_rn(yz, cxp));
+            double K = base;
+            for (int e = 1; e < a.order; ++e) K = __dmul_rn(K, base);
+            const double m = __dmul_rn(__ddiv_rn(th, __dadd_rn(__dmul_rn(lam, K), th)), a.inv_count);
+            const C v = cols[z * PC + yy];
+            cols[z * PC + yy] = CT<C>::make(__dmul_rn((double)v.x, m), __dmul_rn((double)v.y, m));
+        }
+        __syncthreads();
+        fft_lines<true>(cols, YT, fd_yt, 1, PC, a.pz, (const C*)tw, tid, kST);
+        for (int i = tid; i < Nz * YT; i += kST) {
+            const int z = i / YT, yy = i - z * YT;
+            if (yy < ny) Sp[(size_t)z * Ny + y0 + yy] = cols[z * PC + yy];
+        }
+    } else if (MODE == 0) {
         const R lam = F64 ? (R)a.lambda64 : (R)a.lambda, th = F64 ? (R)a.theta64 : (R)a.theta;
         const R scale = F64 ? (R)a.scale64 : (R)a.scale;
         for (int i = tid; i < Nz * YT; i += kST) {
@@ -116,7 +137,7 @@ __global__ void __launch_bounds__(kST) plane_z_kernel(PArgs a, int YT, FastDiv f
         fft_lines<true>(cols, YT, fd_yt, 1, PC, a.pz, (const C*)tw, tid, kST);
         for (int i = tid; i < Nz * YT; i += kST) {
             const int z = i / YT, yy = i - z * YT;
-            if (yy < ny) Sp[(size_t)z * Ny + y0 + yy] = to_f2(cols[z * PC + yy]);
+            if (yy < ny) Sp[(size_t)z * Ny + y0 + yy] = cols[z * PC + yy];
         }
     } else {
         double acc = 0.0;

@@ -115,7 +115,7 @@ __device__ __forceinline__ void st_reals_sum(C* line, int x, const float* v, con
 
 // cp.async all three components' spectrum rows (transposed) into buf; caller waits.
 template <int R2, class C, int NF = kFT>
-__device__ __forceinline__ void stage_spectrum(C* buf, const float2* S, long long lines, long long L0, int nl,
+__device__ __forceinline__ void stage_spectrum(C* buf, const C* S, long long lines, long long L0, int nl,
                                                int tid) {
     constexpr int HX = kR1 * R2 + 1, PM = HX, TL = kFTL;
     for (int i = tid; i < 3 * HX * TL; i += NF) {
@@ -124,7 +124,7 @@ __device__ __forceinline__ void stage_spectrum(C* buf, const float2* S, long lon
         const int c = cp / HX, p = cp - c * HX;
         const bool ok = l < nl;
         if constexpr (sizeof(C) == 16)
-            buf[(c * TL + l) * PM + p] = ok ? cvt_c<C>(S[(size_t)cp * lines + L0 + l]) : CT<C>::make(0, 0);
+            buf[(c * TL + l) * PM + p] = ok ? S[(size_t)cp * lines + L0 + l] : CT<C>::make(0, 0);  // fp64 storage
         else
             cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
     }
@@ -310,7 +310,7 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
 // target values (v_update_voxel_exact) -- and fp64 change / residual / objective sums.
 // The shrinkage's branch |zhat| <= 1 amplifies any rounding difference, so the l1 path
 // spends the extra fp64 issue (it is not the bench path).
-template <int MODE, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0>
+template <int MODE, int DT, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0>
 __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid,
                                                      double& fc, double& fr, double& fo) {
     constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
@@ -398,13 +398,16 @@ __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int
             const float bhj[3] = {bh[0][jj], bh[1][jj], bh[2][jj]};
             const float gj[3] = {g[0][jj], g[1][jj], g[2][jj]};
             float vj[3];
-            v_update_voxel_exact<1>(whj, bhj, gj, wv[jj], tv[jj], theta, eps, vj);
+            v_update_voxel_exact<DT>(whj, bhj, gj, wv[jj], tv[jj], theta, eps, vj);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 vn[c][jj] = vj[c];
                 fc += fabs((double)vj[c] - (double)vp[c][jj]);
             }
-            if (a.sp.log_objective) fo += fabs(data_residual_exact(gj, vj, wv[jj], tv[jj]));
+            if (a.sp.log_objective) {
+                const double rho = data_residual_exact(gj, vj, wv[jj], tv[jj]);
+                fo += DT == 1 ? fabs(rho) : 0.5 * rho * rho;
+            }
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -423,18 +426,18 @@ __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int
 template <int MODE, int DT, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0, class Acc>
 __device__ __forceinline__ void pointwise_any(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid, Acc& fc,
                                               Acc& fr, Acc& fo) {
-    if constexpr (DT == 1)
-        pointwise_tile_exact<MODE, R2, VEC, UNR, C, NTP, HINT>(a, buf, pair, L0, nl, tid, fc, fr, fo);
+    if constexpr (DT == 1 || sizeof(C) == 16)  // l1, or the precise (fp64 transform) mode
+        pointwise_tile_exact<MODE, DT, R2, VEC, UNR, C, NTP, HINT>(a, buf, pair, L0, nl, tid, fc, fr, fo);
     else
         pointwise_tile<MODE, DT, R2, VEC, UNR, C, NTP, HINT>(a, buf, pair, L0, nl, tid, fc, fr, fo);
 }
 
-template <int DT>
-using AccT = typename std::conditional<DT == 1, double, float>::type;
+template <int DT, class C = float2>
+using AccT = typename std::conditional<DT == 1 || sizeof(C) == 16, double, float>::type;
 
 // phase 3: r2c of u (real, natural order in buf) -> spectrum rows in global.
 template <int R2, class C, class Sync, int NF = kFT>
-__device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, float2* S, long long lines,
+__device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, C* S, long long lines,
                                          long long L0, int nl, int tid, Sync sync) {
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     if (nl < TL) {
@@ -475,12 +478,12 @@ __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, flo
         }
         rdft<false, R2>(z0);
         rdft<false, R2>(z1);
-        float2* Sc = S + (size_t)c * HX * lines + L0 + l;
+        C* Sc = S + (size_t)c * HX * lines + L0 + l;
         auto emit = [&](int k, C zk, C zpartner) {
             const C zc = cconj(zpartner);
             const C ee = CT<C>::make((zk.x + zc.x) * 0.5f, (zk.y + zc.y) * 0.5f);
             const C oo = CT<C>::make((zk.y - zc.y) * 0.5f, -(zk.x - zc.x) * 0.5f);
-            Sc[(size_t)k * lines] = to_f2(cadd(ee, cmul(xtw[k], oo)));
+            Sc[(size_t)k * lines] = cadd(ee, cmul(xtw[k], oo));
         };
 #pragma unroll
         for (int p1 = 0; p1 < R2; ++p1) {
@@ -566,16 +569,16 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
     const int nl = (int)min((long long)TL, lines - L0);
     const BlockSync sync{};
 
-    if (MODE != X_FIRST) stage_spectrum<R2>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
+    if (MODE != X_FIRST) stage_spectrum<R2>(buf, spectrum_of<C>(a.F, pair), lines, L0, nl, tid);
     for (int i = tid; i < L; i += kFT) twx[i] = twx_g[i];
     for (int i = tid; i <= HX; i += kFT) xtw[i] = xtw_g[i];
     if (!F64 && MODE != X_FIRST) cp_async_wait_all();
     __syncthreads();
     if (MODE != X_FIRST) c2r_tile<R2>(buf, twx, xtw, tid, sync);
-    AccT<DT> fc = 0, fr = 0, fo = 0;
+    AccT<DT, C> fc = 0, fr = 0, fo = 0;
     pointwise_any<MODE, DT, R2, VEC, UNR>(a, buf, pair, L0, nl, tid, fc, fr, fo);
     if (MODE != X_TAIL)
-        r2c_tile<R2>(buf, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid, sync);
+        r2c_tile<R2>(buf, twx, xtw, spectrum_of<C>(a.F, pair), lines, L0, nl, tid, sync);
     finish_tile<MODE>(a, pair, blockIdx.x, gridDim.x, fc, fr, fo, red, &s_last, tid, sync);
 }
 

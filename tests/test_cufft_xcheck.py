@@ -21,7 +21,7 @@ torch = pytest.importorskip("torch")
 def cufft_w_update(v, bh, cfg, dtype):
     """w = C2R(R2C(v + b_hat) * theta / (lambda K_n + theta)); torch's irfftn divides by N."""
     z, y, x, _ = v.shape
-    K = dreg.laplacian_symbol(cfg.order, (z, y, x)).reshape(z, y, x)[:, :, : x // 2 + 1]
+    K = dreg.laplacian_symbol(cfg.order, (x, y, z))[:, :, : x // 2 + 1]  # Dims3 order in, (z, y, x) out
     mult = torch.as_tensor(cfg.theta / (cfg.lambda_ * K + cfg.theta), device="cuda", dtype=dtype)
     u = torch.as_tensor(v.astype(np.float64) + bh.astype(np.float64), device="cuda", dtype=dtype)
     u = u.permute(3, 0, 1, 2)  # [c][z][y][x]

@@ -464,6 +464,56 @@ def test_config3_all_pairs_against_oracle_records(ctx):
     assert not mismatch, mismatch
 
 
+def _load_phi_fixture(name):
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "run_config3_phi", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "run_config3_phi.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.load(os.path.join(os.path.dirname(__file__), "golden", name))
+
+
+@pytest.mark.slow
+def test_config3_bench_path_full_fields(ctx):
+    """The bench's own call -- all 256 config-3 pairs in ONE device-resident launch chunk
+    (dreg_cuda_register_batch_device) -- against the oracle: every voxel of phi for the 8
+    pairs in tests/golden/config3_phi (tools/run_config3_phi.py; quantised 2^-16) within
+    max-abs 1e-3 and rel-L2 1e-4, and velocity / solve / iteration / folding counts of all
+    256 pairs equal to tests/golden/config3_oracle.json."""
+    import json
+
+    torch = pytest.importorskip("torch")
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    rec = json.load(open(os.path.join(gold, "config3_oracle.json")))["pairs"]
+    shape = (64, 128, 128)
+    N = int(np.prod(shape))
+    F, M = synth.make_batch(3, 1000, 256, shape)
+    tgt = torch.from_numpy(F.reshape(256, N)).cuda()
+    src = torch.from_numpy(M.reshape(256, N)).cuda()
+    phi = torch.empty((256, 3, N), dtype=torch.float32, device="cuda")
+    ctx.set_batch_chunk(0)  # library policy: one 256-pair chunk for a device-resident batch
+    res = ctx.register_batch_device(256, tgt.data_ptr(), src.data_ptr(), shape[::-1], synth.config_cfg("config3"),
+                                    phi.data_ptr(), 0)
+    bad = []
+    for i in range(256):
+        r, o = res[i], rec[str(1000 + i)]
+        lg = abi.level_logs(r)[0]
+        if not (r.velocity_count == o["velocity_count"] and r.solves == o["solves"]
+                and lg["solver_iterations"] == o["solver_iterations"] and r.folding_voxels == o["folding"]):
+            bad.append(1000 + i)
+    assert not bad, bad
+    worst = (0.0, 0.0)
+    for fn in sorted(os.listdir(os.path.join(gold, "config3_phi"))):
+        seed = int(fn.split(".")[0])
+        ref = _load_phi_fixture(os.path.join("config3_phi", fn))  # (z, y, x, 3)
+        got = phi[seed - 1000].cpu().numpy().reshape(3, *shape).transpose(1, 2, 3, 0)
+        e, r = max_abs(got, ref), rel_l2(got, ref)
+        worst = (max(worst[0], e), max(worst[1], r))
+        assert e <= PHI_MAX_ABS and r <= PHI_REL_L2, (seed, e, r)
+    print(f"config 3 full fields (8 pairs): worst max-abs {worst[0]:.2e}, rel-L2 {worst[1]:.2e}")
+
+
 # ---- robustness: grids through the generic kernels, mixed-validity batches --------------
 @pytest.mark.parametrize("shape", [(8, 12, 20), (10, 16, 48), (12, 20, 96), (16, 16, 160), (4, 4, 4)])
 def test_register_generic_grids(ctx, oracle, shape):

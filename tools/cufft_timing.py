@@ -39,7 +39,7 @@ def main():
     a = ap.parse_args()
     z, y, x = SHAPE
     N = z * y * x
-    K = dreg.laplacian_symbol(2, SHAPE).reshape(z, y, x)[:, :, : x // 2 + 1]
+    K = dreg.laplacian_symbol(2, (x, y, z))[:, :, : x // 2 + 1]
     mult = torch.as_tensor(1.0 / (0.1 * K + 1.0) / N, device="cuda", dtype=torch.float32)
     cfg = synth.config_cfg("config3")
     print("| pairs | cuFFT R2C+mult+C2R ms | cuFFT us / pair-iter | ours x-pass+plane ms | ours us / pair-iter | ours / cuFFT |")
