@@ -53,21 +53,59 @@ struct NumFail {
     explicit NumFail(std::string m) : msg(std::move(m)) {}
 };
 
+// Guard-band mode (DREG_GUARD=1; compute-sanitizer is unavailable on the GPU pool):
+// every device buffer gets kGuard bytes of a fixed pattern on both sides, and
+// dreg_cuda_check_guards() / the end of every registration verify them -- any kernel
+// write past either end of any workspace buffer is reported (tests/test_guard.py).
+constexpr size_t kGuard = 64 * 1024;
+constexpr unsigned char kGuardByte = 0xA5;
+inline bool guard_mode() {
+    static const int g = [] {
+        const char* v = std::getenv("DREG_GUARD");
+        return v && *v ? std::atoi(v) : 0;
+    }();
+    return g != 0;
+}
+
 template <class T>
 struct DevArray {
     T* p = nullptr;
     size_t n = 0;
+    unsigned char* base = nullptr;  // allocation start (guard mode: p - kGuard)
     DevArray() = default;
     DevArray(const DevArray&) = delete;
     DevArray& operator=(const DevArray&) = delete;
-    ~DevArray() {
-        if (p) cudaFree(p);
+    ~DevArray() { release(); }
+    void release() {
+        if (base) cudaFree(base);
+        base = nullptr;
+        p = nullptr;
     }
     void alloc(size_t count) {
-        if (p) cudaFree(p);
-        p = nullptr;
+        release();
         n = count;
-        if (count) CK(cudaMalloc(&p, sizeof(T) * count));
+        if (!count) return;
+        const size_t bytes = sizeof(T) * count;
+        if (guard_mode()) {
+            CK(cudaMalloc(&base, bytes + 2 * kGuard));
+            CK(cudaMemset(base, kGuardByte, kGuard));
+            CK(cudaMemset(base + kGuard + bytes, kGuardByte, kGuard));
+            p = reinterpret_cast<T*>(base + kGuard);
+        } else {
+            CK(cudaMalloc(&base, bytes));
+            p = reinterpret_cast<T*>(base);
+        }
+    }
+    // true when both guard bands still hold the pattern (always true outside guard mode)
+    bool guards_intact() const {
+        if (!guard_mode() || !base) return true;
+        std::vector<unsigned char> h(kGuard);
+        for (const unsigned char* g : {base, base + kGuard + sizeof(T) * n}) {
+            CK(cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost));
+            for (unsigned char b : h)
+                if (b != kGuardByte) return false;
+        }
+        return true;
     }
 };
 
@@ -308,9 +346,34 @@ struct Workspace {
         graphs.clear();
     }
 
-    static size_t bytes_per_pair(const Geometry& g) {
-        return sizeof(float) * (size_t)g.N * (15 + 1 + 2 + 6 + 2 + 4 + 6 + 3 + 2) +
-               sizeof(float2) * 3 * (size_t)g.hx * g.lines + sizeof(double) * 3 * kMaxPartials;
+    // device bytes per pair: the ADMM state V BH WP BP G (15 words) + D, I0, I1, PHI x2,
+    // WARPED x2 (11) + the x-spectrum; host-buffer batches add the double-buffered staging
+    // (stage_t, stage_s, stage3, warped x2 and phi_soa: 15 words), allocated lazily
+    static size_t bytes_per_pair(const Geometry& g, bool host) {
+        return sizeof(float) * (size_t)g.N * (26 + (host ? 15 : 0)) + sizeof(float2) * 3 * (size_t)g.hx * g.lines +
+               sizeof(double) * 3 * kMaxPartials;
+    }
+
+    void ensure_staging() {  // host-path staging (register_batch from host buffers, AoS I/O)
+        if (stage3.p) return;
+        const size_t N = (size_t)geo.N;
+        stage_t.alloc(2 * P * N);
+        stage_s.alloc(2 * P * N);
+        stage3.alloc(2 * P * 3 * N);
+        phi_soa.alloc(P * 3 * N);
+        warped.alloc(2 * P * N);
+    }
+
+    // guard-band check of every buffer (DREG_GUARD); returns the first corrupted name
+    const char* corrupted_buffer() const {
+#define DREG_G(b) \
+    if (!b.guards_intact()) return #b;
+        DREG_G(V) DREG_G(BH) DREG_G(WP) DREG_G(BP) DREG_G(G) DREG_G(D) DREG_G(I0) DREG_G(I1) DREG_G(PHI0)
+        DREG_G(PHI1) DREG_G(W0) DREG_G(W1) DREG_G(S) DREG_G(S2) DREG_G(S64) DREG_G(S264) DREG_G(st) DREG_G(part)
+        DREG_G(diag) DREG_G(energy) DREG_G(stage_t) DREG_G(stage_s) DREG_G(stage3) DREG_G(phi_soa) DREG_G(warped)
+        DREG_G(tgt_tab) DREG_G(src_tab) DREG_G(phi_tab) DREG_G(warped_tab) DREG_G(counter) DREG_G(scal) DREG_G(fscal)
+#undef DREG_G
+        return nullptr;
     }
 
     void alloc(dreg_dims3 d, int pairs) {
@@ -335,12 +398,6 @@ struct Workspace {
         st.alloc(P);
         part.alloc((size_t)P * 3 * kMaxPartials);
         energy.alloc(P);
-        // host-path staging is double-buffered (two chunks in flight: copies overlap compute)
-        stage_t.alloc(2 * P * N);
-        stage_s.alloc(2 * P * N);
-        stage3.alloc(2 * P * 3 * N);
-        phi_soa.alloc(P * 3 * N);
-        warped.alloc(2 * P * N);
         tgt_tab.alloc(P);
         src_tab.alloc(P);
         phi_tab.alloc(P);
@@ -945,7 +1002,7 @@ int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs, bool host, bool prec
     tmp.lines = (long long)d.y * d.z;
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t per = Workspace::bytes_per_pair(tmp) + (precise ? sizeof(double2) * 3 * (size_t)tmp.hx * tmp.lines : 0);
+    const size_t per = Workspace::bytes_per_pair(tmp, host) + (precise ? sizeof(double2) * 3 * (size_t)tmp.hx * tmp.lines : 0);
     size_t fit = (size_t)(0.6 * (double)free_b) / std::max<size_t>(per, 1);
     {
         auto it = c->wss.find(std::make_tuple(d.x, d.y, d.z));
@@ -953,6 +1010,17 @@ int pick_chunk(dreg_cuda_ctx* c, dreg_dims3 d, int n_pairs, bool host, bool prec
     }
     int P = (int)std::min<size_t>(fit, host ? 64 : 256);
     return std::max(1, std::min(P, n_pairs));
+}
+
+// DREG_GUARD: verify every workspace buffer's guard bands (see DevArray)
+void check_guards(dreg_cuda_ctx* c) {
+    if (!guard_mode()) return;
+    CK(cudaDeviceSynchronize());
+    for (auto& kv : c->wss)
+        if (const char* b = kv.second->corrupted_buffer())
+            throw CudaFail(std::string("guard band corrupted after the call: buffer ") + b + " of workspace " +
+                           std::to_string(std::get<0>(kv.first)) + "x" + std::to_string(std::get<1>(kv.first)) + "x" +
+                           std::to_string(std::get<2>(kv.first)));
 }
 
 }  // namespace
@@ -1137,6 +1205,7 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     }
     c->ensure_host(w.P);
     c->ensure_states(n_pairs);
+    if (tgt_host) w.ensure_staging();
     const size_t N = (size_t)w.geo.N;
     const size_t Pc = (size_t)w.P;
     cudaStream_t st = c->stream;
@@ -1232,6 +1301,7 @@ static int register_impl(dreg_cuda_ctx* c, int n_pairs, const float* const* tgt_
     }
     CK(cudaStreamSynchronize(st));
     if (host) CK(cudaStreamSynchronize(c->d2h));
+    check_guards(c);
     std::vector<PairState> states(c->h_states, c->h_states + n_pairs);
     const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     for (int q = 0; q < n_pairs; ++q) {
@@ -1305,6 +1375,7 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
         if (!target || !warped_source || !velocity_out) throw ArgFail("null buffer");
         Workspace& w = c->workspace(d, 1);
         w.ensure_diag(cfg->max_iters);
+        w.ensure_staging();
         if (cfg->log_objective && !w.S2.p) w.S2.alloc(w.S.n);
         if (solve_precise(c->precision, *cfg)) {
             w.ensure_s64();
@@ -1326,6 +1397,7 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* c, const float* target, const float*
         std::vector<double> dg((size_t)3 * w.diag_iters);
         CK(cudaMemcpyAsync(dg.data(), w.diag.p, sizeof(double) * dg.size(), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        check_guards(c);
         if (diag) {
             diag->iterations = hs.iterations;
             diag->final_change = hs.final_change;
@@ -1421,6 +1493,7 @@ int dreg_cuda_time_iteration(dreg_cuda_ctx* c, const dreg_solver_cfg* cfg, int r
 // ---- building blocks ------------------------------------------------------------
 static void upload_aos(dreg_cuda_ctx* c, Workspace& w, const float* host_aos, float* dev_soa) {
     const size_t N = (size_t)w.geo.N;
+    w.ensure_staging();
     CK(cudaMemcpyAsync(w.stage3.p, host_aos, sizeof(float) * 3 * N, cudaMemcpyHostToDevice, c->stream));
     CK(launch_aos_to_soa((long long)N, w.stage3.p, dev_soa, c->stream));
     c->launches += 1;
@@ -1428,6 +1501,7 @@ static void upload_aos(dreg_cuda_ctx* c, Workspace& w, const float* host_aos, fl
 
 static void download_aos(dreg_cuda_ctx* c, Workspace& w, const float* dev_soa, float* host_aos) {
     const size_t N = (size_t)w.geo.N;
+    w.ensure_staging();
     CK(launch_soa_to_aos((long long)N, dev_soa, w.stage3.p, c->stream));
     c->launches += 1;
     CK(cudaMemcpyAsync(host_aos, w.stage3.p, sizeof(float) * 3 * N, cudaMemcpyDeviceToHost, c->stream));
@@ -1711,6 +1785,7 @@ int dreg_cuda_upsample_velocity(dreg_cuda_ctx* c, const float* v, dreg_dims3 sd,
         if (dd.x < sd.x || dd.y < sd.y || dd.z < sd.z)
             throw ArgFail("upsample_velocity: target dims smaller than source");
         Workspace& w = c->workspace(dd, 1);  // destination-sized buffers hold both
+        w.ensure_staging();
         const VolGeom src{sd.x, sd.y, sd.z, (long long)sd.x * sd.y * sd.z};
         const VolGeom dst = w.vg();
         CK(cudaMemcpyAsync(w.stage3.p, v, sizeof(float) * 3 * src.N, cudaMemcpyHostToDevice, c->stream));
