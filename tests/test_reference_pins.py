@@ -415,26 +415,22 @@ def test_register_sphere_to_ellipsoid(lib, reference):
     assert lib.jacobian_stats(phi).nonpositive == 0
 
 
-def _perturbed(img, seed=0, amp=6e-8):
-    rng = np.random.default_rng(seed)
-    return (img * (1.0 + rng.uniform(-1.0, 1.0, img.shape) * amp)).astype(np.float32)
-
-
 def test_acceptance_diffeomorphism(lib, reference, oracle):
     """acceptance_main.cpp:261-291 (criterion 5): 13 registrations at 32^3 -- translate
     (3, 0, 0), sphere -> ellipsoid, random smooth seeds 3 and 100..109 (l1, n 2,
     lambda 10, theta 0.05, capped, 3 levels) -- all with 0% non-positive Jacobians.
 
-    The GPU additionally matches the oracle's velocity count, and phi within the
-    contract (max-abs 1e-3, rel-L2 1e-4) OR within twice the oracle's own largest
-    response to four rounding-level perturbations of the target (1 ulp and 1e-6
-    relative, two draws each), whichever is larger: the l1 pyramid is chaotic (the
-    shrinkage z / max(|z|, 1) switches branch on rounding-level changes and the
-    accept/continue decisions compound it), so the reference itself moves phi by up to
-    ~0.5 voxel under a 1-ulp input change."""
+    The GPU additionally matches the oracle's velocity count and phi within the contract
+    (max-abs 1e-3, rel-L2 1e-4).  The l1 pyramid is chaotic (the shrinkage
+    z / max(|z|, 1) switches branch on rounding-level changes: the oracle itself moves
+    phi by up to 0.27 voxel under a 1-ulp change of the target), so the
+    l1 path runs the precise mode, which repeats the reference's arithmetic (fp64
+    spectrum, the reference's multiplier expression, unfused fp64 point-wise updates):
+    on all 13 cases phi is bit-identical to the oracle (tools/l1_parity_table.py)."""
     cases = [("translate", dict(shift=(3.0, 0.0, 0.0))), ("sphere_ellipsoid", {})]
     cases += [("random_smooth", dict(seed=sd)) for sd in [3] + list(range(100, 110))]
     cfg = _capped(1, 10.0, 3)
+    identical = 0
     for kind, kw in cases:
         t, s, _, _ = reference.make_case(kind, (32, 32, 32), **kw)
         phi, warped, res = lib.register_pair(t, s, cfg)
@@ -444,13 +440,10 @@ def test_acceptance_diffeomorphism(lib, reference, oracle):
             phi_o, _, res_o = oracle.register_pair(t, s, cfg)
             assert res.velocity_count == res_o.velocity_count, (kind, kw)
             err, rel = max_abs(phi, phi_o), rel_l2(phi, phi_o)
-            err_p = rel_p = 0.0
-            if err > 1e-3 or rel > 1e-4:
-                for amp in (6e-8, 1e-6):
-                    for sd in (0, 1):
-                        phi_p, _, _ = oracle.register_pair(_perturbed(t, sd, amp), s, cfg)
-                        err_p, rel_p = max(err_p, max_abs(phi_p, phi_o)), max(rel_p, rel_l2(phi_p, phi_o))
-            assert err <= max(1e-3, 2 * err_p) and rel <= max(1e-4, 2 * rel_p), (kind, kw, err, rel, err_p, rel_p)
+            assert err <= 1e-3 and rel <= 1e-4, (kind, kw, err, rel)
+            identical += int(np.array_equal(phi, phi_o))
+    if lib is not oracle:
+        print(f"criterion 5: {identical}/13 phi bit-identical to the oracle")
 
 
 def test_accepted_sad_monotone_and_velocity_bound(lib, reference):
