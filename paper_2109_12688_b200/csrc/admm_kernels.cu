@@ -115,9 +115,9 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
     __syncthreads();
 
     float* V = a.F.V + (size_t)pair * 3 * N;
-    float* BH = a.F.BH + (size_t)pair * 3 * N;
+    float* BH = a.F.BH + (size_t)pair * 3 * N;  // iterations: b_{k-2} in, b_k out (X_FWD: b_hat input)
     float* WP = a.F.WP + (size_t)pair * 3 * N;
-    float* BP = a.F.BP + (size_t)pair * 3 * N;
+    const float* BP = a.F.BP + (size_t)pair * 3 * N;  // b_{k-1}
     const float* G = a.F.G + (size_t)pair * 3 * N;
     const float* Dd = a.F.D + (size_t)pair * N;
     C* S = spectrum_of<C>(a.F, pair);  // fp32 storage, fp64 in precise mode
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             const C* Sc = S + (size_t)c * hx * lines;
             for (int idx = tid; idx < hx * TL; idx += nthr) {
                 const int p = idx >> lt, l = idx & tm;
-                sm.Xs[idx] = l < nl && !(a.dbg_skip & 4) ? Sc[(size_t)p * lines + L0 + l] : CT<C>::make(0, 0);
+                sm.Xs[idx] = l < nl && !DREG_SKIP(a, 4) ? Sc[(size_t)p * lines + L0 + l] : CT<C>::make(0, 0);
             }
             __syncthreads();
             C* bc = sm.buf + (size_t)c * TL * PM;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             }
             __syncthreads();
         }
-        if (!(a.dbg_skip & 1)) fft_lines<true>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
+        if (!DREG_SKIP(a, 1)) fft_lines<true>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
     }
 
     if constexpr (UTIL) {
@@ -202,28 +202,28 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
 
     // ---- phase 2: point-wise ADMM updates on the tile ----
     const double theta = a.sp.theta, inv_theta = 1.0 / a.sp.theta, eps = a.sp.epsilon;
-    const double coef = a.coef;
+    const double coef = a.coef, coefp = a.coef_prev;
     const bool accel = a.sp.accelerate != 0;
+    const bool hp = a.coef_prev != 0.0;  // b_hat_{k-1} differs from b_{k-1}
     double s_change = 0.0, s_res = 0.0, s_obj = 0.0;
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
     if constexpr (!F64) {
         // fp32 arithmetic, fp32 per-thread partial sums (a thread covers <= ~64 voxels)
         const float thf = (float)theta, ithf = (float)inv_theta, epsf = (float)eps, cf = (float)coef;
+        const float cpf = (float)coefp;
         float fc = 0.f, fr = 0.f, fo = 0.f;
 #pragma unroll 2
-        for (int i0 = tid * VEC; i0 < (UTIL || (a.dbg_skip & 2) ? 0 : nvox); i0 += nthr * VEC) {
+        for (int i0 = tid * VEC; i0 < (UTIL || DREG_SKIP(a, 2) ? 0 : nvox); i0 += nthr * VEC) {
             const int l = i0 / M, x0 = i0 - l * M;
             const size_t gi = base + i0;
             float w[3][VEC], vp[3][VEC], bo[3][VEC], wp[3][VEC], bp[3][VEC], g[3][VEC], dv[VEC];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 if (MODE != X_FIRST) ldv<VEC>(V + (size_t)c * N + gi, vp[c]);
-                if (MODE == X_GENERAL) ldv<VEC>(BH + (size_t)c * N + gi, bo[c]);
-                if (MODE == X_GENERAL && accel) {
-                    ldv<VEC>(WP + (size_t)c * N + gi, wp[c]);
-                    ldv<VEC>(BP + (size_t)c * N + gi, bp[c]);
-                }
+                if (MODE == X_GENERAL) ldv<VEC>(BP + (size_t)c * N + gi, bp[c]);
+                if (MODE == X_GENERAL && hp) ldv<VEC>(BH + (size_t)c * N + gi, bo[c]);
+                if (MODE == X_GENERAL && accel) ldv<VEC>(WP + (size_t)c * N + gi, wp[c]);
                 if (MODE != X_TAIL) ldv<VEC>(G + (size_t)c * N + gi, g[c]);
             }
             if (MODE != X_TAIL) ldv<VEC>(Dd + gi, dv);
@@ -234,7 +234,9 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
                 for (int j = 0; j < VEC; ++j) {
                     w[c][j] = MODE == X_FIRST ? 0.f : (float)(!a.odd ? reinterpret_cast<const R*>(bl)[x0 + j] : bl[x0 + j].x);
                     if (MODE == X_FIRST) vp[c][j] = 0.f;
+                    // b_hat_{k-1} re-formed from the stored dual iterates b_{k-1}, b_{k-2} (admm.cpp:130-139)
                     if (MODE != X_GENERAL) bo[c][j] = 0.f;
+                    else bo[c][j] = hp ? fmaf(cpf, bp[c][j] - bo[c][j], bp[c][j]) : bp[c][j];
                 }
             }
             if (MODE == X_TAIL) {
@@ -288,12 +290,9 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             }
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                if (MODE != X_FIRST && accel) {
-                    stv<VEC>(WP + (size_t)c * N + gi, w[c]);
-                    stv<VEC>(BP + (size_t)c * N + gi, bo[c]);
-                }
+                if (MODE != X_FIRST && accel) stv<VEC>(WP + (size_t)c * N + gi, w[c]);
+                if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bo[c]);  // b_k over b_{k-2}
                 stv<VEC>(V + (size_t)c * N + gi, vn[c]);
-                if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bh[c]);
                 C* bl = sm.buf + (size_t)(c * TL + l) * PM;
 #pragma unroll
                 for (int j = 0; j < VEC; ++j) {
@@ -307,7 +306,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
         s_res = fr;
         s_obj = fo;
     } else {
-    for (int i0 = tid * VEC; i0 < (UTIL || (a.dbg_skip & 2) ? 0 : nvox); i0 += nthr * VEC) {
+    for (int i0 = tid * VEC; i0 < (UTIL || DREG_SKIP(a, 2) ? 0 : nvox); i0 += nthr * VEC) {
         const int l = i0 / M, x0 = i0 - l * M;
         const size_t gi = base + i0;
         float w[3][VEC], vp[3][VEC];
@@ -350,9 +349,23 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
         } else {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float bo[VEC];
-                if (MODE == X_GENERAL) ldv<VEC>(BH + (size_t)c * N + gi, bo);
-                else {
+                float bo[VEC], bp[VEC];
+                if (MODE == X_GENERAL) {
+                    // b_hat_{k-1} = float(b_{k-1} + c_{k-2} (b_{k-1} - b_{k-2})) (admm.cpp:130-139),
+                    // the reference's expression on the stored fp32 iterates: the same bits
+                    ldv<VEC>(BP + (size_t)c * N + gi, bp);
+                    if (hp) {
+                        ldv<VEC>(BH + (size_t)c * N + gi, bo);
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) {
+                            const double ab = bp[j];
+                            bo[j] = (float)__dadd_rn(ab, __dmul_rn(coefp, __dsub_rn(ab, (double)bo[j])));
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < VEC; ++j) bo[j] = bp[j];
+                    }
+                } else {
 #pragma unroll
                     for (int j = 0; j < VEC; ++j) bo[j] = 0.f;
                 }
@@ -365,9 +378,8 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
                     s_res += dd * dd;
                 }
                 if (accel && MODE == X_GENERAL) {
-                    float wp[VEC], bp[VEC];
+                    float wp[VEC];
                     ldv<VEC>(WP + (size_t)c * N + gi, wp);
-                    ldv<VEC>(BP + (size_t)c * N + gi, bp);
 #pragma unroll
                     for (int j = 0; j < VEC; ++j) {  // av + scale * (av - b), unfused like the reference
                         const double aw = w[c][j], ab = b[j];
@@ -379,10 +391,8 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
 #pragma unroll
                     for (int j = 0; j < VEC; ++j) { wh[c][j] = w[c][j]; bh[c][j] = b[j]; }
                 }
-                if (accel) {
-                    stv<VEC>(WP + (size_t)c * N + gi, w[c]);
-                    stv<VEC>(BP + (size_t)c * N + gi, b);
-                }
+                if (accel) stv<VEC>(WP + (size_t)c * N + gi, w[c]);
+                stv<VEC>(BH + (size_t)c * N + gi, b);  // b_k over b_{k-2}
             }
         }
         float g[3][VEC], dv[VEC], tv[VEC];
@@ -420,7 +430,6 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             stv<VEC>(V + (size_t)c * N + gi, vn[c]);
-            if (MODE != X_FIRST) stv<VEC>(BH + (size_t)c * N + gi, bh[c]);
             C* bl = sm.buf + (size_t)(c * TL + l) * PM;
             if (!a.odd) {
                 R* ul = reinterpret_cast<R*>(bl);
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             }
         }
         __syncthreads();
-        if (!(a.dbg_skip & 1)) fft_lines<false>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
+        if (!DREG_SKIP(a, 1)) fft_lines<false>(sm.buf, 3 * TL, a.fd_lines, PM, 1, a.px, sm.twx, tid, nthr);
         for (int cidx = tid; cidx < 3 * hx * TL; cidx += nthr) {
             const int c = cidx >= 2 * hx * TL ? 2 : (cidx >= hx * TL ? 1 : 0);
             const int idx = cidx - c * hx * TL;
@@ -461,7 +470,7 @@ __global__ void __launch_bounds__(kXThreads, (VEC == 4 && F64) ? 2 : MINB) xpass
             } else {
                 X = bl[sm.xpos[k]];
             }
-            if (!(a.dbg_skip & 4)) S[((size_t)c * hx + k) * lines + L0 + l] = X;
+            if (!DREG_SKIP(a, 4)) S[((size_t)c * hx + k) * lines + L0 + l] = X;
         }
     }
 
@@ -636,7 +645,6 @@ static cudaError_t launch_x_dt(const XArgs& a, int npairs, cudaStream_t s) {
 
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s) {
     if (mode <= X_TAIL && xpass_fast_eligible(a)) return launch_xpass_fast(a, mode, npairs, s);
-    if (mode <= X_TAIL && xpass_tma_eligible(a)) return launch_xpass_tma(a, mode, npairs, s);
     switch (mode) {
         case X_FIRST: return launch_x_dt<X_FIRST>(a, npairs, s);
         case X_SECOND: return launch_x_dt<X_SECOND>(a, npairs, s);

@@ -176,7 +176,7 @@ float one_minus_cos(int k, int n) {  // 1 - cos(2 pi k / n) = 2 sin^2(pi k / n);
 struct Geometry {
     int M = 0, Ny = 0, Nz = 0, hx = 0;
     long long N = 0, lines = 0;
-    int L = 0, odd = 0, TL = 0, TLp = 0, PM = 0, PY = 0, xvec = 1, tma = 0;
+    int L = 0, odd = 0, TL = 0, TLp = 0, PM = 0, PY = 0, xvec = 1;
     AxisPlan px{}, py{}, pz{};
     DevArray<float2> twx, xtw, twy, twz;
     DevArray<int> xpos;
@@ -201,8 +201,7 @@ struct Geometry {
         pz = make_plan(Nz);
         PM = (L % 2 == 0) ? L + 1 : L;
         PY = (Ny % 2 == 0) ? Ny + 1 : Ny;
-        tma = env_int("DREG_TMA", 0) && (M % 4 == 0) && (lines % 2 == 0);
-        TL = tma ? env_int("DREG_TMA_TL", 8) : env_int("DREG_TL", 32);
+        TL = env_int("DREG_TL", 32);
         xvec = env_int("DREG_XVEC", 2);
         {
             int t = 4;  // power of two (the x-pass index math uses shifts)
@@ -685,9 +684,9 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.odd = w.geo.odd;
     a.vec = w.geo.xvec;
     a.prefetch = w.geo.prefetch && (w.geo.M % 4 == 0);
-    a.tma = w.geo.tma;
-    a.tma_ctas_per_sm = env_int("DREG_TMA_CTAS", 1);
+#ifdef DREG_EXPERIMENTS
     a.dbg_skip = env_int("DREG_DBG_SKIP", 0);
+#endif
     a.f64 = env_int("DREG_F64", 0);
     a.minb = env_int("DREG_XMINB", 3);
     a.fast_x = env_int("DREG_FAST_X", 1);
@@ -788,13 +787,20 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     };
     xa.k = 0;
     xa.coef = 0.0;
+    xa.coef_prev = 0.0;
     L(launch_xpass(xa, X_FIRST, P, st));
     if (log_obj) energy(0);
+    // The dual iterates ping-pong between the two b buffers: pass k reads b_{k-1} (F.BP) and
+    // b_{k-2} (F.BH), re-forms b_hat_{k-1} with c_{k-2} and writes b_k over b_{k-2}.
+    float* const bbuf[2] = {xa.F.BH, xa.F.BP};
     for (int k = 1; k < I; ++k) {
         pa.k = k - 1;
         L(launch_plane(pa, 0, P, st));
         xa.k = k;
         xa.coef = coef[k - 1];
+        xa.coef_prev = k >= 2 ? coef[k - 2] : 0.0;
+        xa.F.BP = bbuf[(k - 1) & 1];
+        xa.F.BH = bbuf[k & 1];
         L(launch_xpass(xa, k == 1 ? X_SECOND : X_GENERAL, P, st));
         if (log_obj) energy(k);
     }
@@ -1442,6 +1448,7 @@ static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, in
     XArgs xa = make_xargs(w, sp, false, precise);
     xa.k = 5;
     xa.coef = 0.5;
+    xa.coef_prev = 0.4;
     PArgs pa = make_pargs(w, sp, false, precise);
     Launcher L{c};
     L(launch_state_reset(w.st.p, P, st));
@@ -1470,7 +1477,7 @@ static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, in
     const double spec = 2.0 * 3.0 * (double)w.geo.hx * (double)w.geo.lines * 8.0;  // read + write
     out[0] = tx / reps;
     out[1] = tp / reps;
-    out[2] = P * (28.0 * 4.0 * N + spec);  // 16 field words read + 12 written, spectrum in/out
+    out[2] = P * (25.0 * 4.0 * N + spec);  // 16 field words read + 9 written (v, b, w), spectrum in/out
     out[3] = P * spec;
     out[4] = P;
     out[5] = precise ? 1.0 : 0.0;

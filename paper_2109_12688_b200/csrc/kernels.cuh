@@ -13,9 +13,10 @@ struct Fields {
     long long N;       // voxels
     long long lines;   // Ny * Nz x-lines
     float* V;          // v_k                 [P][3][N]
-    float* BH;         // b_hat_k             [P][3][N]
+    float* BH;         // dual iterate b_{k-2} in, b_k out (the two b buffers swap roles every
+                       // iteration; b_hat is re-formed from them)  [P][3][N]
     float* WP;         // w_{k-1} (w_prev)    [P][3][N]
-    float* BP;         // b_{k-1} (b_prev)    [P][3][N]
+    float* BP;         // dual iterate b_{k-1}  [P][3][N]
     float* G;          // grad(warped)        [P][3][N]
     float* D;          // warped - target     [P][N]; l1 data term: the warped image itself
     const float* T;    // target (I0)         [P][N]; l1: residual = g.u + warped - target

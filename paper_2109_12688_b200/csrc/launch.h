@@ -5,6 +5,14 @@
 
 #include "kernels.cuh"
 
+// Work-skipping switches exist only in experiment builds (make EXPERIMENTS=1); the
+// release library has no way to skip part of an iteration.
+#ifdef DREG_EXPERIMENTS
+#define DREG_SKIP(a, bit) (((a).dbg_skip & (bit)) != 0)
+#else
+#define DREG_SKIP(a, bit) false
+#endif
+
 namespace dregb {
 
 // X_FIRST/SECOND/GENERAL: ADMM iteration k = 0 / 1 / >= 2; X_TAIL: w and residual of the
@@ -20,6 +28,7 @@ struct XArgs {
     const int* xpos;    // position of frequency k in the digit-reversed line, k in [0, L)
     SolverParams sp;
     double coef;        // Nesterov coefficient c_{k-1} (admm.cpp:294-295)
+    double coef_prev;   // c_{k-2}: b_hat_{k-1} = b_{k-1} + c_{k-2} (b_{k-1} - b_{k-2}) is re-formed, not stored
     int k;              // iteration index
     int TL;             // x-lines per CTA
     int PM;             // shared-memory line pitch (complex, odd)
@@ -27,8 +36,6 @@ struct XArgs {
     int add_bh;         // X_FWD: transform V + BH instead of V
     int vec;            // point-wise vector width (1, 2 or 4; 4/2 need M % 4 / M % 2 == 0)
     int prefetch;       // L2 bulk prefetch of the tile's field rows at kernel start
-    int tma;            // use the TMA-staged x-pass (xpass_tma.cu) when eligible
-    int tma_ctas_per_sm;  // persistent CTAs per SM for the TMA x-pass
     int f64;            // fp64 point-wise arithmetic in the generic x-pass (DREG_F64)
     int minb;           // x-pass launch-bounds variant: min CTAs per SM (3 or 4)
     int fast_x;         // use the specialised x-pass (xpass_fast.cu) for M in {64, 128, 256}
@@ -36,7 +43,9 @@ struct XArgs {
     int precise;        // fp64 x-FFT arithmetic (long solves; see plane_split.cu)
     const double2* twx64;
     const double2* xtw64;
+#ifdef DREG_EXPERIMENTS
     int dbg_skip;       // timing experiments only (DREG_DBG_SKIP): 1 = skip x-FFTs, 2 = skip point-wise, 4 = skip spectrum I/O
+#endif
     FastDiv fd_lines;   // divide by 3 * TL
     int pipe;           // warp-specialised persistent x-pass for X_GENERAL, M in {64, 128} (DREG_PIPE: 0 off; default on)
     int pipe_all;       // A/B knob (DREG_PIPE_ALL): split all pairs' tiles statically, not just the iterating ones
@@ -90,9 +99,6 @@ bool plane_reg_supported(int Ny, int Nz);
 bool plane_split_needed(const PArgs& a);
 cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
-bool xpass_tma_eligible(const XArgs& a);
-size_t xpass_tma_smem_bytes(int L, int hx, int TL, int PM, int M);
-cudaError_t launch_xpass_tma(const XArgs& a, int mode, int npairs, cudaStream_t s);
 bool xpass_fast_eligible(const XArgs& a);
 cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s);

@@ -203,14 +203,15 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
     constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
     const long long N = a.F.N;
     float* V = a.F.V + (size_t)pair * 3 * N;
-    float* BH = a.F.BH + (size_t)pair * 3 * N;
+    float* BO = a.F.BH + (size_t)pair * 3 * N;  // b_{k-2} in, b_k out (the dual iterates ping-pong)
     float* WP = a.F.WP + (size_t)pair * 3 * N;
-    float* BP = a.F.BP + (size_t)pair * 3 * N;
+    const float* BP = a.F.BP + (size_t)pair * 3 * N;  // b_{k-1}
     const float* G = a.F.G + (size_t)pair * 3 * N;
     const float* Dd = a.F.D + (size_t)pair * N;
     const float thf = (float)a.sp.theta, ithf = (float)(1.0 / a.sp.theta), epsf = (float)a.sp.epsilon;
-    const float cf = (float)a.coef;
+    const float cf = (float)a.coef, cpf = (float)a.coef_prev;
     const bool accel = a.sp.accelerate != 0;
+    const bool hp = a.coef_prev != 0.0;  // b_hat_{k-1} differs from b_{k-1}
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
 #pragma unroll UNR
@@ -221,11 +222,9 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (MODE != X_FIRST) ldvN<VEC, HINT>(V + (size_t)c * N + gi, vp[c]);
-            if (MODE == X_GENERAL) ldvN<VEC, HINT>(BH + (size_t)c * N + gi, bo[c]);
-            if (MODE == X_GENERAL && accel) {
-                ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
-                ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);
-            }
+            if (MODE == X_GENERAL) ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);        // b_{k-1}
+            if (MODE == X_GENERAL && hp) ldvN<VEC, HINT>(BO + (size_t)c * N + gi, bo[c]);  // b_{k-2}
+            if (MODE == X_GENERAL && accel) ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
             if (MODE != X_TAIL) ldvN<VEC, HINT>(G + (size_t)c * N + gi, g[c]);
         }
         if (MODE != X_TAIL) ldvN<VEC, HINT>(Dd + gi, dv);
@@ -239,7 +238,11 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
                     w[c][jj] = 0.f;
                     vp[c][jj] = 0.f;
                 }
+                // b_hat_{k-1} = b_{k-1} + c_{k-2} (b_{k-1} - b_{k-2}) (admm.cpp:130-139), re-formed from
+                // the two stored dual iterates -- the bits the previous pass computed -- instead of a
+                // stored b_hat field (saves one 12 B/voxel write per iteration)
                 if (MODE != X_GENERAL) bo[c][jj] = 0.f;
+                else bo[c][jj] = hp ? fmaf(cpf, bp[c][jj] - bo[c][jj], bp[c][jj]) : bp[c][jj];
             }
         }
         if (MODE == X_TAIL) {
@@ -293,12 +296,9 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            if (MODE != X_FIRST && accel) {
-                stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
-                stvN<VEC>(BP + (size_t)c * N + gi, bo[c]);
-            }
+            if (MODE != X_FIRST && accel) stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
+            if (MODE != X_FIRST) stvN<VEC>(BO + (size_t)c * N + gi, bo[c]);  // b_k over b_{k-2}
             stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
-            if (MODE != X_FIRST) stvN<VEC>(BH + (size_t)c * N + gi, bh[c]);
             st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);
         }
     }
@@ -316,14 +316,15 @@ __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int
     constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
     const long long N = a.F.N;
     float* V = a.F.V + (size_t)pair * 3 * N;
-    float* BH = a.F.BH + (size_t)pair * 3 * N;
+    float* BO = a.F.BH + (size_t)pair * 3 * N;  // b_{k-2} in, b_k out (the dual iterates ping-pong)
     float* WP = a.F.WP + (size_t)pair * 3 * N;
-    float* BP = a.F.BP + (size_t)pair * 3 * N;
+    const float* BP = a.F.BP + (size_t)pair * 3 * N;  // b_{k-1}
     const float* G = a.F.G + (size_t)pair * 3 * N;
     const float* Wd = a.F.D + (size_t)pair * N;  // l1: D holds the warped image itself
     const float* Td = a.F.T + (size_t)pair * N;
-    const double theta = a.sp.theta, eps = a.sp.epsilon, coef = a.coef;
+    const double theta = a.sp.theta, eps = a.sp.epsilon, coef = a.coef, coefp = a.coef_prev;
     const bool accel = a.sp.accelerate != 0;
+    const bool hp = a.coef_prev != 0.0;
     const size_t base = (size_t)L0 * M;
     const int nvox = nl * M;
 #pragma unroll UNR
@@ -334,11 +335,9 @@ __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (MODE != X_FIRST) ldvN<VEC, HINT>(V + (size_t)c * N + gi, vp[c]);
-            if (MODE == X_GENERAL) ldvN<VEC, HINT>(BH + (size_t)c * N + gi, bo[c]);
-            if (MODE == X_GENERAL && accel) {
-                ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
-                ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);
-            }
+            if (MODE == X_GENERAL) ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);        // b_{k-1}
+            if (MODE == X_GENERAL && hp) ldvN<VEC, HINT>(BO + (size_t)c * N + gi, bo[c]);  // b_{k-2}
+            if (MODE == X_GENERAL && accel) ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
             if (MODE != X_TAIL) ldvN<VEC, HINT>(G + (size_t)c * N + gi, g[c]);
         }
         if (MODE != X_TAIL) {
@@ -355,7 +354,13 @@ __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int
                     w[c][jj] = 0.f;
                     vp[c][jj] = 0.f;
                 }
+                // b_hat_{k-1} = float(b_{k-1} + c_{k-2} (b_{k-1} - b_{k-2})) (admm.cpp:130-139): the
+                // reference's own expression on the stored fp32 iterates, so the same bits
                 if (MODE != X_GENERAL) bo[c][jj] = 0.f;
+                else if (hp) {
+                    const double db1 = (double)bp[c][jj];
+                    bo[c][jj] = (float)__dadd_rn(db1, __dmul_rn(coefp, __dsub_rn(db1, (double)bo[c][jj])));
+                } else bo[c][jj] = bp[c][jj];
             }
         }
         if (MODE == X_TAIL) {
@@ -411,12 +416,9 @@ __device__ __forceinline__ void pointwise_tile_exact(const XArgs& a, C* buf, int
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            if (MODE != X_FIRST && accel) {
-                stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
-                stvN<VEC>(BP + (size_t)c * N + gi, bo[c]);
-            }
+            if (MODE != X_FIRST && accel) stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
+            if (MODE != X_FIRST) stvN<VEC>(BO + (size_t)c * N + gi, bo[c]);  // b_k over b_{k-2}
             stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
-            if (MODE != X_FIRST) stvN<VEC>(BH + (size_t)c * N + gi, bh[c]);
             st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);  // u = v + b_hat (admm.cpp:77-80)
         }
     }
@@ -693,7 +695,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             if (cur >= 0) {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
                 sync();  // staged spectrum (and, first round, the tables) visible to the group
-                if (!(a.dbg_skip & 1)) c2r_tile<R2, float2, NamedSync<kBarFFT, NF>, NF>(buf, twx, xtw, tid, sync);
+                if (!DREG_SKIP(a, 1)) c2r_tile<R2, float2, NamedSync<kBarFFT, NF>, NF>(buf, twx, xtw, tid, sync);
             }
             if (tid == 0) tile_of[b] = cur;
             ring_bar<kBarW, NALL, true>(b);
@@ -705,7 +707,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
                 const int pair = plist[prev / T], tile = prev - (prev / T) * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
-                if (!(a.dbg_skip & 1))
+                if (!DREG_SKIP(a, 1))
                     r2c_tile<R2, float2, NamedSync<kBarFFT, NF>, NF>(ring + pb * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl,
                                  tid, sync);
                 sync();  // buffer pb is restaged next round by this group
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             const long long L0 = (long long)tile * TL;
             const int nl = (int)min((long long)TL, lines - L0);
             AccT<DT> fc = 0, fr = 0, fo = 0;
-            if (!(a.dbg_skip & 2))
+            if (!DREG_SKIP(a, 2))
                 pointwise_any<MODE, DT, R2, VEC, UNR, float2, NTP, HINT>(a, ring + b * BUF, pair, L0, nl, tid, fc,
                                                                          fr, fo);
             ring_bar<kBarU, NALL, true>(b);
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             acc[2] += (double)fo;
             // the run ends at the pair's last tile or the end of this CTA's range
             if (tile != T - 1 && cur + 1 != g_end) continue;
-            if (a.dbg_skip & 8) {
+            if (DREG_SKIP(a, 8)) {
                 acc[0] = acc[1] = acc[2] = 0.0;
                 run_start = -1;
                 continue;
