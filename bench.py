@@ -423,16 +423,34 @@ def run_ours(args, rank, world, local_rank):
         with open(peaks_path) as f:
             peak = float(json.load(f)["hbm_gbs"])
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
-    achieved = tk["xpass_bytes"] / (tk["xpass_ms"] / 1e3) / 1e9
+    # the two per-iteration kernels; `roofline` describes the one that takes longer
+    ss = tk.get("spectral_state", 0)
+    kern = {
+        "xpass": {
+            "what": ("xpass, spectral-state form (x c2r -> v-update -> x r2c; streams grad, diff"
+                     + (", v" if ss == 1 else "") + " and the x-spectrum)") if ss else
+                    "xpass (fused x c2r + dual/Nesterov + v-update + x r2c)",
+            "ms": tk["xpass_ms"], "bytes": tk["xpass_bytes"]},
+        "plane": {
+            "what": ("plane, spectral-state form (yz FFT -> U_j = V^ + (1-m) Ut_{j-1}, Ut_j, (2m-1) Ut_j / N -> "
+                     "yz FFT^-1; 5 half-spectra)") if ss else "plane (yz FFT -> multiplier -> yz FFT^-1)",
+            "ms": tk["plane_ms"], "bytes": tk["plane_bytes"]},
+    }
+    for kv in kern.values():
+        kv["GBps"] = kv["bytes"] / (kv["ms"] / 1e3) / 1e9
+        kv["frac"] = kv["GBps"] / peak
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    achieved = kern[dom]["GBps"]
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "xpass_dram_bytes.json")
+    prof = os.path.join(ROOT, "profiles", "ss_dram_bytes.json" if ss else "xpass_dram_bytes.json")
     if os.path.exists(prof) and name == "config3":
         with open(prof) as f:
             pj = json.load(f)
+        pj = pj.get(dom, pj) if ss else (pj if dom == "xpass" else {})
         if pj.get("pairs"):
             traffic = pj["dram_bytes_per_launch"] / pj["pairs"] * tk["pairs"]
             traffic_src = ("recorded ncu constant, not measured in this run: dram__bytes_read.sum + "
-                           f"dram__bytes_write.sum of one x-pass launch ({pj.get('source', 'profiles/')}), "
+                           f"dram__bytes_write.sum of one {dom} launch ({pj.get('source', 'profiles/')}), "
                            "scaled per pair to this launch")
     it_ms = tk["xpass_ms"] + tk["plane_ms"]
     line = {
@@ -464,7 +482,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "roofline": {
             "bound": "hbm",
-            "kernel": "xpass (fused c2r + dual/Nesterov + v-update + r2c)",
+            "kernel": kern[dom]["what"],
             "achieved": achieved,
             "peak": peak,
             "peak_source": peak_src,
@@ -472,12 +490,16 @@ def run_ours(args, rank, world, local_rank):
             "frac": achieved / peak,
             "traffic": traffic,
             "traffic_source": traffic_src,
-            "bytes_per_launch": tk["xpass_bytes"],
+            "bytes_per_launch": kern[dom]["bytes"],
             "pairs_per_launch": tk["pairs"],
+            "iteration_state": {0: "real-space (w, b fields)", 1: "spectral (U_j, U_{j-1}), change norm on",
+                                2: "spectral (U_j, U_{j-1}), no change norm (tol = 0)"}[ss],
+            "kernels": kern,
             "xpass_ms": tk["xpass_ms"],
             "plane_ms": tk["plane_ms"],
-            "plane_GBps": tk["plane_bytes"] / (tk["plane_ms"] / 1e3) / 1e9,
+            "plane_GBps": kern["plane"]["GBps"],
             "iteration_ms_per_pair": it_ms / tk["pairs"],
+            "iteration_bytes_per_voxel": (tk["xpass_bytes"] + tk["plane_bytes"]) / tk["pairs"] / N,
             "iteration_frac": (tk["xpass_bytes"] + tk["plane_bytes"]) / (it_ms / 1e3) / 1e9 / peak,
             "precise": bool(tk.get("precise", 0)),
         },

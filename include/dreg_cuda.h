@@ -240,7 +240,9 @@ int dreg_cuda_solve_velocity(dreg_cuda_ctx* ctx, const float* target,
 int dreg_cuda_time_kernels(dreg_cuda_ctx* ctx, int reps, double* out);
 /* Same, with `cfg`'s data term / order / lambda / theta and the precision the
  * context's policy picks for cfg->max_iters; out[5] = 1 when the precise (fp64
- * spectral arithmetic) kernels were timed.  out holds 6 doubles. */
+ * spectral arithmetic) kernels were timed; out[6] = 0 when the real-space-state kernels
+ * were timed, 1 / 2 for the spectral-state pair with / without the change norm (the
+ * kernels a registration's solves run for this configuration).  out holds 7 doubles. */
 int dreg_cuda_time_iteration(dreg_cuda_ctx* ctx, const dreg_solver_cfg* cfg, int reps, double* out);
 
 /* ---- DREG volume container (io.hpp:15-41; README.md:99-114) ---------------------

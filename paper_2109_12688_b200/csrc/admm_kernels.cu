@@ -645,6 +645,7 @@ static cudaError_t launch_x_dt(const XArgs& a, int npairs, cudaStream_t s) {
 
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s) {
     if (mode <= X_TAIL && xpass_fast_eligible(a)) return launch_xpass_fast(a, mode, npairs, s);
+    if (mode == X_SS || mode == X_SSN) return launch_xpass_fast(a, mode, npairs, s);  // fast kernels only
     switch (mode) {
         case X_FIRST: return launch_x_dt<X_FIRST>(a, npairs, s);
         case X_SECOND: return launch_x_dt<X_SECOND>(a, npairs, s);
@@ -702,6 +703,21 @@ static cudaError_t launch_reg(const PArgs& a, int mode, int npairs, cudaStream_t
     using Lay = PlaneLayout<NY, NY / 8>;
     const size_t smem = sizeof(float2) * (NZ * Lay::P + NY + NZ) + sizeof(double) * 32 + sizeof(float) * (NY + NZ);
     void (*k)(PArgs) = plane_reg_kernel<NY, NZ, R1Z, 1, 0>;
+    if (mode == 2) {  // spectral-state iteration: 2 CTAs per SM, all 16 state elements of a radix block in flight
+        constexpr int DB = (NY * NZ <= 8192) ? 3 : 1, B2 = DB > 1 ? 2 : 1;
+        switch (a.order) {
+            case 1: k = plane_reg_kernel<NY, NZ, R1Z, 2, 1, B2, 16>; break;
+            case 2:
+                switch (a.ss_variant) {  // DREG_PLANE_SS = CTAs per SM * 100 + load batch (experiment knob)
+                    case 304: k = plane_reg_kernel<NY, NZ, R1Z, 2, 2, DB, 4>; break;
+                    case 208: k = plane_reg_kernel<NY, NZ, R1Z, 2, 2, B2, 8>; break;
+                    default: k = plane_reg_kernel<NY, NZ, R1Z, 2, 2, B2, 16>; break;
+                }
+                break;
+            case 3: k = plane_reg_kernel<NY, NZ, R1Z, 2, 3, B2, 16>; break;
+            default: k = plane_reg_kernel<NY, NZ, R1Z, 2, 0, B2, 16>; break;
+        }
+    }
     if (mode == 0) {
         switch (a.order) {
             case 1: k = plane_reg_kernel<NY, NZ, R1Z, 0, 1>; break;

@@ -382,9 +382,12 @@ struct Workspace {
         P = pairs;
         const size_t N = (size_t)geo.N;
         V.alloc(P * 3 * N);
-        BH.alloc(P * 3 * N);
+        // the two dual-iterate buffers double as the spectral-state iteration's U_j / U_{j-1}
+        // ([3][hx][lines] complex = 3 (M + 2) lines floats per pair)
+        const size_t bwords = (size_t)P * 3 * (size_t)(geo.M + 2) * (size_t)geo.lines;
+        BH.alloc(std::max((size_t)P * 3 * N, bwords));
         WP.alloc(P * 3 * N);
-        BP.alloc(P * 3 * N);
+        BP.alloc(std::max((size_t)P * 3 * N, bwords));
         G.alloc(P * 3 * N);
         D.alloc(P * N);
         I0.alloc(P * N);
@@ -693,6 +696,7 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.fx_variant = env_int("DREG_FX", 22);
     a.pipe = env_int("DREG_PIPE", 1);
     a.pipe_all = env_int("DREG_PIPE_ALL", 0);
+    a.pipe_ss = env_int("DREG_PIPE_SS", 120442);
     if (precise) a.TL = w.geo.TLp;
     a.fd_lines.init((unsigned)(3 * a.TL));
     return a;
@@ -729,6 +733,7 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     // plane_reg_kernel L2-prefetches the plane one wave of resident CTAs ahead (-2% time;
     // an L2 prefetch of the x-pass state instead thrashed L2: +38%)
     p.pf_ahead = env_int("DREG_PLANE_PF", 1);
+    p.ss_variant = env_int("DREG_PLANE_SS", 0);
     p.order = sp.order;
     p.PY = w.geo.PY;
     p.energy_out = w.energy.p;
@@ -746,6 +751,15 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
 bool solve_precise(int policy, const dreg_solver_cfg& s) {
     return policy == 2 || (policy == 0 && (s.max_iters > 100 || s.data_term == 1));
 }
+
+// Which solves run the spectral-state iteration (plane_fast.cuh MODE 2 + X_SS): l2, fp32,
+// grids the register-blocked plane kernel and the pipelined x-pass cover, no diagnostics.
+bool solve_uses_spectral_state(const Workspace& w, const dreg_solver_cfg& s, const XArgs& xa, bool diag, bool need_tail,
+                               bool precise) {
+    return !diag && !need_tail && !precise && s.data_term == 2 && w.geo.fast >= 2 &&
+           plane_reg_supported(w.geo.Ny, w.geo.Nz) && xpass_ss_eligible(xa) && env_int("DREG_SS", 1) != 0;
+}
+bool ss_needs_change(const dreg_solver_cfg& s) { return s.tol > 0.0 || env_int("DREG_SS_CHG", 0) != 0; }
 
 // One accelerated-ADMM velocity solve for all active pairs (admm.cpp:252-314):
 // grad/diff setup, then I iterations of (plane, xpass).  need_tail adds the last
@@ -790,6 +804,32 @@ void enqueue_solve(Launcher& L, Workspace& w, int P, const dreg_solver_cfg& s, b
     xa.coef_prev = 0.0;
     L(launch_xpass(xa, X_FIRST, P, st));
     if (log_obj) energy(0);
+    // Spectral-state iteration (plane_fast.cuh MODE 2 + X_SS): the ADMM state is kept as two
+    // Fourier-domain iterates U_j, U_{j-1} inside the plane pass, the x-pass streams only
+    // v, grad and diff.  Same recurrence (admm.cpp:275-308) in fp32; not for the logged /
+    // diagnostic solves (no w, b fields to take the residual from), l1 or precise mode.
+    const bool ss = solve_uses_spectral_state(w, s, xa, diag, need_tail, precise);
+    if (ss) {
+        // without a tolerance the change norm is not needed: v is neither read nor written
+        // until the last iteration (an exactly-zero change is still caught at k = 0)
+        const int xmode = ss_needs_change(s) ? X_SS : X_SSN;
+        float2* const ubuf[2] = {reinterpret_cast<float2*>(w.BH.p), reinterpret_cast<float2*>(w.BP.p)};
+        pa.inv_nf = (float)(1.0 / (double)w.geo.N);
+        for (int k = 1; k < I; ++k) {
+            pa.k = k - 1;
+            pa.c_cur = (float)coef[k - 1];
+            pa.c_prev = k >= 2 ? (float)coef[k - 2] : 0.f;
+            pa.has1 = k >= 2;
+            pa.has0 = pa.c_prev != 0.f;
+            pa.U1 = ubuf[(k - 1) & 1];
+            pa.U0 = ubuf[k & 1];
+            L(launch_plane(pa, 2, P, st));
+            xa.k = k;
+            xa.ss_last = k == I - 1;
+            L(launch_xpass(xa, xmode, P, st));
+        }
+        return;
+    }
     // The dual iterates ping-pong between the two b buffers: pass k reads b_{k-1} (F.BP) and
     // b_{k-2} (F.BH), re-forms b_hat_{k-1} with c_{k-2} and writes b_k over b_{k-2}.
     float* const bbuf[2] = {xa.F.BH, xa.F.BP};
@@ -1450,19 +1490,32 @@ static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, in
     xa.coef = 0.5;
     xa.coef_prev = 0.4;
     PArgs pa = make_pargs(w, sp, false, precise);
+    // the kernels a registration's solves run: the spectral-state pair when eligible
+    const bool ss = solve_uses_spectral_state(w, s, xa, false, false, precise);
+    const int xmode = !ss ? X_GENERAL : (ss_needs_change(s) ? X_SS : X_SSN);
+    const int pmode = ss ? 2 : 0;
+    if (ss) {
+        pa.inv_nf = (float)(1.0 / (double)w.geo.N);
+        pa.c_cur = 0.5f;
+        pa.c_prev = 0.4f;
+        pa.has1 = pa.has0 = 1;
+        pa.U1 = reinterpret_cast<float2*>(w.BP.p);
+        pa.U0 = reinterpret_cast<float2*>(w.BH.p);
+        xa.ss_last = 0;
+    }
     Launcher L{c};
     L(launch_state_reset(w.st.p, P, st));
     cudaEvent_t e[4];
     for (auto& ev : e) CK(cudaEventCreate(&ev));
     // warm-up
-    L(launch_plane(pa, 0, P, st));
-    L(launch_xpass(xa, X_GENERAL, P, st));
+    L(launch_plane(pa, pmode, P, st));
+    L(launch_xpass(xa, xmode, P, st));
     float tx = 0.f, tp = 0.f;
     for (int r = 0; r < reps; ++r) {
         CK(cudaEventRecord(e[0], st));
-        L(launch_plane(pa, 0, P, st));
+        L(launch_plane(pa, pmode, P, st));
         CK(cudaEventRecord(e[1], st));
-        L(launch_xpass(xa, X_GENERAL, P, st));
+        L(launch_xpass(xa, xmode, P, st));
         CK(cudaEventRecord(e[2], st));
         CK(cudaEventSynchronize(e[2]));
         float a = 0.f, b = 0.f;
@@ -1479,14 +1532,21 @@ static int time_iteration_impl(dreg_cuda_ctx* c, const dreg_solver_cfg* scfg, in
     out[1] = tp / reps;
     out[2] = P * (25.0 * 4.0 * N + spec);  // 16 field words read + 9 written (v, b, w), spectrum in/out
     out[3] = P * spec;
+    if (ss) {
+        // x-pass: grad + diff (4 words) [+ v read and written with the change norm], spectrum in/out;
+        // plane: V^ in, U_{j-1} and U_{j-2} in, U_j and the filtered spectrum out = 5 half-spectra
+        out[2] = P * ((xmode == X_SS ? 10.0 : 4.0) * 4.0 * N + spec);
+        out[3] = P * 2.5 * spec;
+    }
     out[4] = P;
     out[5] = precise ? 1.0 : 0.0;
+    out[6] = ss ? (xmode == X_SS ? 1.0 : 2.0) : 0.0;
     return DREG_OK;
 }
 
 int dreg_cuda_time_kernels(dreg_cuda_ctx* c, int reps, double* out) {
     return guarded(c, [&] {
-        double o[6];
+        double o[7];
         const int r = time_iteration_impl(c, nullptr, reps, o);
         for (int i = 0; i < 5; ++i) out[i] = o[i];
         return r;

@@ -18,7 +18,11 @@ namespace dregb {
 // X_FIRST/SECOND/GENERAL: ADMM iteration k = 0 / 1 / >= 2; X_TAIL: w and residual of the
 // last iteration only (diagnostics); X_FWD: r2c of V (+ BH when add_bh) into S;
 // X_INV: c2r of S into WP.
-enum XMode { X_FIRST = 0, X_SECOND = 1, X_GENERAL = 2, X_TAIL = 3, X_FWD = 4, X_INV = 5 };
+// X_SS / X_SSN: spectral-state iteration (k >= 1; see plane_fast.cuh MODE 2): the staged
+// spectrum is w_hat - b_hat itself, the tile does c2r -> v-update -> r2c of v and streams
+// only v, grad and diff; X_SSN neither reads v (no change norm: tol = 0) nor writes it
+// before the last iteration.
+enum XMode { X_FIRST = 0, X_SECOND = 1, X_GENERAL = 2, X_TAIL = 3, X_FWD = 4, X_INV = 5, X_SS = 6, X_SSN = 7 };
 
 struct XArgs {
     Fields F;
@@ -48,6 +52,8 @@ struct XArgs {
 #endif
     FastDiv fd_lines;   // divide by 3 * TL
     int pipe;           // warp-specialised persistent x-pass for X_GENERAL, M in {64, 128} (DREG_PIPE: 0 off; default on)
+    int pipe_ss;        // warp split of the spectral-state x-pass (DREG_PIPE_SS)
+    int ss_last;        // X_SSN: this is the solve's last iteration (v is written)
     int pipe_all;       // A/B knob (DREG_PIPE_ALL): split all pairs' tiles statically, not just the iterating ones
 };
 
@@ -79,6 +85,13 @@ struct PArgs {
     float lambda, theta, scale;  // scale = theta / voxels
     float lam_n, n_f;            // lambda N / theta and N: multiplier 1 / (lam_n K + n_f)
     int pf_ahead;                // plane_reg_kernel: L2-prefetch the plane this many blocks ahead (0 = off)
+    // spectral-state iteration (plane_reg_kernel MODE 2): the two 3-D Fourier-domain iterates
+    const float2* U1;            // U_{j-1}                 [P][3][hx][Ny*Nz]
+    float2* U0;                  // U_{j-2} in, U_j out
+    float c_cur, c_prev;         // Nesterov coefficients c_{j-1}, c_{j-2}
+    float inv_nf;                // 1 / voxels
+    int ss_variant;              // DREG_PLANE_SS experiment knob
+    int has1, has0;              // U_{j-1} exists (j >= 2); U_{j-2} enters (c_{j-2} != 0)
     int order;
     int PY;             // plane row pitch (complex, odd)
     int k;
@@ -100,6 +113,7 @@ bool plane_split_needed(const PArgs& a);
 cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
 bool xpass_fast_eligible(const XArgs& a);
+bool xpass_ss_eligible(const XArgs& a);
 cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s);
 

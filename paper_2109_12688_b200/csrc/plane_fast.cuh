@@ -257,8 +257,20 @@ __device__ __forceinline__ float kn_pow(float base, int order) {
     }
 }
 
-template <int NY, int NZ, int R1Z, int MODE, int ORD>
-__global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), (NY * NZ <= 8192) ? 3 : 1) plane_reg_kernel(PArgs a) {
+//
+// MODE 2 is the spectral-state iteration: the plane holds V^_j = r2c_x(v_j);
+// the ADMM state lives here, in the 3-D Fourier domain, as U_j = FFT(v_j + b_hat_{j-1})
+// (two iterates, ping-pong).  With m = theta / (lambda K_n + theta) the reference's
+// w_j = m U_j and b_j = (1 - m) U_j (admm.cpp:66-101,142-153), so with the extrapolated
+// Ut_j = U_j + c_{j-1} (U_j - U_{j-1}) (admm.cpp:130-139, linear in w and b alike)
+//     b_hat_j = (1 - m) Ut_j,   w_hat_j - b_hat_j = (2 m - 1) Ut_j.
+// One pass:  U_j = yzFFT(V^_j) + (1 - m) Ut_{j-1};  store U_j over U_{j-2};
+//            plane <- yzFFT^-1((2 m - 1) Ut_j / N)   (= the v-update's argument, x-spectrum).
+// Element (b, e) of a plane's state sits at e * (NY * R1Z) + b (coalesced per e).
+// UPF = state elements per load batch: batch 0 is issued before the forward radix-R2Z, batch
+// n + 1 before batch n is consumed (register software pipeline); MINB = CTAs per SM.
+template <int NY, int NZ, int R1Z, int MODE, int ORD, int MINB = ((NY * NZ <= 8192) ? 3 : 1), int UPF = 4>
+__global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), MINB) plane_reg_kernel(PArgs a) {
     constexpr int R2Y = NY / 8, R2Z = NZ / R1Z, NT = R2Y * R2Z;
     static_assert(R2Y <= 16 && R2Z <= 16 && (R1Z == 4 || R1Z == 8), "radix split outside rdft<>");
     using Lay = PlaneLayout<NY, R2Y>;
@@ -288,6 +300,14 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), (NY * NZ <= 8192) ? 3 :
     const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
     float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)a.F.lines;
     const int y1 = tid % R2Y, z1 = tid / R2Y;
+    if (MODE == 2 && tid == 0) {
+        // this plane's state iterates are needed after the forward transforms: bring them to L2 now
+        const size_t pl = ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)(NY * NZ);
+        if (a.has1)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.U1 + pl), "r"((unsigned)(NY * NZ * 8)) : "memory");
+        if (a.has0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.U0 + pl), "r"((unsigned)(NY * NZ * 8)) : "memory");
+    }
 
     // stage A: global -> registers (all loads in flight at once)
     float2 x[R1Z][8];  // [z sub-index][y sub-index]
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), (NY * NZ <= 8192) ? 3 :
 #pragma unroll
         for (int t = 0; t < 8; ++t) x[u][t] = __ldg(Sp + (z1 + R2Z * u) * NY + y1 + R2Y * t);
     // position tables doubled (exact) for the multiplier base 2 (sx + sy + sz)
-    const float dbl = MODE == 0 ? 2.0f : 1.0f;
+    const float dbl = MODE != 1 ? 2.0f : 1.0f;
     for (int i = tid; i < NY; i += NT) {
         twy[i] = __ldg(a.twy + i);
         sys[i] = dbl * __ldg(a.sy_fast + i);
@@ -354,11 +374,50 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), (NY * NZ <= 8192) ? 3 :
     for (int b = tid; b < NY * R1Z; b += NT) {
         const int y = b % NY, blk = b / NY;
         float2 v[R2Z];
+        float2 u1[R2Z], u0[R2Z];  // MODE 2: U_{j-1}, U_{j-2} of this thread's elements
+        const float2* U1 = nullptr;
+        float2* U0 = nullptr;
+        auto load_state = [&](int e0) {
+#pragma unroll
+            for (int q = 0; q < UPF; ++q) {
+                const int e = e0 + q;
+                u1[e] = a.has1 ? __ldcs(U1 + (size_t)e * (NY * R1Z)) : make_float2(0.f, 0.f);
+                u0[e] = a.has0 ? __ldcs(U0 + (size_t)e * (NY * R1Z)) : u1[e];
+            }
+        };
+        if (MODE == 2) {
+            const size_t pl = ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)(NY * NZ) + b;
+            U1 = a.U1 + pl;  // U_{j-1}
+            U0 = a.U0 + pl;  // U_{j-2} in, U_j out
+            load_state(0);   // in flight across the shared-memory loads and the forward radix
+        }
 #pragma unroll
         for (int e = 0; e < R2Z; ++e) v[e] = buf[Lay::at(y, blk * R2Z + e)];
         rdft<false, R2Z>(v);
         const float sy = sys[y];
-        if (MODE == 0) {
+        if (MODE == 2) {
+            const float sxy = sxp + sy;  // doubled
+            const float cc = a.c_cur, cp = a.c_prev, inv_n = a.inv_nf;
+#pragma unroll
+            for (int e0 = 0; e0 < R2Z; e0 += UPF) {
+                if (e0 + UPF < R2Z) load_state(e0 + UPF);
+#pragma unroll
+                for (int q = 0; q < UPF; ++q) {
+                    const int e = e0 + q;
+                    // q_ = (lambda N / theta) K_n:  1 - m = q_ r,  (2 m - 1) / N = (N - q_) r / N,  r = 1 / (q_ + N)
+                    const float qk = lam_n * kn_pow<ORD>(sxy + szs[blk * R2Z + e], order);
+                    const float r = rcp_nr(qk + n_f);
+                    const float m1 = qk * r, m2 = (n_f - qk) * r * inv_n;
+                    const float2 utp = make_float2(fmaf(cp, u1[e].x - u0[e].x, u1[e].x), fmaf(cp, u1[e].y - u0[e].y, u1[e].y));
+                    const float2 un = make_float2(fmaf(m1, utp.x, v[e].x), fmaf(m1, utp.y, v[e].y));
+                    __stcs(U0 + (size_t)e * (NY * R1Z), un);
+                    v[e] = make_float2(m2 * fmaf(cc, un.x - u1[e].x, un.x), m2 * fmaf(cc, un.y - u1[e].y, un.y));
+                }
+            }
+            rdft<true, R2Z>(v);
+#pragma unroll
+            for (int e = 0; e < R2Z; ++e) buf[Lay::at(y, blk * R2Z + e)] = v[e];
+        } else if (MODE == 0) {
             const float sxy = sxp + sy;  // doubled
 #pragma unroll
             for (int e = 0; e < R2Z; ++e) {

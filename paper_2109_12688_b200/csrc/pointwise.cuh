@@ -84,7 +84,9 @@ __device__ __forceinline__ double data_residual_exact(const float g[3], const fl
 // l2: v = u - g (g.u + d) / (theta + |g|^2), algebraically equal to the reference's
 //     rhs/theta - g (g.rhs) / (theta (theta + |g|^2)), rhs = theta u - d g;
 // l1: identical expression order to admm.cpp:33-39.
-template <int DT>
+// FASTDIV (spectral-state x-pass, theta + |g|^2 >= theta > 0): MUFU.RCP + one Newton step
+// instead of the IEEE division's slow path.
+template <int DT, bool FASTDIV = false>
 __device__ __forceinline__ void v_update_voxel_f32(const float wh[3], const float bh[3], const float g[3], float d,
                                                    float theta, float inv_theta, float eps, float v[3]) {
     const float ux = wh[0] - bh[0], uy = wh[1] - bh[1], uz = wh[2] - bh[2];
@@ -96,7 +98,7 @@ __device__ __forceinline__ void v_update_voxel_f32(const float wh[3], const floa
         const float clip = zhat / fmaxf(fabsf(zhat), 1.0f);
         s = clip * inv_theta;
     } else {
-        s = (gu + d) / (theta + gg);
+        s = FASTDIV ? (gu + d) * rcp_nr(theta + gg) : (gu + d) / (theta + gg);
     }
     v[0] = fmaf(-g[0], s, ux);
     v[1] = fmaf(-g[1], s, uy);

@@ -114,19 +114,27 @@ __device__ __forceinline__ void st_reals_sum(C* line, int x, const float* v, con
 // runs the phase; `sync` is that group's barrier.
 
 // cp.async all three components' spectrum rows (transposed) into buf; caller waits.
+// A thread keeps its line l = tid % 32 and walks the (component, x-bin) rows with
+// incremental addresses (the index arithmetic was 24 integer instructions per 8-byte
+// copy, 17% of the spectral-state x-pass's issue slots).
 template <int R2, class C, int NF = kFT>
 __device__ __forceinline__ void stage_spectrum(C* buf, const C* S, long long lines, long long L0, int nl,
                                                int tid) {
     constexpr int HX = kR1 * R2 + 1, PM = HX, TL = kFTL;
-    for (int i = tid; i < 3 * HX * TL; i += NF) {
-        const int l = i & (TL - 1);
-        const int cp = i >> 5;  // c * HX + p
-        const int c = cp / HX, p = cp - c * HX;
-        const bool ok = l < nl;
-        if constexpr (sizeof(C) == 16)
-            buf[(c * TL + l) * PM + p] = ok ? S[(size_t)cp * lines + L0 + l] : CT<C>::make(0, 0);  // fp64 storage
-        else
-            cp_async8(buf + (c * TL + l) * PM + p, S + (size_t)cp * lines + L0 + (ok ? l : 0), ok);
+    static_assert(NF % TL == 0, "a thread keeps its line");
+    constexpr int STEP = NF / TL;
+    const int l = tid & (TL - 1);
+    const bool ok = l < nl;
+    int cp = tid >> 5;  // c * HX + p
+    const C* src = S + (size_t)cp * lines + L0 + (ok ? l : 0);
+    C* dst = buf + l * PM + cp;
+    const size_t sstep = (size_t)STEP * lines;
+#pragma unroll 4
+    for (; cp < 3 * HX; cp += STEP, src += sstep, dst += STEP) {
+        // row (c, p) of line l lives at (c * TL + l) * PM + p = l * PM + cp + c * (TL * PM - HX)
+        C* d = dst + (cp >= 2 * HX ? 2 * (TL * PM - HX) : (cp >= HX ? TL * PM - HX : 0));
+        if constexpr (sizeof(C) == 16) *d = ok ? *src : CT<C>::make(0, 0);  // fp64 storage
+        else cp_async8(d, src, ok);
     }
 }
 
@@ -221,7 +229,7 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
         float w[3][VEC], vp[3][VEC], bo[3][VEC], wp[3][VEC], bp[3][VEC], g[3][VEC], dv[VEC];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            if (MODE != X_FIRST) ldvN<VEC, HINT>(V + (size_t)c * N + gi, vp[c]);
+            if (MODE != X_FIRST && MODE != X_SSN) ldvN<VEC, HINT>(V + (size_t)c * N + gi, vp[c]);
             if (MODE == X_GENERAL) ldvN<VEC, HINT>(BP + (size_t)c * N + gi, bp[c]);        // b_{k-1}
             if (MODE == X_GENERAL && hp) ldvN<VEC, HINT>(BO + (size_t)c * N + gi, bo[c]);  // b_{k-2}
             if (MODE == X_GENERAL && accel) ldvN<VEC, HINT>(WP + (size_t)c * N + gi, wp[c]);
@@ -238,6 +246,7 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
                     w[c][jj] = 0.f;
                     vp[c][jj] = 0.f;
                 }
+                if (MODE == X_SSN) vp[c][jj] = 0.f;
                 // b_hat_{k-1} = b_{k-1} + c_{k-2} (b_{k-1} - b_{k-2}) (admm.cpp:130-139), re-formed from
                 // the two stored dual iterates -- the bits the previous pass computed -- instead of a
                 // stored b_hat field (saves one 12 B/voxel write per iteration)
@@ -265,6 +274,11 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
                     bh[c][jj] = 0.f;
                     continue;
                 }
+                if (MODE == X_SS || MODE == X_SSN) {  // the staged field is w_hat - b_hat; u = v
+                    wh[c][jj] = w[c][jj];
+                    bh[c][jj] = 0.f;
+                    continue;
+                }
                 const float dd = vp[c][jj] - w[c][jj];
                 fr = fmaf(dd, dd, fr);
                 const float b = bo[c][jj] + dd;  // dual update (admm.cpp:142-153)
@@ -283,11 +297,11 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
             const float bhj[3] = {bh[0][jj], bh[1][jj], bh[2][jj]};
             const float gj[3] = {g[0][jj], g[1][jj], g[2][jj]};
             float vj[3];
-            v_update_voxel_f32<DT>(whj, bhj, gj, dv[jj], thf, ithf, epsf, vj);
+            v_update_voxel_f32<DT, (MODE == X_SS || MODE == X_SSN) && DT == 2>(whj, bhj, gj, dv[jj], thf, ithf, epsf, vj);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 vn[c][jj] = vj[c];
-                fc += fabsf(vj[c] - vp[c][jj]);
+                if (MODE != X_SSN) fc += fabsf(vj[c] - vp[c][jj]);
             }
             if (a.sp.log_objective) {
                 const float rho = fmaf(gj[0], vj[0], fmaf(gj[1], vj[1], gj[2] * vj[2])) + dv[jj];
@@ -296,9 +310,10 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            if (MODE != X_FIRST && accel) stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
-            if (MODE != X_FIRST) stvN<VEC>(BO + (size_t)c * N + gi, bo[c]);  // b_k over b_{k-2}
-            stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
+            constexpr bool SS = MODE == X_SS || MODE == X_SSN;
+            if (MODE != X_FIRST && !SS && accel) stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
+            if (MODE != X_FIRST && !SS) stvN<VEC>(BO + (size_t)c * N + gi, bo[c]);  // b_k over b_{k-2}
+            if (MODE != X_SSN || a.ss_last) stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
             st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);
         }
     }
@@ -547,7 +562,7 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
     const int pair = blockIdx.y;
     PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;
-    if (MODE <= X_GENERAL && st->solve_done) return;
+    if ((MODE <= X_GENERAL || MODE == X_SS || MODE == X_SSN) && st->solve_done) return;
 
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool F64 = sizeof(C) == 16;
@@ -581,6 +596,10 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
     pointwise_any<MODE, DT, R2, VEC, UNR>(a, buf, pair, L0, nl, tid, fc, fr, fo);
     if (MODE != X_TAIL)
         r2c_tile<R2>(buf, twx, xtw, spectrum_of<C>(a.F, pair), lines, L0, nl, tid, sync);
+    if (MODE == X_SSN) {  // no norms: only the iteration count
+        if (blockIdx.x == 0 && tid == 0) st->iterations = a.k + 1;
+        return;
+    }
     finish_tile<MODE>(a, pair, blockIdx.x, gridDim.x, fc, fr, fo, red, &s_last, tid, sync);
 }
 
@@ -614,9 +633,8 @@ __device__ __forceinline__ void ring_bar(int b) {
 #undef DREG_RB
 }
 
-template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0>
+template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL>
 __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
-    constexpr int MODE = X_GENERAL;
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     constexpr int BUF = 3 * TL * PM;
     constexpr int NF = 32 * FW, NTP = 32 * NPW, NALL = NF + NTP;
@@ -734,6 +752,10 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
                 pointwise_any<MODE, DT, R2, VEC, UNR, float2, NTP, HINT>(a, ring + b * BUF, pair, L0, nl, tid, fc,
                                                                          fr, fo);
             ring_bar<kBarU, NALL, true>(b);
+            if (MODE == X_SSN) {  // no norms to reduce: only the iteration count is kept
+                if (tile == 0 && tid == 0) a.F.st[pair].iterations = a.k + 1;
+                continue;
+            }
             if (run_start < 0) run_start = tile;
             acc[0] += (double)fc;
             acc[1] += (double)fr;
@@ -838,12 +860,12 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0>
+template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL>
 static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
     constexpr int L = kR1 * R2, NB = 3;
     const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 64 +
                         sizeof(int) * (size_t)npairs;
-    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT>;
+    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT, MODE>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
@@ -867,6 +889,38 @@ static cudaError_t launch_pipe_r(const XArgs& a, int npairs, cudaStream_t s) {
     }
 }
 
+template <int MODE, int R2, int VEC, int UNR, int MINB>
+static cudaError_t launch_fast_ss(const XArgs& a, int npairs, cudaStream_t s) {
+    const dim3 grid((unsigned)((a.F.lines + kFTL - 1) / kFTL), (unsigned)npairs);
+    const size_t smem = fast_smem<R2>();
+    void (*k)(XArgs) = xpass_fast_kernel<MODE, 2, R2, VEC, UNR, float2, MINB>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kFT, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+// spectral-state x-pass (l2 only): the point-wise group streams 40 B/voxel instead of 100,
+// so the warp split is tuned separately (DREG_PIPE_SS: FFT warps * 10000 + point-wise
+// warps * 100 + VEC * 10 + unroll)
+template <int R2, int MODE>
+static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
+    switch (a.pipe_ss) {
+        case 3: return launch_fast_ss<MODE, R2, 2, 2, 3>(a, npairs, s);  // one tile per CTA, 3 CTAs per SM
+        case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);
+        case 120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE>(a, npairs, s);
+        case 120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE>(a, npairs, s);
+        case 120642: return launch_pipe_t<2, R2, 6, 4, 2, 12, 0, MODE>(a, npairs, s);
+        case 160442: return launch_pipe_t<2, R2, 4, 4, 2, 16, 0, MODE>(a, npairs, s);
+        case 120444: return launch_pipe_t<2, R2, 4, 4, 4, 12, 0, MODE>(a, npairs, s);
+        // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each;
+        // 4 point-wise warps with two iterations of loads in flight keep up with 16 B/voxel
+        default: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);  // 120442
+    }
+}
+
 template <int MODE, int DT>
 static cudaError_t launch_fast_r(const XArgs& a, int npairs, cudaStream_t s) {
     switch (a.F.M) {
@@ -876,8 +930,17 @@ static cudaError_t launch_fast_r(const XArgs& a, int npairs, cudaStream_t s) {
     }
 }
 
+bool xpass_ss_eligible(const XArgs& a) {
+    return xpass_fast_eligible(a) && a.pipe && !a.precise && a.sp.data_term == 2 && (a.F.M == 64 || a.F.M == 128);
+}
+
 cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t s) {
     const bool l1 = a.sp.data_term == 1;
+    if (mode == X_SS || mode == X_SSN) {
+        if (!xpass_ss_eligible(a)) return cudaErrorInvalidConfiguration;
+        if (a.F.M == 128) return mode == X_SS ? launch_pipe_ss<8, X_SS>(a, npairs, s) : launch_pipe_ss<8, X_SSN>(a, npairs, s);
+        return mode == X_SS ? launch_pipe_ss<4, X_SS>(a, npairs, s) : launch_pipe_ss<4, X_SSN>(a, npairs, s);
+    }
     if (mode == X_GENERAL && a.pipe && !a.precise && a.F.M == 128)
         return l1 ? launch_pipe_r<1, 8>(a, npairs, s) : launch_pipe_r<2, 8>(a, npairs, s);
     if (mode == X_GENERAL && a.pipe && !a.precise && a.F.M == 64)

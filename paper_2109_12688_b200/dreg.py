@@ -455,13 +455,13 @@ class Context:
     def time_kernels(self, reps: int = 20, solver: SolverCfg | None = None) -> dict:
         """CUDA-event timing of the per-iteration kernels on the current workspace
         (with `solver`'s parameters and precision policy when given)."""
-        out = np.zeros(6, np.float64)
+        out = np.zeros(7, np.float64)
         if solver is None:
             self._check(self.lib.dreg_cuda_time_kernels(self.h, reps, out.ctypes.data_as(_D)))
         else:
             self._check(self.lib.dreg_cuda_time_iteration(self.h, C.byref(solver), reps, out.ctypes.data_as(_D)))
         return {"xpass_ms": out[0], "plane_ms": out[1], "xpass_bytes": out[2], "plane_bytes": out[3],
-                "pairs": int(out[4]), "precise": int(out[5])}
+                "pairs": int(out[4]), "precise": int(out[5]), "spectral_state": int(out[6])}
 
     # ---- building blocks ---------------------------------------------------------
     def v_update(self, target, warped, grad, w_hat, b_hat, cfg: SolverCfg) -> np.ndarray:

@@ -645,8 +645,77 @@ def test_pipelined_xpass_bit_identical_to_one_tile_kernel(shape):
             "print(h.hexdigest(), [r.velocity_count for r in res])\n") % (root, shape)
     outs = []
     for pipe in ("0", "1"):
-        env = dict(os.environ, DREG_PIPE=pipe)
+        env = dict(os.environ, DREG_PIPE=pipe, DREG_SS="0")  # the real-space-state iteration
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1], outs
+
+
+# ---- spectral-state iteration (plane_fast.cuh MODE 2 + X_SS / X_SSN) -------------------
+_SS_CODE = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+            "from paper_2109_12688_b200 import dreg, synth\n"
+            "F, M = synth.make_batch(3, 1000, 3, %r)\n"
+            "cfg = synth.config_cfg('config3')\n"
+            "cfg.max_warps_per_level[0] = 3\n"
+            "with dreg.Context(0) as ctx:\n"
+            "    phis, _, res = ctx.register_batch(list(F), list(M), cfg, want_warped=False)\n"
+            "h = hashlib.sha256(b''.join(np.ascontiguousarray(p).tobytes() for p in phis))\n"
+            "print(h.hexdigest(), [r.velocity_count for r in res])\n")
+
+
+def _digest_under(env_extra, shape=(64, 128, 128)):
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", _SS_CODE % (root, shape)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout.strip().splitlines()[-1]
+
+
+def test_spectral_state_variants_bit_identical():
+    """The spectral-state x-pass gives the same bits with and without the change norm
+    (X_SS reads / writes v every iteration, X_SSN only writes the last one), pipelined or
+    one tile per CTA or another warp split: the variants only move data differently."""
+    base = _digest_under({})
+    assert _digest_under({"DREG_SS_CHG": "1"}) == base
+    assert _digest_under({"DREG_PIPE_SS": "3"}) == base
+    assert _digest_under({"DREG_PIPE_SS": "80841"}) == base
+
+
+@pytest.mark.parametrize("shape", [(64, 128, 128), (64, 64, 64)])
+def test_spectral_state_matches_real_space_state(shape):
+    """Same accelerated-ADMM recurrence (admm.cpp:275-308) carried as Fourier-domain iterates:
+    against the real-space-state kernels (DREG_SS=0) the registrations agree far inside the
+    parity contract (both are fp32 evaluations of the reference's fp64 arithmetic)."""
+    F, M = synth.make_batch(3, 1000, 2, shape)
+    cfg = synth.config_cfg("config3")
+    cfg.max_warps_per_level[0] = 3
+    out = {}
+    for ss in ("1", "0"):
+        os.environ["DREG_SS"] = ss
+        try:
+            with dreg.Context(0) as c2:
+                phis, _, res = c2.register_batch(list(F), list(M), cfg, want_warped=False)
+        finally:
+            os.environ.pop("DREG_SS", None)
+        out[ss] = (phis, [r.velocity_count for r in res])
+    assert out["1"][1] == out["0"][1]
+    for a, b in zip(out["1"][0], out["0"][0]):
+        print(f"spectral vs real-space state: phi max-abs {max_abs(a, b):.3e} rel-L2 {rel_l2(a, b):.3e}")
+        assert max_abs(a, b) <= 2e-4 and rel_l2(a, b) <= 5e-5
+
+
+@pytest.mark.parametrize("tol", [0.0, 5e-5])
+def test_register_spectral_state_grid(ctx, oracle, tol):
+    """64^3 (a grid the spectral-state kernels cover) against the oracle, without a tolerance
+    (X_SSN: v only written by the last iteration) and with one (X_SS: change norm, per-pair
+    early exit at the oracle's iteration counts)."""
+    f, m = synth.make_pair(2, 5, (64, 64, 64))
+    s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=50, tol=tol, log_objective=False)
+    phi, res = _reg_parity(ctx, oracle, f, m, abi.reg_cfg(s, 1, (4,), (50,)))
+    if tol > 0:  # the tolerance stops the last solve inside the spectral-state loop (oracle: [50, 50, 50, 2])
+        assert any(1 < it < 50 for it in abi.level_logs(res)[0]["solver_iterations"][: res.solves])
