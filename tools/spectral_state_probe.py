@@ -115,3 +115,28 @@ vb = spectral_state()
 report("spectral fp32", vb)
 e = va.astype(np.float64) - vb
 print(f"between the two  max-abs {np.abs(e).max():.3e}")
+
+
+def spectral_state_mixed():
+    """fp32 transforms and v-update, fp64 state recurrence (U, Ut) -- what a mixed mode would do."""
+    hx = shape[2] // 2 + 1
+    C128 = np.complex128
+    one_m64 = lam * K / (lam * K + theta)
+    two_m164 = (theta - lam * K) / (lam * K + theta)
+    Z = [np.zeros((shape[0], shape[1], hx), C64) for _ in range(3)]
+    U1 = [np.zeros((shape[0], shape[1], hx), C128) for _ in range(3)]
+    U0 = [z.copy() for z in U1]
+    Ut = [z.copy() for z in U1]
+    for k in range(iters):
+        z = [inv(Z[i]) for i in range(3)]
+        v = prox(z)
+        for i in range(3):
+            Un = fwd(v[i]).astype(C128) + one_m64 * Ut[i]
+            U0[i], U1[i] = U1[i], Un
+            Ut[i] = U1[i] + c[k] * (U1[i] - U0[i])
+            Z[i] = (two_m164 * Ut[i]).astype(C64)
+    return np.stack(v, -1)
+
+
+if len(sys.argv) > 6:
+    report("fp64 state mix", spectral_state_mixed())
