@@ -300,7 +300,7 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), MINB) plane_reg_kernel(
     const int c = blockIdx.x / hx, p = blockIdx.x - c * hx;
     float2* Sp = a.F.S + ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)a.F.lines;
     const int y1 = tid % R2Y, z1 = tid / R2Y;
-    if (MODE == 2 && tid == 0) {
+    if (MODE == 2 && tid == 0 && a.ss_prefetch) {
         // this plane's state iterates are needed after the forward transforms: bring them to L2 now
         const size_t pl = ((size_t)pair * 3 * hx + (size_t)c * hx + p) * (size_t)(NY * NZ);
         if (a.has1)

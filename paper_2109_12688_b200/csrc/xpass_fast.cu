@@ -125,16 +125,19 @@ __device__ __forceinline__ void stage_spectrum(C* buf, const C* S, long long lin
     constexpr int STEP = NF / TL;
     const int l = tid & (TL - 1);
     const bool ok = l < nl;
-    int cp = tid >> 5;  // c * HX + p
-    const C* src = S + (size_t)cp * lines + L0 + (ok ? l : 0);
-    C* dst = buf + l * PM + cp;
+    const int w = tid >> 5;  // first x-bin of this thread; it then walks p = w, w + STEP, ...
     const size_t sstep = (size_t)STEP * lines;
-#pragma unroll 4
-    for (; cp < 3 * HX; cp += STEP, src += sstep, dst += STEP) {
-        // row (c, p) of line l lives at (c * TL + l) * PM + p = l * PM + cp + c * (TL * PM - HX)
-        C* d = dst + (cp >= 2 * HX ? 2 * (TL * PM - HX) : (cp >= HX ? TL * PM - HX : 0));
-        if constexpr (sizeof(C) == 16) *d = ok ? *src : CT<C>::make(0, 0);  // fp64 storage
-        else cp_async8(d, src, ok);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const C* src = S + ((size_t)c * HX + w) * lines + L0 + (ok ? l : 0);
+        C* dst = buf + (c * TL + l) * PM + w;
+#pragma unroll
+        for (int i = 0; i < (HX + STEP - 1) / STEP; ++i, src += sstep, dst += STEP) {
+            if (w + i * STEP < HX) {
+                if constexpr (sizeof(C) == 16) *dst = ok ? *src : CT<C>::make(0, 0);  // fp64 storage
+                else cp_async8(dst, src, ok);
+            }
+        }
     }
 }
 
@@ -633,12 +636,14 @@ __device__ __forceinline__ void ring_bar(int b) {
 #undef DREG_RB
 }
 
-template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL>
-__global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
+// NB = 2 (two tile buffers, MINB = 2 CTAs per SM): the next tile is staged only after the
+// previous one is transformed back, and the co-resident CTA covers that latency.
+template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL, int MINB = 1>
+__global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     constexpr int BUF = 3 * TL * PM;
     constexpr int NF = 32 * FW, NTP = 32 * NPW, NALL = NF + NTP;
-    static_assert(NB == 3, "ring of three tile buffers");
+    static_assert(NB == 3 || NB == 2, "ring of three (or two) tile buffers");
     extern __shared__ __align__(16) unsigned char smem[];
     float2* ring = reinterpret_cast<float2*>(smem);  // [NB][3][TL][PM]
     float2* twx = ring + NB * BUF;
@@ -718,7 +723,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
             if (tid == 0) tile_of[b] = cur;
             ring_bar<kBarW, NALL, true>(b);
             // prefetch tile i+1 into buffer (i+1) % NB: it held tile i-2, transformed back last round
-            if (next >= 0) stage(next, ring + ((i + 1) % NB) * BUF);
+            if (NB == 3 && next >= 0) stage(next, ring + ((i + 1) % NB) * BUF);
             if (prev >= 0) {
                 const int pb = (i + NB - 1) % NB;
                 ring_bar<kBarU, NALL, false>(pb);
@@ -730,6 +735,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), 1) xpass_pipe_kernel(XArgs a,
                                  tid, sync);
                 sync();  // buffer pb is restaged next round by this group
             }
+            if (NB == 2 && next >= 0) stage(next, ring + ((i + 1) % NB) * BUF);  // the buffer just transformed back
             if (cur < 0) break;
             prev = cur;
             cur = next;
@@ -860,12 +866,12 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL>
+template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL, int NB = 3, int MINB = 1>
 static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
-    constexpr int L = kR1 * R2, NB = 3;
+    constexpr int L = kR1 * R2;
     const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 64 +
                         sizeof(int) * (size_t)npairs;
-    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT, MODE>;
+    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT, MODE, MINB>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
@@ -875,7 +881,7 @@ static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
     // DREG_XPASS_SMS (experiment knob): persistent CTAs, i.e. SMs the x-pass occupies
     const char* lim = std::getenv("DREG_XPASS_SMS");
     if (lim && std::atoi(lim) > 0) sms = std::min(sms, std::atoi(lim));
-    const int grid = std::min(tiles * npairs, sms);
+    const int grid = std::min(tiles * npairs, sms * MINB);
     k<<<grid, 32 * (FW + NPW), smem, s>>>(a, tiles, npairs);
     return cudaGetLastError();
 }
@@ -910,6 +916,11 @@ static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
     switch (a.pipe_ss) {
         case 3: return launch_fast_ss<MODE, R2, 2, 2, 3>(a, npairs, s);  // one tile per CTA, 3 CTAs per SM
         case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);
+        // two CTAs per SM, two tile buffers each
+        case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);
+        case 2060244: return launch_pipe_t<2, R2, 2, 4, 4, 6, 0, MODE, 2, 2>(a, npairs, s);
+        case 2060442: return launch_pipe_t<2, R2, 4, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);
+        case 2040442: return launch_pipe_t<2, R2, 4, 4, 2, 4, 0, MODE, 2, 2>(a, npairs, s);
         case 120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE>(a, npairs, s);
         case 120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE>(a, npairs, s);
         case 120642: return launch_pipe_t<2, R2, 6, 4, 2, 12, 0, MODE>(a, npairs, s);
