@@ -317,7 +317,11 @@ __device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair,
             if (MODE != X_FIRST && !SS && accel) stvN<VEC>(WP + (size_t)c * N + gi, w[c]);
             if (MODE != X_FIRST && !SS) stvN<VEC>(BO + (size_t)c * N + gi, bo[c]);  // b_k over b_{k-2}
             if (MODE != X_SSN || a.ss_last) stvN<VEC>(V + (size_t)c * N + gi, vn[c]);
-            st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);
+            if constexpr (SS && sizeof(C) == 8 && VEC >= 2) {  // u = v: no b_hat to add
+#pragma unroll
+                for (int q = 0; q < VEC; q += 2) (buf + (c * TL + l) * PM)[(x0 + q) >> 1] = make_float2(vn[c][q], vn[c][q + 1]);
+            } else
+                st_reals_sum<VEC>(buf + (c * TL + l) * PM, x0, vn[c], bh[c]);
         }
     }
 }
@@ -621,6 +625,7 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
 // fixed tree) and the pair's ticket counts tiles, so the per-pair totals are
 // deterministic for a given SM count.
 constexpr int kBarFFT = 1, kBarPW = 2, kBarW = 3, kBarU = 6;  // W/U use NB ids each (NB <= 3)
+constexpr int kBarFFTB = 9, kBarF = 10;  // split FFT groups: the r2c group's barrier and FREE(b)
 
 // named barrier base + b with a compile-time id (a run-time id makes ptxas reserve all 16)
 template <int BASE, int N, bool ARRIVE>
@@ -638,7 +643,12 @@ __device__ __forceinline__ void ring_bar(int b) {
 
 // NB = 2 (two tile buffers, MINB = 2 CTAs per SM): the next tile is staged only after the
 // previous one is transformed back, and the co-resident CTA covers that latency.
-template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL, int MINB = 1>
+// SPLIT: the FFT warps form two groups, one staging + inverse-transforming tile i + 1 while the
+// other forward-transforms tile i - 1 (and the point-wise group updates tile i), so the three
+// stages of the ring run concurrently instead of the FFT group alternating between two of them;
+// FREE(b) (r2c group arrives, c2r group waits) returns a buffer for restaging.
+template <int DT, int R2, int NB, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL, int MINB = 1,
+          bool SPLIT = false>
 __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs a, int tiles_per_pair, int npairs) {
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     constexpr int BUF = 3 * TL * PM;
@@ -704,7 +714,61 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    if (fft_group) {
+    if (SPLIT && fft_group) {
+        static_assert(!SPLIT || (NB == 3 && FW % 2 == 0), "split FFT groups: ring of three, even warp count");
+        constexpr int NA = NF / 2;  // threads per FFT sub-group
+        // W: c2r group arrives, point-wise waits; U: point-wise arrives, r2c group waits
+        if (tid < NA) {
+            const NamedSync<kBarFFT, NA> sync{};
+            for (int i = tid; i < L; i += NA) twx[i] = a.twx[i];
+            for (int i = tid; i <= HX; i += NA) xtw[i] = a.xtw[i];
+            auto stage_a = [&](int g, float2* buf) {
+                const int pair = plist[g / T], tile = g - (g / T) * T;
+                const long long L0 = (long long)tile * TL;
+                const int nl = (int)min((long long)TL, lines - L0);
+                stage_spectrum<R2, float2, NA>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            };
+            int cur = runnable_from(range_start(blockIdx.x));
+            if (cur >= 0) stage_a(cur, ring);
+            for (int i = 0;; ++i) {
+                const int b = i % NB;
+                const int next = cur >= 0 ? runnable_from(cur + 1) : -1;
+                if (cur >= 0) {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    sync();
+                    c2r_tile<R2, float2, NamedSync<kBarFFT, NA>, NA>(ring + b * BUF, twx, xtw, tid, sync);
+                }
+                if (tid == 0) tile_of[b] = cur;
+                ring_bar<kBarW, NA + NTP, true>(b);
+                if (cur < 0) break;
+                // slot i + 1 (the next tile, or the end marker) reuses the buffer, tile_of[] entry and
+                // W barrier of tile i - 2: wait until the r2c group (hence the point-wise group) is done with it
+                const int nb = (i + 1) % NB;
+                if (i + 1 >= NB) ring_bar<kBarF, NF, false>(nb);
+                if (next >= 0) stage_a(next, ring + nb * BUF);
+                cur = next;
+            }
+        } else {
+            const int tb = tid - NA;
+            const NamedSync<kBarFFTB, NA> sync{};
+            int n_tiles = 0;
+            for (int g = runnable_from(range_start(blockIdx.x)); g >= 0; g = runnable_from(g + 1)) ++n_tiles;
+            // this group trails the point-wise group, whose tickets may raise solve_done for a
+            // pair it has finished: the tile ids come from tile_of[], not from the pair flags
+            for (int i = 0; i < n_tiles; ++i) {
+                const int b = i % NB;
+                ring_bar<kBarU, NA + NTP, false>(b);
+                const int cur = tile_of[b];
+                const int pair = plist[cur / T], tile = cur - (cur / T) * T;
+                const long long L0 = (long long)tile * TL;
+                const int nl = (int)min((long long)TL, lines - L0);
+                r2c_tile<R2, float2, NamedSync<kBarFFTB, NA>, NA>(ring + b * BUF, twx, xtw,
+                                                                  a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tb, sync);
+                if (i + NB <= n_tiles) ring_bar<kBarF, NF, true>(b);  // slot i + NB (a tile or the end marker) reuses b
+            }
+        }
+    } else if (fft_group) {
         const NamedSync<kBarFFT, NF> sync{};
         for (int i = tid; i < L; i += NF) twx[i] = a.twx[i];
         for (int i = tid; i <= HX; i += NF) xtw[i] = a.xtw[i];
@@ -747,7 +811,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
         int run_start = -1;
         for (int i = 0;; ++i) {
             const int b = i % NB;
-            ring_bar<kBarW, NALL, false>(b);
+            ring_bar<kBarW, SPLIT ? NF / 2 + NTP : NALL, false>(b);
             const int cur = tile_of[b];
             if (cur < 0) break;
             const int slot = cur / T, pair = plist[slot], tile = cur - slot * T;
@@ -757,7 +821,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
             if (!DREG_SKIP(a, 2))
                 pointwise_any<MODE, DT, R2, VEC, UNR, float2, NTP, HINT>(a, ring + b * BUF, pair, L0, nl, tid, fc,
                                                                          fr, fo);
-            ring_bar<kBarU, NALL, true>(b);
+            ring_bar<kBarU, SPLIT ? NF / 2 + NTP : NALL, true>(b);
             if (MODE == X_SSN) {  // no norms to reduce: only the iteration count is kept
                 if (tile == 0 && tid == 0) a.F.st[pair].iterations = a.k + 1;
                 continue;
@@ -866,12 +930,13 @@ static cudaError_t launch_fast_x(const XArgs& a, int npairs, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL, int NB = 3, int MINB = 1>
+template <int DT, int R2, int NPW, int VEC, int UNR, int FW = 8, int HINT = 0, int MODE = X_GENERAL, int NB = 3, int MINB = 1,
+          bool SPLIT = false>
 static cudaError_t launch_pipe_t(const XArgs& a, int npairs, cudaStream_t s) {
     constexpr int L = kR1 * R2;
     const size_t smem = sizeof(float2) * ((size_t)NB * 3 * kFTL * (L + 1) + L + L + 2) + sizeof(double) * 64 +
                         sizeof(int) * (size_t)npairs;
-    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT, MODE, MINB>;
+    void (*k)(XArgs, int, int) = xpass_pipe_kernel<DT, R2, NB, NPW, VEC, UNR, FW, HINT, MODE, MINB, SPLIT>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0;
@@ -916,19 +981,22 @@ static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
     switch (a.pipe_ss) {
         case 3: return launch_fast_ss<MODE, R2, 2, 2, 3>(a, npairs, s);  // one tile per CTA, 3 CTAs per SM
         case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);
+        // split FFT groups (c2r group / r2c group)
+        case 1120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE, 3, 1, true>(a, npairs, s);
+        case 1120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE, 3, 1, true>(a, npairs, s);
+        case 1121241: return launch_pipe_t<2, R2, 12, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
+        case 1120641: return launch_pipe_t<2, R2, 6, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
+        case 1160841: return launch_pipe_t<2, R2, 8, 4, 1, 16, 0, MODE, 3, 1, true>(a, npairs, s);
+        case 120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);
         // two CTAs per SM, two tile buffers each
         case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);
-        case 2060244: return launch_pipe_t<2, R2, 2, 4, 4, 6, 0, MODE, 2, 2>(a, npairs, s);
-        case 2060442: return launch_pipe_t<2, R2, 4, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);
         case 2040442: return launch_pipe_t<2, R2, 4, 4, 2, 4, 0, MODE, 2, 2>(a, npairs, s);
         case 120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE>(a, npairs, s);
         case 120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE>(a, npairs, s);
-        case 120642: return launch_pipe_t<2, R2, 6, 4, 2, 12, 0, MODE>(a, npairs, s);
-        case 160442: return launch_pipe_t<2, R2, 4, 4, 2, 16, 0, MODE>(a, npairs, s);
-        case 120444: return launch_pipe_t<2, R2, 4, 4, 4, 12, 0, MODE>(a, npairs, s);
         // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each;
         // 4 point-wise warps with two iterations of loads in flight keep up with 16 B/voxel
-        default: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);  // 120442
+        // split groups: 6 c2r + 6 r2c warps, 8 point-wise warps (1120841)
+        default: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
     }
 }
 
