@@ -735,6 +735,7 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     p.pf_ahead = env_int("DREG_PLANE_PF", 1);
     p.ss_variant = env_int("DREG_PLANE_SS", 0);
     p.ss_prefetch = env_int("DREG_PLANE_UPF", 1);
+    p.ss_stream = env_int("DREG_PLANE_STREAM", 1);
     p.order = sp.order;
     p.PY = w.geo.PY;
     p.energy_out = w.energy.p;

@@ -91,6 +91,7 @@ struct PArgs {
     float c_cur, c_prev;         // Nesterov coefficients c_{j-1}, c_{j-2}
     float inv_nf;                // 1 / voxels
     int ss_variant;              // DREG_PLANE_SS experiment knob
+    int ss_stream;               // MODE 2: streaming (evict-first) loads / stores of the plane itself (DREG_PLANE_STREAM)
     int ss_prefetch;             // L2-prefetch the plane's state iterates at CTA start (DREG_PLANE_UPF)
     int has1, has0;              // U_{j-1} exists (j >= 2); U_{j-2} enters (c_{j-2} != 0)
     int order;

@@ -314,7 +314,11 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), MINB) plane_reg_kernel(
 #pragma unroll
     for (int u = 0; u < R1Z; ++u)
 #pragma unroll
-        for (int t = 0; t < 8; ++t) x[u][t] = __ldg(Sp + (z1 + R2Z * u) * NY + y1 + R2Y * t);
+        for (int t = 0; t < 8; ++t) {
+            const float2* src = Sp + (z1 + R2Z * u) * NY + y1 + R2Y * t;
+            // MODE 2 streams five half-spectra through L2: every line is touched once (evict first)
+            x[u][t] = (MODE == 2 && a.ss_stream) ? __ldcs(src) : __ldg(src);
+        }
     // position tables doubled (exact) for the multiplier base 2 (sx + sy + sz)
     const float dbl = MODE != 1 ? 2.0f : 1.0f;
     for (int i = tid; i < NY; i += NT) {
@@ -490,7 +494,11 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), MINB) plane_reg_kernel(
     for (int u = 0; u < R1Z; ++u) {
         dft8<true>(x[u]);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) Sp[(z1 + R2Z * u) * NY + y1 + R2Y * t] = x[u][t];
+        for (int t = 0; t < 8; ++t) {
+            float2* dst = Sp + (z1 + R2Z * u) * NY + y1 + R2Y * t;
+            if (MODE == 2 && a.ss_stream) __stcs(dst, x[u][t]);
+            else *dst = x[u][t];
+        }
     }
 }
 

@@ -42,7 +42,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // HINT 1: streaming loads, no L1 allocation, 256-byte L2 prefetch granule
 template <int N, int HINT = 0>
 __device__ __forceinline__ void ldvN(const float* p, float* out) {
-    if constexpr (N == 4 && HINT == 1) {
+    if constexpr (N == 4 && HINT == 2) {  // HINT 2: evict-first streaming load (ld.global.cs)
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+        out[0] = t.x;
+        out[1] = t.y;
+        out[2] = t.z;
+        out[3] = t.w;
+    } else if constexpr (N == 4 && HINT == 1) {
         asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(out[0]), "=f"(out[1]), "=f"(out[2]), "=f"(out[3])
                      : "l"(p));
@@ -460,7 +466,7 @@ template <int DT, class C = float2>
 using AccT = typename std::conditional<DT == 1 || sizeof(C) == 16, double, float>::type;
 
 // phase 3: r2c of u (real, natural order in buf) -> spectrum rows in global.
-template <int R2, class C, class Sync, int NF = kFT>
+template <int R2, class C, class Sync, int NF = kFT, bool STREAM = false>
 __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, C* S, long long lines,
                                          long long L0, int nl, int tid, Sync sync) {
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
@@ -507,7 +513,9 @@ __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, C* 
             const C zc = cconj(zpartner);
             const C ee = CT<C>::make((zk.x + zc.x) * 0.5f, (zk.y + zc.y) * 0.5f);
             const C oo = CT<C>::make((zk.y - zc.y) * 0.5f, -(zk.x - zc.x) * 0.5f);
-            Sc[(size_t)k * lines] = cadd(ee, cmul(xtw[k], oo));
+            const C out = cadd(ee, cmul(xtw[k], oo));
+            if constexpr (STREAM && sizeof(C) == 8) __stcs(Sc + (size_t)k * lines, out);  // read once, by the plane pass
+            else Sc[(size_t)k * lines] = out;
         };
 #pragma unroll
         for (int p1 = 0; p1 < R2; ++p1) {
@@ -763,7 +771,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
                 const int pair = plist[cur / T], tile = cur - (cur / T) * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
-                r2c_tile<R2, float2, NamedSync<kBarFFTB, NA>, NA>(ring + b * BUF, twx, xtw,
+                r2c_tile<R2, float2, NamedSync<kBarFFTB, NA>, NA, HINT == 2>(ring + b * BUF, twx, xtw,
                                                                   a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tb, sync);
                 if (i + NB <= n_tiles) ring_bar<kBarF, NF, true>(b);  // slot i + NB (a tile or the end marker) reuses b
             }
@@ -983,10 +991,8 @@ static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
         case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);
         // split FFT groups (c2r group / r2c group)
         case 1120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE, 3, 1, true>(a, npairs, s);
+        case 1120861: return launch_pipe_t<2, R2, 8, 4, 1, 12, 2, MODE, 3, 1, true>(a, npairs, s);  // streaming hints
         case 1120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE, 3, 1, true>(a, npairs, s);
-        case 1121241: return launch_pipe_t<2, R2, 12, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
-        case 1120641: return launch_pipe_t<2, R2, 6, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
-        case 1160841: return launch_pipe_t<2, R2, 8, 4, 1, 16, 0, MODE, 3, 1, true>(a, npairs, s);
         case 120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);
         // two CTAs per SM, two tile buffers each
         case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);
