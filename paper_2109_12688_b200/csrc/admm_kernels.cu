@@ -762,7 +762,10 @@ cudaError_t launch_plane(const PArgs& a, int mode, int npairs, cudaStream_t s) {
         DREG_FAST_CASES(X)
 #undef X
     }
-    if (plane_split_needed(a)) return launch_plane_split(a, mode, npairs, s);
+    if (plane_split_needed(a)) {
+        if (mode == 0 && plane_cluster_eligible(a)) return launch_plane_cluster(a, npairs, s);  // one pass over DSMEM
+        return launch_plane_split(a, mode, npairs, s);
+    }
     const dim3 grid((unsigned)(3 * a.F.hx), (unsigned)npairs);
     const size_t smem = plane_smem_bytes(a.F.Ny, a.F.Nz, a.PY);
     void (*k)(PArgs) = mode == 0 ? plane_kernel<0> : plane_kernel<1>;

@@ -697,6 +697,7 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.pipe = env_int("DREG_PIPE", 1);
     a.pipe_all = env_int("DREG_PIPE_ALL", 0);
     a.pipe_ss = env_int("DREG_PIPE_SS", 1120841);
+    a.pipe256 = env_int("DREG_PIPE256", 1);
     if (precise) a.TL = w.geo.TLp;
     a.fd_lines.init((unsigned)(3 * a.TL));
     return a;
@@ -734,6 +735,7 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     // an L2 prefetch of the x-pass state instead thrashed L2: +38%)
     p.pf_ahead = env_int("DREG_PLANE_PF", 1);
     p.ss_variant = env_int("DREG_PLANE_SS", 0);
+    p.cluster = env_int("DREG_CLUSTER", 0);  // opt-in: correct, but slower than the 3-pass split so far
     p.ss_prefetch = env_int("DREG_PLANE_UPF", 1);
     p.ss_stream = env_int("DREG_PLANE_STREAM", 1);
     p.order = sp.order;

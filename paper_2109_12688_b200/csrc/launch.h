@@ -52,6 +52,7 @@ struct XArgs {
 #endif
     FastDiv fd_lines;   // divide by 3 * TL
     int pipe;           // warp-specialised persistent x-pass for X_GENERAL, M in {64, 128} (DREG_PIPE: 0 off; default on)
+    int pipe256;        // pipelined x-pass at M = 256 (two-buffer ring; DREG_PIPE256)
     int pipe_ss;        // warp split of the spectral-state x-pass (DREG_PIPE_SS)
     int ss_last;        // X_SSN: this is the solve's last iteration (v is written)
     int pipe_all;       // A/B knob (DREG_PIPE_ALL): split all pairs' tiles statically, not just the iterating ones
@@ -91,6 +92,7 @@ struct PArgs {
     float c_cur, c_prev;         // Nesterov coefficients c_{j-1}, c_{j-2}
     float inv_nf;                // 1 / voxels
     int ss_variant;              // DREG_PLANE_SS experiment knob
+    int cluster;                 // 2-CTA cluster plane kernel for planes over one CTA's shared memory (DREG_CLUSTER)
     int ss_stream;               // MODE 2: streaming (evict-first) loads / stores of the plane itself (DREG_PLANE_STREAM)
     int ss_prefetch;             // L2-prefetch the plane's state iterates at CTA start (DREG_PLANE_UPF)
     int has1, has0;              // U_{j-1} exists (j >= 2); U_{j-2} enters (c_{j-2} != 0)
@@ -112,6 +114,8 @@ bool plane_fast_supported(int Ny, int Nz);
 bool plane_reg_supported(int Ny, int Nz);
 // three-pass plane for planes above one CTA's shared memory (plane_split.cu)
 bool plane_split_needed(const PArgs& a);
+bool plane_cluster_eligible(const PArgs& a);
+cudaError_t launch_plane_cluster(const PArgs& a, int npairs, cudaStream_t s);
 cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);
 bool xpass_fast_eligible(const XArgs& a);

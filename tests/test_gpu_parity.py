@@ -652,6 +652,37 @@ def test_pipelined_xpass_bit_identical_to_one_tile_kernel(shape):
     assert outs[0] == outs[1], outs
 
 
+def test_cluster_plane_kernel_matches_split_path():
+    """The opt-in 2-CTA cluster / DSMEM plane kernel (plane_cluster.cu, DREG_CLUSTER=1) computes the
+    same w-update as the 3-pass split on the config-5 plane (256 x 192) within fp32 rounding."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "from paper_2109_12688_b200 import abi, dreg\n"
+            "rng = np.random.default_rng(7)\n"
+            "v = rng.standard_normal((192, 256, 32, 3)).astype(np.float32)\n"
+            "b = rng.standard_normal((192, 256, 32, 3)).astype(np.float32)\n"
+            "cfg = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=50)\n"
+            "with dreg.Context(0) as ctx:\n"
+            "    w = ctx.w_update(v, b, cfg)\n"
+            "np.save(sys.argv[1], w)\n") % root
+    import tempfile
+
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for flag in ("0", "1"):
+            path = os.path.join(td, f"w{flag}.npy")
+            r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, DREG_CLUSTER=flag),
+                               capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+    scale = float(np.abs(outs[0]).max())
+    print(f"cluster vs split w-update: max-abs {max_abs(outs[1], outs[0]):.3e} (max|w| {scale:.3f})")
+    assert max_abs(outs[1], outs[0]) <= 1e-5 * scale
+
+
 # ---- spectral-state iteration (plane_fast.cuh MODE 2 + X_SS / X_SSN) -------------------
 _SS_CODE = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
             "from paper_2109_12688_b200 import dreg, synth\n"
