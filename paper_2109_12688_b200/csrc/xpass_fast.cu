@@ -163,7 +163,46 @@ __device__ __forceinline__ void c2r_tile(C* buf, const C* twx, const C* xtw, int
         const bool act = line < 3 * TL;
         const C* X = buf + line * PM;
         C z[2][R2];
-        if (act) {
+        if constexpr (sizeof(C) == 8) {
+            // fp32: bins k and L - k need the same two inputs A = X[k], B = X[L-k] and share
+            // s = A + conj(B), d = A - conj(B), o = d conj(W_M^k) (W_M^{L-k} = -conj(W_M^k)):
+            // Z'[k] = (s.x - o.y, s.y + o.x), Z'[L-k] = (s.x + o.y, o.x - s.y) -- half the loads
+            // and half the arithmetic of treating the two bins separately.
+            auto joint = [&](int k, C& zk, C& zp) {
+                const C A = X[k], B = X[L - k], w = xtw[k];
+                const C s = CT<C>::make(A.x + B.x, A.y - B.y), d = CT<C>::make(A.x - B.x, A.y + B.y);
+                const C o = CT<C>::make(fmaf(d.x, w.x, d.y * w.y), fmaf(d.y, w.x, -(d.x * w.y)));
+                zk = CT<C>::make(s.x - o.y, s.y + o.x);
+                zp = CT<C>::make(s.x + o.y, o.x - s.y);
+            };
+            auto single = [&](int k, C& zk) {  // self-paired bins (k = 0 with L, k = L/2)
+                C A = X[k];
+                C B = X[L - k];
+                if (k == 0) {
+                    A.y = 0;
+                    B.y = 0;
+                }
+                B.y = -B.y;
+                const C e = cadd(A, B);
+                const C o = cmulc(csub(A, B), xtw[k]);
+                zk = CT<C>::make(e.x - o.y, e.y + o.x);
+            };
+            if (act) {
+                if (j != 0) {  // blocks j and 8 - j: bin 8 p1 + j pairs with 8 (R2-1-p1) + (8 - j)
+#pragma unroll
+                    for (int p1 = 0; p1 < R2; ++p1) joint(kR1 * p1 + j, z[0][p1], z[1][R2 - 1 - p1]);
+                } else {  // block 0 pairs p1 with R2 - p1 (0 and R2/2 are self-paired); block 4 pairs p1 with R2-1-p1
+                    single(0, z[0][0]);
+                    single(kR1 * (R2 / 2), z[0][R2 / 2]);
+#pragma unroll
+                    for (int p1 = 1; p1 < R2 / 2; ++p1) joint(kR1 * p1, z[0][p1], z[0][R2 - p1]);
+#pragma unroll
+                    for (int p1 = 0; p1 < R2 / 2; ++p1) joint(kR1 * p1 + kR1 / 2, z[1][p1], z[1][R2 - 1 - p1]);
+                }
+                rdft<true, R2>(z[0]);
+                rdft<true, R2>(z[1]);
+            }
+        } else if (act) {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int b = q == 0 ? j : (j == 0 ? kR1 / 2 : kR1 - j);
@@ -509,27 +548,55 @@ __device__ __forceinline__ void r2c_tile(C* buf, const C* twx, const C* xtw, C* 
         rdft<false, R2>(z0);
         rdft<false, R2>(z1);
         C* Sc = S + (size_t)c * HX * lines + L0 + l;
+        auto put = [&](int k, C out) {
+            if constexpr (STREAM && sizeof(C) == 8) __stcs(Sc + (size_t)k * lines, out);  // read once, by the plane pass
+            else Sc[(size_t)k * lines] = out;
+        };
         auto emit = [&](int k, C zk, C zpartner) {
             const C zc = cconj(zpartner);
             const C ee = CT<C>::make((zk.x + zc.x) * 0.5f, (zk.y + zc.y) * 0.5f);
             const C oo = CT<C>::make((zk.y - zc.y) * 0.5f, -(zk.x - zc.x) * 0.5f);
-            const C out = cadd(ee, cmul(xtw[k], oo));
-            if constexpr (STREAM && sizeof(C) == 8) __stcs(Sc + (size_t)k * lines, out);  // read once, by the plane pass
-            else Sc[(size_t)k * lines] = out;
+            put(k, cadd(ee, cmul(xtw[k], oo)));
         };
+        if constexpr (sizeof(C) == 8) {
+            // fp32: X[k] and X[L-k] share s = Z[k] + conj(Z[L-k]), d = Z[k] - conj(Z[L-k]):
+            // X[k] = s/2 + (t1, t2), X[L-k] = (s.x/2 - t1, t2 - s.y/2), (t1, t2) = W_M^k (d.y, -d.x) / 2
+            auto joint = [&](int k, C a_, C b_) {
+                const C w = xtw[k];
+                const C s_ = CT<C>::make(a_.x + b_.x, a_.y - b_.y), d = CT<C>::make(a_.x - b_.x, a_.y + b_.y);
+                const float hx_ = 0.5f * w.x, hy_ = 0.5f * w.y;
+                const float t1 = fmaf(hx_, d.y, hy_ * d.x), t2 = fmaf(hy_, d.y, -(hx_ * d.x));
+                const float sx = 0.5f * s_.x, sy = 0.5f * s_.y;
+                put(k, CT<C>::make(sx + t1, sy + t2));
+                put(L - k, CT<C>::make(sx - t1, t2 - sy));
+            };
+            if (j != 0) {
 #pragma unroll
-        for (int p1 = 0; p1 < R2; ++p1) {
-            if (j == 0) {
-                // block 0: partner of k = 8 p1 is L - k = 8 (R2 - p1) in block 0
-                emit(kR1 * p1, z0[p1], z0[(R2 - p1) & (R2 - 1)]);
-                // block 4 is self-paired: partner index R2 - 1 - p1
-                emit(kR1 * p1 + kR1 / 2, z1[p1], z1[R2 - 1 - p1]);
+                for (int p1 = 0; p1 < R2; ++p1) joint(kR1 * p1 + b0, z0[p1], z1[R2 - 1 - p1]);
             } else {
-                emit(kR1 * p1 + b0, z0[p1], z1[R2 - 1 - p1]);
-                emit(kR1 * p1 + b1, z1[p1], z0[R2 - 1 - p1]);
+                emit(0, z0[0], z0[0]);
+                emit(L, z0[0], z0[0]);  // Nyquist bin k = L (Z[L] = Z[0])
+                emit(kR1 * (R2 / 2), z0[R2 / 2], z0[R2 / 2]);
+#pragma unroll
+                for (int p1 = 1; p1 < R2 / 2; ++p1) joint(kR1 * p1, z0[p1], z0[R2 - p1]);
+#pragma unroll
+                for (int p1 = 0; p1 < R2 / 2; ++p1) joint(kR1 * p1 + kR1 / 2, z1[p1], z1[R2 - 1 - p1]);
             }
+        } else {
+#pragma unroll
+            for (int p1 = 0; p1 < R2; ++p1) {
+                if (j == 0) {
+                    // block 0: partner of k = 8 p1 is L - k = 8 (R2 - p1) in block 0
+                    emit(kR1 * p1, z0[p1], z0[(R2 - p1) & (R2 - 1)]);
+                    // block 4 is self-paired: partner index R2 - 1 - p1
+                    emit(kR1 * p1 + kR1 / 2, z1[p1], z1[R2 - 1 - p1]);
+                } else {
+                    emit(kR1 * p1 + b0, z0[p1], z1[R2 - 1 - p1]);
+                    emit(kR1 * p1 + b1, z1[p1], z0[R2 - 1 - p1]);
+                }
+            }
+            if (j == 0) emit(L, z0[0], z0[0]);  // Nyquist bin k = L (Z[L] = Z[0])
         }
-        if (j == 0) emit(L, z0[0], z0[0]);  // Nyquist bin k = L (Z[L] = Z[0])
     }
 }
 
@@ -771,8 +838,10 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
                 const int pair = plist[cur / T], tile = cur - (cur / T) * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
-                r2c_tile<R2, float2, NamedSync<kBarFFTB, NA>, NA, HINT == 2>(ring + b * BUF, twx, xtw,
-                                                                  a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tb, sync);
+                // the last spectral-state iteration's v is the solve's result: nothing reads its spectrum
+                if (!((MODE == X_SS || MODE == X_SSN) && a.ss_last))
+                    r2c_tile<R2, float2, NamedSync<kBarFFTB, NA>, NA, HINT == 2>(
+                        ring + b * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tb, sync);
                 if (i + NB <= n_tiles) ring_bar<kBarF, NF, true>(b);  // slot i + NB (a tile or the end marker) reuses b
             }
         }
@@ -802,7 +871,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
                 const int pair = plist[prev / T], tile = prev - (prev / T) * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
-                if (!DREG_SKIP(a, 1))
+                if (!DREG_SKIP(a, 1) && !((MODE == X_SS || MODE == X_SSN) && a.ss_last))
                     r2c_tile<R2, float2, NamedSync<kBarFFT, NF>, NF>(ring + pb * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl,
                                  tid, sync);
                 sync();  // buffer pb is restaged next round by this group
