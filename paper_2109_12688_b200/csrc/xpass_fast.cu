@@ -1102,8 +1102,7 @@ cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t
     // M = 256 (config 5): a tile is 99 KB, so the ring has two buffers; the point-wise group's
     // 100 B/voxel stream is the long stage and covers the later restaging (DREG_PIPE256=0: one tile per CTA)
     if (mode == X_GENERAL && a.pipe && a.pipe256 && !a.precise && a.F.M == 256 && !l1)
-        return a.pipe256 == 2 ? launch_pipe_t<2, 16, 12, 4, 1, 4, 0, X_GENERAL, 2, 1>(a, npairs, s)
-                              : launch_pipe_t<2, 16, 8, 4, 1, 4, 0, X_GENERAL, 2, 1>(a, npairs, s);
+        return launch_pipe_t<2, 16, 8, 4, 1, 4, 0, X_GENERAL, 2, 1>(a, npairs, s);
     switch (mode) {
         case X_FIRST: return l1 ? launch_fast_r<X_FIRST, 1>(a, npairs, s) : launch_fast_r<X_FIRST, 2>(a, npairs, s);
         case X_SECOND: return l1 ? launch_fast_r<X_SECOND, 1>(a, npairs, s) : launch_fast_r<X_SECOND, 2>(a, npairs, s);
