@@ -742,7 +742,7 @@ static cudaError_t launch_reg(const PArgs& a, int mode, int npairs, cudaStream_t
     return cudaGetLastError();
 }
 
-#define DREG_REG_CASES(X) X(64, 64) X(64, 128) X(128, 64) X(128, 128)
+#define DREG_REG_CASES(X) X(64, 32) X(128, 32) X(64, 64) X(64, 128) X(128, 64) X(128, 128)
 
 bool plane_reg_supported(int Ny, int Nz) {
 #define X(a, b) if (Ny == a && Nz == b) return true;

@@ -272,7 +272,7 @@ __device__ __forceinline__ float kn_pow(float base, int order) {
 template <int NY, int NZ, int R1Z, int MODE, int ORD, int MINB = ((NY * NZ <= 8192) ? 3 : 1), int UPF = 4>
 __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), MINB) plane_reg_kernel(PArgs a) {
     constexpr int R2Y = NY / 8, R2Z = NZ / R1Z, NT = R2Y * R2Z;
-    static_assert(R2Y <= 16 && R2Z <= 16 && (R1Z == 4 || R1Z == 8), "radix split outside rdft<>");
+    static_assert(R2Y <= 16 && R2Z <= 16 && (R1Z == 2 || R1Z == 4 || R1Z == 8), "radix split outside rdft<>");
     using Lay = PlaneLayout<NY, R2Y>;
     const int pair = blockIdx.y;
     if (a.pf_ahead && threadIdx.x == 0) {
