@@ -291,6 +291,26 @@ struct Geometry {
         fast = plane_fast_supported(Ny, Nz) ? env_int("DREG_FAST_PLANE", 3) : 0;
         if (fast >= 2 && !plane_reg_supported(Ny, Nz)) fast = 1;
         prefetch = env_int("DREG_PREFETCH", 0);
+        if (!fast && plane_cluster_fast_supported(Ny, Nz)) {
+            // position tables of the cluster plane kernel's splits (y: 16 x Ny/16, z: Nz/16 x 16)
+            auto split2 = [](int n, int r1) {
+                AxisPlan q{};
+                q.n = n;
+                q.nst = 2;
+                q.radix[0] = r1;
+                q.radix[1] = n / r1;
+                q.n1[0] = q.radix[1];
+                q.n1[1] = 1;
+                return q;
+            };
+            const AxisPlan fy = split2(Ny, 16), fz = split2(Nz, Nz / 16);
+            s.assign(Ny, 0.f);
+            for (int pos = 0; pos < Ny; ++pos) s[pos] = one_minus_cos(freq_of_pos(fy, pos), Ny);
+            up(sy_fast, s);
+            s.assign(Nz, 0.f);
+            for (int pos = 0; pos < Nz; ++pos) s[pos] = one_minus_cos(freq_of_pos(fz, pos), Nz);
+            up(sz_fast, s);
+        }
         if (fast) {
             // tables for the two-stage split R1 x R2 of the specialised kernel
             auto split = [](int n, int r1) {
@@ -735,7 +755,7 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     // an L2 prefetch of the x-pass state instead thrashed L2: +38%)
     p.pf_ahead = env_int("DREG_PLANE_PF", 1);
     p.ss_variant = env_int("DREG_PLANE_SS", 0);
-    p.cluster = env_int("DREG_CLUSTER", 0);  // opt-in: correct, but slower than the 3-pass split so far
+    p.cluster = env_int("DREG_CLUSTER", 1);  // 1: register-blocked cluster kernel where it applies; 2: generic; 0: split
     p.ss_prefetch = env_int("DREG_PLANE_UPF", 1);
     p.ss_stream = env_int("DREG_PLANE_STREAM", 1);
     p.order = sp.order;

@@ -115,6 +115,7 @@ bool plane_reg_supported(int Ny, int Nz);
 // three-pass plane for planes above one CTA's shared memory (plane_split.cu)
 bool plane_split_needed(const PArgs& a);
 bool plane_cluster_eligible(const PArgs& a);
+bool plane_cluster_fast_supported(int Ny, int Nz);
 cudaError_t launch_plane_cluster(const PArgs& a, int npairs, cudaStream_t s);
 cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);

@@ -653,8 +653,9 @@ def test_pipelined_xpass_bit_identical_to_one_tile_kernel(shape):
 
 
 def test_cluster_plane_kernel_matches_split_path():
-    """The opt-in 2-CTA cluster / DSMEM plane kernel (plane_cluster.cu, DREG_CLUSTER=1) computes the
-    same w-update as the 3-pass split on the config-5 plane (256 x 192) within fp32 rounding."""
+    """The 2-CTA cluster / DSMEM plane kernels (plane_cluster.cu: DREG_CLUSTER=1 register-blocked, the
+    default on the config-5 plane; 2 generic) compute the same w-update as the 3-pass split
+    (DREG_CLUSTER=0) on the config-5 plane (256 x 192) within fp32 rounding."""
     import subprocess
     import sys
 
@@ -672,15 +673,17 @@ def test_cluster_plane_kernel_matches_split_path():
 
     outs = []
     with tempfile.TemporaryDirectory() as td:
-        for flag in ("0", "1"):
+        for flag in ("0", "1", "2"):  # 3-pass split, register-blocked cluster kernel, generic cluster kernel
             path = os.path.join(td, f"w{flag}.npy")
             r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, DREG_CLUSTER=flag),
                                capture_output=True, text=True, timeout=600)
             assert r.returncode == 0, r.stderr[-2000:]
             outs.append(np.load(path))
     scale = float(np.abs(outs[0]).max())
-    print(f"cluster vs split w-update: max-abs {max_abs(outs[1], outs[0]):.3e} (max|w| {scale:.3f})")
+    print(f"cluster vs split w-update: max-abs {max_abs(outs[1], outs[0]):.3e} / {max_abs(outs[2], outs[0]):.3e} "
+          f"(max|w| {scale:.3f})")
     assert max_abs(outs[1], outs[0]) <= 1e-5 * scale
+    assert max_abs(outs[2], outs[0]) <= 1e-5 * scale
 
 
 # ---- spectral-state iteration (plane_fast.cuh MODE 2 + X_SS / X_SSN) -------------------
