@@ -184,6 +184,7 @@ struct Geometry {
     DevArray<double2> twx64, xtw64, twy64, twz64;  // precise-mode tables
     DevArray<double> sx64, sy64, sz64;
     DevArray<double> cx64, cy64, cz64;  // reference axis cosines for the precise multiplier
+    DevArray<double> cy64_fast, cz64_fast;  // ... at the cluster plane kernel's positions
     int fast = 0, prefetch = 1;
     size_t xsmem = 0, psmem = 0;
 
@@ -285,6 +286,25 @@ struct Geometry {
             sd.assign(Nz, 0.0);
             for (int pos = 0; pos < Nz; ++pos) sd[pos] = cos_ref(freq_of_pos(pz, pos), Nz);
             up(cz64, sd);
+            if (plane_cluster_fast64_supported(Ny, Nz)) {  // splits y: 16 x Ny/16, z: Nz/16 x 16
+                auto split2 = [](int n, int r1) {
+                    AxisPlan q{};
+                    q.n = n;
+                    q.nst = 2;
+                    q.radix[0] = r1;
+                    q.radix[1] = n / r1;
+                    q.n1[0] = q.radix[1];
+                    q.n1[1] = 1;
+                    return q;
+                };
+                const AxisPlan fy = split2(Ny, 16), fz = split2(Nz, Nz / 16);
+                sd.assign(Ny, 0.0);
+                for (int pos = 0; pos < Ny; ++pos) sd[pos] = cos_ref(freq_of_pos(fy, pos), Ny);
+                up(cy64_fast, sd);
+                sd.assign(Nz, 0.0);
+                for (int pos = 0; pos < Nz; ++pos) sd[pos] = cos_ref(freq_of_pos(fz, pos), Nz);
+                up(cz64_fast, sd);
+            }
         }
         // 1 = plane_fast_kernel; >= 2 (default 3) = register-blocked plane_reg_kernel where
         // it applies (first stages radix 8 on y and Nz / 16 on z, second stages in smem)
@@ -737,6 +757,8 @@ PArgs make_pargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     p.cx64 = w.geo.cx64.p;
     p.cy64 = w.geo.cy64.p;
     p.cz64 = w.geo.cz64.p;
+    p.cy64_fast = w.geo.cy64_fast.p;
+    p.cz64_fast = w.geo.cz64_fast.p;
     p.inv_count = 1.0 / (double)w.geo.N;
     p.F = w.fields(diag);
     p.py = w.geo.py;

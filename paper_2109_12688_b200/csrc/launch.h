@@ -82,6 +82,8 @@ struct PArgs {
     const double* cx64;
     const double* cy64;
     const double* cz64;
+    const double* cy64_fast;     // the same cosines at the cluster plane kernel's positions (precise, 128 x 128)
+    const double* cz64_fast;
     double inv_count;
     float lambda, theta, scale;  // scale = theta / voxels
     float lam_n, n_f;            // lambda N / theta and N: multiplier 1 / (lam_n K + n_f)
@@ -116,6 +118,7 @@ bool plane_reg_supported(int Ny, int Nz);
 bool plane_split_needed(const PArgs& a);
 bool plane_cluster_eligible(const PArgs& a);
 bool plane_cluster_fast_supported(int Ny, int Nz);
+bool plane_cluster_fast64_supported(int Ny, int Nz);
 cudaError_t launch_plane_cluster(const PArgs& a, int npairs, cudaStream_t s);
 cudaError_t launch_plane_split(const PArgs& a, int mode, int npairs, cudaStream_t s);
 cudaError_t launch_xpass(const XArgs& a, int mode, int npairs, cudaStream_t s);

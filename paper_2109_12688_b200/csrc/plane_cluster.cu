@@ -175,21 +175,27 @@ __device__ __forceinline__ void dft12(float2* x) {
     }
 }
 
-template <bool INV, int R>
-__device__ __forceinline__ void rdftz(float2* x) {
+template <bool INV, int R, class C>
+__device__ __forceinline__ void rdftz(C* x) {
     if constexpr (R == 12) dft12<INV>(x);
     else rdft<INV, R>(x);
 }
 
 constexpr int kFT2 = 512;
 
-template <int NY, int NZ>
+// C = double2 is the precise mode (config 4: 128 x 128 planes): fp64 spectrum storage, butterflies
+// and twiddles, and the reference's own multiplier expression (admm.cpp:92, regularizer.cpp:69-76,
+// no contraction) from its axis cosines at this kernel's digit-reversed positions.
+template <int NY, int NZ, class C>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_cluster_fast_kernel(PArgs a) {
+    using R = typename CT<C>::R;
+    constexpr bool F64 = sizeof(C) == 16;
     constexpr int R1Y = 16, R2Y = NY / 16, R1Z = NZ / 16, R2Z = 16, ZH = NZ / 2, YH = NY / 2;
     constexpr int PR = NY + NY / R2Y + 4;
     static_assert(R2Y == 16 || R2Y == 8, "y second stage radix");
     static_assert(R1Z == 12 || R1Z == 8 || R1Z == 16, "z first stage radix");
     static_assert(ZH % R2Z == 0, "z blocks must not straddle the two CTAs");
+    static_assert(!F64 || R1Z != 12, "dft12 is fp32 only");
     const int pair = blockIdx.z;
     const PairState* st = a.F.st + pair;
     if (!st->active || st->status) return;  // both CTAs of the cluster leave together
@@ -198,45 +204,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     cg::cluster_group cluster = cg::this_cluster();
     const int r = (int)cluster.block_rank();
     extern __shared__ __align__(16) unsigned char smem[];
-    float2* buf = reinterpret_cast<float2*>(smem);  // [ZH][PR]
-    float2* twy = buf + ZH * PR;
-    float2* twz = twy + NY;
-    float* sys = reinterpret_cast<float*>(twz + NZ);
-    float* szs = sys + NY;
-    float2* peer = cluster.map_shared_rank(buf, r ^ 1);
+    C* buf = reinterpret_cast<C*>(smem);  // [ZH][PR]
+    C* twy = buf + ZH * PR;
+    C* twz = twy + NY;
+    R* sys = reinterpret_cast<R*>(twz + NZ);  // fp32: doubled 1 - cos tables; fp64: the reference's axis cosines
+    R* szs = sys + NY;
+    C* peer = cluster.map_shared_rank(buf, r ^ 1);
     const int tid = threadIdx.x;
     const int hx = a.F.hx;
     const int plane = blockIdx.y;
     const int p = plane - (plane / hx) * hx;
-    float2* Sp = a.F.S + ((size_t)pair * 3 * hx + plane) * (size_t)a.F.lines + (size_t)(r * ZH) * NY;
+    C* Sp = spectrum_of<C>(a.F, pair) + (size_t)plane * (size_t)a.F.lines + (size_t)(r * ZH) * NY;
     auto at = [](int zl, int y) { return zl * PR + y + y / R2Y; };
     if (a.pf_ahead && tid == 0) {
         // L2-prefetch the half-plane the cluster that takes over these two SMs will load
         // (clusters are dispatched in linear (plane, pair) order, one wave = pf_ahead clusters)
         const unsigned lin = blockIdx.z * gridDim.y + blockIdx.y + (unsigned)a.pf_ahead;
         if (lin < gridDim.y * gridDim.z) {
-            const float2* nxt = a.F.S + (size_t)lin * (size_t)a.F.lines + (size_t)(r * ZH) * NY;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"((unsigned)(ZH * NY * 8)) : "memory");
+            const C* nxt = spectrum_of<C>(a.F, 0) + (size_t)lin * (size_t)a.F.lines + (size_t)(r * ZH) * NY;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"((unsigned)(ZH * NY * sizeof(C))) : "memory");
         }
     }
 
     for (int i = tid; i < NY; i += kFT2) {
-        twy[i] = a.twy[i];
-        sys[i] = 2.0f * a.sy_fast[i];
+        if constexpr (F64) {
+            twy[i] = a.twy64[i];
+            sys[i] = a.cy64_fast[i];
+        } else {
+            twy[i] = a.twy[i];
+            sys[i] = 2.0f * a.sy_fast[i];
+        }
     }
     for (int i = tid; i < NZ; i += kFT2) {
-        twz[i] = a.twz[i];
-        szs[i] = 2.0f * a.sz_fast[i];
+        if constexpr (F64) {
+            twz[i] = a.twz64[i];
+            szs[i] = a.cz64_fast[i];
+        } else {
+            twz[i] = a.twz[i];
+            szs[i] = 2.0f * a.sz_fast[i];
+        }
     }
+    __syncthreads();
     // Y1: global -> radix 16 over t (stride R2Y) -> twiddle W_NY^(j1 k) -> shared
     for (int w = tid; w < ZH * R2Y; w += kFT2) {
         const int j1 = w % R2Y, row = w / R2Y;
-        float2 x[R1Y];
+        C x[R1Y];
 #pragma unroll
         for (int t = 0; t < R1Y; ++t) x[t] = __ldcs(Sp + row * NY + j1 + R2Y * t);
         rdft<false, R1Y>(x);
 #pragma unroll
-        for (int k = 1; k < R1Y; ++k) x[k] = cmul(x[k], __ldg(a.twy + j1 * k));
+        for (int k = 1; k < R1Y; ++k) x[k] = cmul(x[k], twy[j1 * k]);
 #pragma unroll
         for (int k = 0; k < R1Y; ++k) buf[at(row, j1 + R2Y * k)] = x[k];
     }
@@ -244,7 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     // Y2: radix R2Y on contiguous blocks
     for (int w = tid; w < ZH * R1Y; w += kFT2) {
         const int blk = w % R1Y, row = w / R1Y;
-        float2 v[R2Y];
+        C v[R2Y];
 #pragma unroll
         for (int e = 0; e < R2Y; ++e) v[e] = buf[at(row, blk * R2Y + e)];
         rdft<false, R2Y>(v);
@@ -255,7 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     // Z1: radix R1Z over rows j1 + 16 t; rows of the other half are the peer's (DSMEM), in place
     for (int w = tid; w < YH * R2Z; w += kFT2) {
         const int y = r * YH + w % YH, j1 = w / YH;
-        float2 x[R1Z];
+        C x[R1Z];
 #pragma unroll
         for (int t = 0; t < R1Z; ++t) {
             const int z = j1 + R2Z * t;  // t < R1Z / 2 <=> z < ZH: owner 0
@@ -273,22 +290,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     cluster.sync();
     // Z2 on the local blocks (R1Z / 2 of them): radix 16, multiplier, adjoint radix 16
     {
-        const float sxp = 2.0f * __ldg(a.sx + p);
-        const float lam_n = a.lam_n, n_f = a.n_f;
         const int order = a.order;
         for (int w = tid; w < NY * (R1Z / 2); w += kFT2) {
             const int y = w % NY, bl = w / NY;
-            float2 v[R2Z];
+            C v[R2Z];
 #pragma unroll
             for (int e = 0; e < R2Z; ++e) v[e] = buf[at(bl * R2Z + e, y)];
             rdft<false, R2Z>(v);
-            const float sxy = sxp + sys[y];
             const int zp0 = (r * (R1Z / 2) + bl) * R2Z;
+            if constexpr (F64) {
+                const double lam = a.lambda64, th = a.theta64, cxp = a.cx64[p], cyp = sys[y];
 #pragma unroll
-            for (int e = 0; e < R2Z; ++e) {
-                // theta / (lambda (2 s)^n + theta) / N = 1 / ((lambda N / theta) K_n + N) (regularizer.cpp:69-73)
-                const float K = kn_pow<0>(sxy + szs[zp0 + e], order);
-                v[e] = cscale(v[e], rcp_nr(fmaf(lam_n, K, n_f)));
+                for (int e = 0; e < R2Z; ++e) {
+                    const double yz = __dsub_rn(__dsub_rn(3.0, cyp), szs[zp0 + e]);
+                    const double base = __dmul_rn(2.0, __dsub_rn(yz, cxp));
+                    double K = base;
+                    for (int q = 1; q < order; ++q) K = __dmul_rn(K, base);
+                    const double m = __dmul_rn(__ddiv_rn(th, __dadd_rn(__dmul_rn(lam, K), th)), a.inv_count);
+                    v[e] = CT<C>::make(__dmul_rn(v[e].x, m), __dmul_rn(v[e].y, m));
+                }
+            } else {
+                const float sxy = 2.0f * __ldg(a.sx + p) + sys[y];
+                const float lam_n = a.lam_n, n_f = a.n_f;
+#pragma unroll
+                for (int e = 0; e < R2Z; ++e) {
+                    // theta / (lambda (2 s)^n + theta) / N = 1 / ((lambda N / theta) K_n + N) (regularizer.cpp:69-73)
+                    const float K = kn_pow<0>(sxy + szs[zp0 + e], order);
+                    const float m = rcp_nr(fmaf(lam_n, K, n_f));
+                    v[e] = CT<C>::make(v[e].x * m, v[e].y * m);
+                }
             }
             rdft<true, R2Z>(v);
 #pragma unroll
@@ -299,7 +329,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     // Z1 adjoint
     for (int w = tid; w < YH * R2Z; w += kFT2) {
         const int y = r * YH + w % YH, j1 = w / YH;
-        float2 x[R1Z];
+        C x[R1Z];
 #pragma unroll
         for (int k = 0; k < R1Z; ++k) {
             const int z = j1 + R2Z * k;
@@ -318,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     // Y2 adjoint
     for (int w = tid; w < ZH * R1Y; w += kFT2) {
         const int blk = w % R1Y, row = w / R1Y;
-        float2 v[R2Y];
+        C v[R2Y];
 #pragma unroll
         for (int e = 0; e < R2Y; ++e) v[e] = buf[at(row, blk * R2Y + e)];
         rdft<true, R2Y>(v);
@@ -329,7 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     // Y1 adjoint, straight to global
     for (int w = tid; w < ZH * R2Y; w += kFT2) {
         const int j1 = w % R2Y, row = w / R2Y;
-        float2 x[R1Y];
+        C x[R1Y];
 #pragma unroll
         for (int k = 0; k < R1Y; ++k) x[k] = buf[at(row, j1 + R2Y * k)];
 #pragma unroll
@@ -340,12 +370,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFT2, 1) plane_clust
     }
 }
 
+// fp32: config 5's 256 x 192 plane; precise (fp64): config 4's 128 x 128 plane
 bool plane_cluster_fast_supported(int Ny, int Nz) { return Ny == 256 && Nz == 192; }
+bool plane_cluster_fast64_supported(int Ny, int Nz) { return Ny == 128 && Nz == 128; }
 
-static cudaError_t launch_plane_cluster_fast(const PArgs& a, int npairs, cudaStream_t s) {
-    constexpr int NY = 256, NZ = 192;
-    constexpr size_t smem = sizeof(float2) * ((NZ / 2) * (NY + NY / 16 + 4) + NY + NZ) + sizeof(float) * (NY + NZ);
-    cudaError_t e = cudaFuncSetAttribute(plane_cluster_fast_kernel<NY, NZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int NY, int NZ, class C>
+static cudaError_t launch_plane_cluster_fast_t(const PArgs& a, int npairs, cudaStream_t s) {
+    using R = typename CT<C>::R;
+    constexpr size_t smem = sizeof(C) * ((NZ / 2) * (NY + NY / (NY / 16) + 4) + NY + NZ) + sizeof(R) * (NY + NZ);
+    cudaError_t e = cudaFuncSetAttribute(plane_cluster_fast_kernel<NY, NZ, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     PArgs b = a;
@@ -355,8 +388,13 @@ static cudaError_t launch_plane_cluster_fast(const PArgs& a, int npairs, cudaStr
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         b.pf_ahead = b.pf_ahead * (sms / 2);
     }
-    plane_cluster_fast_kernel<NY, NZ><<<dim3(2, (unsigned)(3 * a.F.hx), (unsigned)npairs), kFT2, smem, s>>>(b);
+    plane_cluster_fast_kernel<NY, NZ, C><<<dim3(2, (unsigned)(3 * a.F.hx), (unsigned)npairs), kFT2, smem, s>>>(b);
     return cudaGetLastError();
+}
+
+static cudaError_t launch_plane_cluster_fast(const PArgs& a, int npairs, cudaStream_t s) {
+    if (a.precise) return launch_plane_cluster_fast_t<128, 128, double2>(a, npairs, s);
+    return launch_plane_cluster_fast_t<256, 192, float2>(a, npairs, s);
 }
 
 static size_t cluster_smem(int Ny, int Nz) {
@@ -367,8 +405,12 @@ static size_t cluster_smem(int Ny, int Nz) {
 
 bool plane_cluster_eligible(const PArgs& a) {
     const int Ny = a.F.Ny, Nz = a.F.Nz;
-    if (a.precise || !a.cluster || Ny % 2 || Nz % 2) return false;
-    if (a.cluster == 1) return plane_cluster_fast_supported(Ny, Nz) && a.sy_fast && a.sz_fast;  // 2 = the generic version
+    if (!a.cluster || Ny % 2 || Nz % 2) return false;
+    if (a.cluster == 1) {  // register-blocked versions; 2 = the generic one
+        if (a.precise) return plane_cluster_fast64_supported(Ny, Nz) && a.cy64_fast && a.cz64_fast && a.F.S64;
+        return plane_cluster_fast_supported(Ny, Nz) && a.sy_fast && a.sz_fast;
+    }
+    if (a.precise) return false;
     if ((size_t)(Nz / 2) * Ny > (size_t)kCT * kCE) return false;
     return cluster_smem(Ny, Nz) <= 227 * 1024;
 }
