@@ -1055,22 +1055,13 @@ static cudaError_t launch_fast_ss(const XArgs& a, int npairs, cudaStream_t s) {
 // warps * 100 + VEC * 10 + unroll)
 template <int R2, int MODE>
 static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
-    switch (a.pipe_ss) {
+    switch (a.pipe_ss) {  // the measured alternatives (profiles/r2c_ss_sweep.md); the rest of the sweep was dropped
         case 3: return launch_fast_ss<MODE, R2, 2, 2, 3>(a, npairs, s);  // one tile per CTA, 3 CTAs per SM
-        case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);
-        // split FFT groups (c2r group / r2c group)
-        case 1120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE, 3, 1, true>(a, npairs, s);
-        case 1120861: return launch_pipe_t<2, R2, 8, 4, 1, 12, 2, MODE, 3, 1, true>(a, npairs, s);  // streaming hints
-        case 1120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE, 3, 1, true>(a, npairs, s);
-        case 120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);
-        // two CTAs per SM, two tile buffers each
-        case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);
-        case 2040442: return launch_pipe_t<2, R2, 4, 4, 2, 4, 0, MODE, 2, 2>(a, npairs, s);
-        case 120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE>(a, npairs, s);
-        case 120842: return launch_pipe_t<2, R2, 8, 4, 2, 12, 0, MODE>(a, npairs, s);
-        // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each;
-        // 4 point-wise warps with two iterations of loads in flight keep up with 16 B/voxel
-        // split groups: 6 c2r + 6 r2c warps, 8 point-wise warps (1120841)
+        case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);   // 8 FFT + 8 point-wise warps
+        case 120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);  // 12 FFT + 4 point-wise, unsplit
+        case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);  // two CTAs per SM, two buffers each
+        // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each; split
+        // into a c2r group and an r2c group (6 + 6) beside 8 point-wise warps: 1120841
         default: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
     }
 }
