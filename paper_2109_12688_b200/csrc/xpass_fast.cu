@@ -699,8 +699,13 @@ __global__ void __launch_bounds__(kFT, (sizeof(C) == 8) ? MINB : 2) xpass_fast_k
 // a run of consecutive tiles of one pair are reduced once per run (fp64 per-thread sums,
 // fixed tree) and the pair's ticket counts tiles, so the per-pair totals are
 // deterministic for a given SM count.
-constexpr int kBarFFT = 1, kBarPW = 2, kBarW = 3, kBarU = 6;  // W/U use NB ids each (NB <= 3)
-constexpr int kBarFFTB = 9, kBarF = 10;  // split FFT groups: the r2c group's barrier and FREE(b)
+// Named barriers: 1 = FFT (c2r) group, 2 = point-wise group, then NB ids each for W and U, one for
+// the r2c group of the split form and NB for FREE -- 4 + 3 NB <= 16 ids, so the ring holds at most 4 tiles.
+constexpr int kBarFFT = 1, kBarPW = 2, kBarW = 3;
+template <int NB> struct RingBars {
+    static constexpr int U = kBarW + NB, FFTB = kBarW + 2 * NB, F = kBarW + 2 * NB + 1;
+    static_assert(F + NB <= 16, "named barrier ids");
+};
 
 // named barrier base + b with a compile-time id (a run-time id makes ptxas reserve all 16)
 template <int BASE, int N, bool ARRIVE>
@@ -711,7 +716,8 @@ __device__ __forceinline__ void ring_bar(int b) {
     switch (b) {
         case 0: DREG_RB(BASE + 0) break;
         case 1: DREG_RB(BASE + 1) break;
-        default: DREG_RB(BASE + 2) break;
+        case 2: DREG_RB(BASE + 2) break;
+        default: DREG_RB(BASE + 3) break;
     }
 #undef DREG_RB
 }
@@ -728,7 +734,8 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
     constexpr int L = kR1 * R2, HX = L + 1, PM = L + 1, TL = kFTL;
     constexpr int BUF = 3 * TL * PM;
     constexpr int NF = 32 * FW, NTP = 32 * NPW, NALL = NF + NTP;
-    static_assert(NB == 3 || NB == 2, "ring of three (or two) tile buffers");
+    static_assert(NB == 3 || NB == 2 || (NB == 4 && SPLIT), "ring of three tile buffers (two: unsplit; four: split form)");
+    constexpr int kBarU = RingBars<NB>::U, kBarFFTB = RingBars<NB>::FFTB, kBarF = RingBars<NB>::F;
     extern __shared__ __align__(16) unsigned char smem[];
     float2* ring = reinterpret_cast<float2*>(smem);  // [NB][3][TL][PM]
     float2* twx = ring + NB * BUF;
@@ -790,7 +797,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
     };
 
     if (SPLIT && fft_group) {
-        static_assert(!SPLIT || (NB == 3 && FW % 2 == 0), "split FFT groups: ring of three, even warp count");
+        static_assert(!SPLIT || ((NB == 3 || NB == 4) && FW % 2 == 0), "split FFT groups: ring of three or four, even warp count");
         constexpr int NA = NF / 2;  // threads per FFT sub-group
         // W: c2r group arrives, point-wise waits; U: point-wise arrives, r2c group waits
         if (tid < NA) {
@@ -1060,6 +1067,8 @@ static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
         case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);   // 8 FFT + 8 point-wise warps
         case 120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);  // 12 FFT + 4 point-wise, unsplit
         case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);  // two CTAs per SM, two buffers each
+        case 41120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 4, 1, true>(a, npairs, s);  // ring of four tiles
+        case 1240841: return launch_pipe_t<2, R2, 8, 4, 1, 24, 0, MODE, 3, 1, true>(a, npairs, s);  // 12 + 12 FFT, 8 point-wise
         // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each; split
         // into a c2r group and an r2c group (6 + 6) beside 8 point-wise warps: 1120841
         default: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);

@@ -1,0 +1,7 @@
+#!/bin/bash
+O=gpurun_out/ss18; mkdir -p $O
+timeout 200 env DREG_PIPE_SS=41120841 python tools/phi_digest.py 4 > $O/digest_nb4.txt 2>&1 || { echo "nb4 failed/hung" >> $O/digest_nb4.txt; }
+python tools/phi_digest.py 4 > $O/digest.txt 2>&1
+for V in "DREG_SS=1" "DREG_PIPE_SS=41120841" "DREG_PIPE_SS=41120842" "DREG_PIPE_SS=41240841"; do
+  env ${V//,/ } timeout 300 python bench.py --no-cpu --no-e2e --allow-env --steps 3 --warmup 3 --pairs ${PAIRS:-128} > $O/bench_$V.json 2> $O/bench_$V.err
+done
