@@ -7,7 +7,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err
 for C in 1 2 4 5; do
-  timeout 600 python bench.py --config $C --steps 3 --warmup 3 > $O/bench_config$C.json 2> $O/bench_config$C.err
+  timeout 600 python bench.py --config $C --steps 10 --warmup 5 > $O/bench_config$C.json 2> $O/bench_config$C.err
 done
 if [ "${NCU:-1}" = 1 ]; then
 CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --pairs 32"
