@@ -736,7 +736,7 @@ XArgs make_xargs(const Workspace& w, const SolverParams& sp, bool diag, bool pre
     a.fx_variant = env_int("DREG_FX", 22);
     a.pipe = env_int("DREG_PIPE", 1);
     a.pipe_all = env_int("DREG_PIPE_ALL", 0);
-    a.pipe_ss = env_int("DREG_PIPE_SS", 1120841);
+    a.pipe_ss = env_int("DREG_PIPE_SS", 1120444);
     a.pipe256 = env_int("DREG_PIPE256", 1);
     if (precise) a.TL = w.geo.TLp;
     a.fd_lines.init((unsigned)(3 * a.TL));

@@ -254,16 +254,18 @@ __device__ __forceinline__ void c2r_tile(C* buf, const C* twx, const C* xtw, int
 // phase 2: point-wise ADMM updates (fp32) of one tile; accumulates change / residual /
 // data-term partials of this thread.
 template <int MODE, int DT, int R2, int VEC, int UNR, class C, int NTP = kFT, int HINT = 0>
-__device__ __forceinline__ void pointwise_tile(const XArgs& a, C* buf, int pair, long long L0, int nl, int tid,
+__device__ __forceinline__ void pointwise_tile(const XArgs& a, C* __restrict__ buf, int pair, long long L0, int nl, int tid,
                                                float& fc, float& fr, float& fo) {
     constexpr int L = kR1 * R2, PM = L + 1, M = 2 * L, TL = kFTL;
     const long long N = a.F.N;
-    float* V = a.F.V + (size_t)pair * 3 * N;
-    float* BO = a.F.BH + (size_t)pair * 3 * N;  // b_{k-2} in, b_k out (the dual iterates ping-pong)
-    float* WP = a.F.WP + (size_t)pair * 3 * N;
-    const float* BP = a.F.BP + (size_t)pair * 3 * N;  // b_{k-1}
-    const float* G = a.F.G + (size_t)pair * 3 * N;
-    const float* Dd = a.F.D + (size_t)pair * N;
+    // the field arrays and the shared-memory tile never alias: __restrict__ lets the unrolled loop
+    // hoist the next iteration's global loads above this iteration's shared-memory stores
+    float* __restrict__ V = a.F.V + (size_t)pair * 3 * N;
+    float* __restrict__ BO = a.F.BH + (size_t)pair * 3 * N;  // b_{k-2} in, b_k out (the dual iterates ping-pong)
+    float* __restrict__ WP = a.F.WP + (size_t)pair * 3 * N;
+    const float* __restrict__ BP = a.F.BP + (size_t)pair * 3 * N;  // b_{k-1}
+    const float* __restrict__ G = a.F.G + (size_t)pair * 3 * N;
+    const float* __restrict__ Dd = a.F.D + (size_t)pair * N;
     const float thf = (float)a.sp.theta, ithf = (float)(1.0 / a.sp.theta), epsf = (float)a.sp.epsilon;
     const float cf = (float)a.coef, cpf = (float)a.coef_prev;
     const bool accel = a.sp.accelerate != 0;
@@ -808,7 +810,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
                 const int pair = plist[g / T], tile = g - (g / T) * T;
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
-                stage_spectrum<R2, float2, NA>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
+                if (!DREG_SKIP(a, 4)) stage_spectrum<R2, float2, NA>(buf, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tid);
                 asm volatile("cp.async.commit_group;" ::: "memory");
             };
             int cur = runnable_from(range_start(blockIdx.x));
@@ -819,7 +821,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
                 if (cur >= 0) {
                     asm volatile("cp.async.wait_group 0;" ::: "memory");
                     sync();
-                    c2r_tile<R2, float2, NamedSync<kBarFFT, NA>, NA>(ring + b * BUF, twx, xtw, tid, sync);
+                    if (!DREG_SKIP(a, 1)) c2r_tile<R2, float2, NamedSync<kBarFFT, NA>, NA>(ring + b * BUF, twx, xtw, tid, sync);
                 }
                 if (tid == 0) tile_of[b] = cur;
                 ring_bar<kBarW, NA + NTP, true>(b);
@@ -846,7 +848,7 @@ __global__ void __launch_bounds__(32 * (FW + NPW), MINB) xpass_pipe_kernel(XArgs
                 const long long L0 = (long long)tile * TL;
                 const int nl = (int)min((long long)TL, lines - L0);
                 // the last spectral-state iteration's v is the solve's result: nothing reads its spectrum
-                if (!((MODE == X_SS || MODE == X_SSN) && a.ss_last))
+                if (!((MODE == X_SS || MODE == X_SSN) && a.ss_last) && !DREG_SKIP(a, 1))
                     r2c_tile<R2, float2, NamedSync<kBarFFTB, NA>, NA, HINT == 2>(
                         ring + b * BUF, twx, xtw, a.F.S + (size_t)pair * 3 * HX * lines, lines, L0, nl, tb, sync);
                 if (i + NB <= n_tiles) ring_bar<kBarF, NF, true>(b);  // slot i + NB (a tile or the end marker) reuses b
@@ -1040,6 +1042,7 @@ static cudaError_t launch_pipe_r(const XArgs& a, int npairs, cudaStream_t s) {
     switch (a.pipe) {  // FFT warps * 10000 + point-wise warps * 100 + VEC * 10 + unroll
         case 80841: return launch_pipe_t<DT, R2, 8, 4, 1, 8>(a, npairs, s);
         case 41221: return launch_pipe_t<DT, R2, 12, 2, 1, 4>(a, npairs, s);
+        case 40842: return launch_pipe_t<DT, R2, 8, 4, 2, 4>(a, npairs, s);
         default: return launch_pipe_t<DT, R2, 8, 4, 1, 4>(a, npairs, s);  // 40841: measured best at M = 128
     }
 }
@@ -1067,11 +1070,13 @@ static cudaError_t launch_pipe_ss(const XArgs& a, int npairs, cudaStream_t s) {
         case 80841: return launch_pipe_t<2, R2, 8, 4, 1, 8, 0, MODE>(a, npairs, s);   // 8 FFT + 8 point-wise warps
         case 120442: return launch_pipe_t<2, R2, 4, 4, 2, 12, 0, MODE>(a, npairs, s);  // 12 FFT + 4 point-wise, unsplit
         case 2060242: return launch_pipe_t<2, R2, 2, 4, 2, 6, 0, MODE, 2, 2>(a, npairs, s);  // two CTAs per SM, two buffers each
+        case 1120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);  // split, 8 point-wise warps
         case 41120841: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 4, 1, true>(a, npairs, s);  // ring of four tiles
         case 1240841: return launch_pipe_t<2, R2, 8, 4, 1, 24, 0, MODE, 3, 1, true>(a, npairs, s);  // 12 + 12 FFT, 8 point-wise
-        // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each; split
-        // into a c2r group and an r2c group (6 + 6) beside 8 point-wise warps: 1120841
-        default: return launch_pipe_t<2, R2, 8, 4, 1, 12, 0, MODE, 3, 1, true>(a, npairs, s);
+        // 12 FFT warps cover a tile's 96 lines x 4 block pairs / 384 r2c tasks in one round each, split
+        // into a c2r group and an r2c group (6 + 6); 4 point-wise warps with four iterations of grad /
+        // diff loads in flight (the loop is unrolled 4x over __restrict__ pointers): 1120444
+        default: return launch_pipe_t<2, R2, 4, 4, 4, 12, 0, MODE, 3, 1, true>(a, npairs, s);
     }
 }
 
@@ -1102,7 +1107,8 @@ cudaError_t launch_xpass_fast(const XArgs& a, int mode, int npairs, cudaStream_t
     // M = 256 (config 5): a tile is 99 KB, so the ring has two buffers; the point-wise group's
     // 100 B/voxel stream is the long stage and covers the later restaging (DREG_PIPE256=0: one tile per CTA)
     if (mode == X_GENERAL && a.pipe && a.pipe256 && !a.precise && a.F.M == 256 && !l1)
-        return launch_pipe_t<2, 16, 8, 4, 1, 4, 0, X_GENERAL, 2, 1>(a, npairs, s);
+        return a.pipe256 == 2 ? launch_pipe_t<2, 16, 8, 4, 2, 4, 0, X_GENERAL, 2, 1>(a, npairs, s)  // two iterations of loads in flight
+                              : launch_pipe_t<2, 16, 8, 4, 1, 4, 0, X_GENERAL, 2, 1>(a, npairs, s);
     switch (mode) {
         case X_FIRST: return l1 ? launch_fast_r<X_FIRST, 1>(a, npairs, s) : launch_fast_r<X_FIRST, 2>(a, npairs, s);
         case X_SECOND: return l1 ? launch_fast_r<X_SECOND, 1>(a, npairs, s) : launch_fast_r<X_SECOND, 2>(a, npairs, s);
