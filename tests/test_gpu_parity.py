@@ -686,6 +686,63 @@ def test_cluster_plane_kernel_matches_split_path():
     assert max_abs(outs[2], outs[0]) <= 1e-5 * scale
 
 
+def test_cluster_plane_kernel_precise_matches_split_path():
+    """The fp64 instance of the cluster plane kernel (128 x 128 planes, precise mode: config 4) against
+    the generic fp64 3-pass split: same reference multiplier expression, fp64 transforms in a different
+    order -- the w-updates agree to ~1e-13 relative."""
+    import subprocess
+    import sys
+    import tempfile
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "from paper_2109_12688_b200 import abi, dreg\n"
+            "rng = np.random.default_rng(11)\n"
+            "v = rng.standard_normal((128, 128, 16, 3)).astype(np.float32)\n"
+            "b = rng.standard_normal((128, 128, 16, 3)).astype(np.float32)\n"
+            "cfg = abi.solver_cfg(data_term=2, order=3, lambda_=0.05, theta=0.5, max_iters=200)\n"
+            "with dreg.Context(0) as ctx:\n"
+            "    ctx.set_precision(2)\n"
+            "    w = ctx.w_update(v, b, cfg)\n"
+            "np.save(sys.argv[1], w)\n") % root
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for flag in ("0", "1"):
+            path = os.path.join(td, f"w{flag}.npy")
+            r = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, DREG_CLUSTER=flag),
+                               capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+    scale = float(np.abs(outs[0]).max())
+    print(f"precise cluster vs split w-update: max-abs {max_abs(outs[1], outs[0]):.3e} (max|w| {scale:.3f})")
+    assert max_abs(outs[1], outs[0]) <= 2e-7 * scale  # both round the same fp64 result to fp32
+
+
+def test_pipelined_xpass_m256_bit_identical_to_one_tile_kernel():
+    """M = 256: the pipelined x-pass with its two-buffer ring (DREG_PIPE256=1, default) and the
+    one-tile-per-CTA kernel give bit-identical phi."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
+            "from paper_2109_12688_b200 import abi, dreg, synth\n"
+            "F, M = synth.make_batch(3, 1000, 2, (6, 48, 256))\n"
+            "s = abi.solver_cfg(data_term=2, order=2, lambda_=0.1, theta=1.0, max_iters=12, tol=0.0, log_objective=False)\n"
+            "cfg = abi.reg_cfg(s, 1, (2,), (12,))\n"
+            "with dreg.Context(0) as ctx:\n"
+            "    phis, _, res = ctx.register_batch(list(F), list(M), cfg, want_warped=False)\n"
+            "h = hashlib.sha256(b''.join(np.ascontiguousarray(p).tobytes() for p in phis))\n"
+            "print(h.hexdigest(), [r.velocity_count for r in res])\n") % root
+    outs = []
+    for flag in ("0", "1"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, DREG_PIPE256=flag), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1], outs
+
+
 # ---- spectral-state iteration (plane_fast.cuh MODE 2 + X_SS / X_SSN) -------------------
 _SS_CODE = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r)\n"
             "from paper_2109_12688_b200 import dreg, synth\n"
