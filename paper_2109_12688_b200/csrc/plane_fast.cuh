@@ -278,10 +278,17 @@ __global__ void __launch_bounds__((NY / 8) * (NZ / R1Z), MINB) plane_reg_kernel(
     if (a.pf_ahead && threadIdx.x == 0) {
         // L2 prefetch of the plane the CTA starting about one wave later will load
         // (blocks are dispatched in linear order as resident slots free up)
-        const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x + (unsigned)a.pf_ahead;
+        // (a negative DREG_PLANE_PF prefetches unconditionally: the A/B knob for the check below)
+        const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x + (unsigned)(a.pf_ahead < 0 ? -a.pf_ahead : a.pf_ahead);
         if (lin < gridDim.x * gridDim.y) {
-            const float2* nxt = a.F.S + (size_t)lin * (size_t)a.F.lines;  // plane index pair*3*hx + c*hx + p
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"((unsigned)(NY * NZ * 8)) : "memory");
+            // only for a plane that will be transformed: the CTAs of finished pairs exit below, and a
+            // 64 KB prefetch from each of them made an all-finished launch cost 0.5 ms of HBM time
+            const PairState* ts = a.F.st + lin / gridDim.x;
+            const bool live = ts->active && !ts->status && !(ts->solve_done && (!a.need_tail || a.k > ts->done_iter));
+            if (live || a.pf_ahead < 0) {
+                const float2* nxt = a.F.S + (size_t)lin * (size_t)a.F.lines;  // plane index pair*3*hx + c*hx + p
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nxt), "r"((unsigned)(NY * NZ * 8)) : "memory");
+            }
         }
     }
     PairState* st = a.F.st + pair;
